@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the uneven-FSDP train step (BASELINE.json metric: train
+samples/s at 1/2/4/8 B200, emulated heterogeneous; uneven AG/RS bus GB/s in
+bench_collectives.py).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt2_small]
+  torchrun --nproc-per-node N ... bench.py --gpus N ...     (one rank per GPU)
+  python bench.py --impl reference ...                      (CPU reference arm)
+
+A step = one full Cephalo iteration (AG, layered fwd/bwd, weighted RS,
+AdamW) of the named config on N GPUs with global batch batch_per_gpu * N
+(weak scaling). Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2411_01075_b200 import hetstep as K  # noqa: E402
+from paper_2411_01075_b200.configs import CONFIGS, build_job  # noqa: E402
+from paper_2411_01075_b200.data import rank_tokens  # noqa: E402
+from paper_2411_01075_b200.step import AdamWConfig, UnevenFSDPTrainer  # noqa: E402
+
+SEED = 1234
+OPT = AdamWConfig()
+HBM_FALLBACK = 6650.0
+
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def setup_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def make_comms(world: int, rank: int):
+    if world == 1:
+        return None, None
+    ids = [K.unique_id(), K.unique_id()] if rank == 0 else [None, None]
+    dist.broadcast_object_list(ids, src=0)
+    return K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
+
+
+def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None) -> dict:
+    """The oracle step (torch CPU fp32, N simulated ranks in one process) on a
+    bounded sample of the same workload: `sample` global samples per step."""
+    from oracle import model_oracle as MO
+    from paper_2411_01075_b200.model import init_flat
+    cores = len(os.sched_getaffinity(0))
+    torch.set_num_threads(cores)
+    arch = job.arch
+    units = []
+    for u in range(arch.layers + 1):
+        g = torch.Generator().manual_seed(u)
+        units.append(init_flat(arch.root_layout() if u == arch.layers else arch.unit_layout(), g,
+                               "cpu"))
+    opt = dict(lr=OPT.lr, beta1=OPT.betas[0], beta2=OPT.betas[1], eps=OPT.eps,
+               weight_decay=OPT.weight_decay)
+    st = MO.CPUStep(arch, units[:-1], units[-1], opt)
+    sample = 2 if arch.d >= 512 else 8
+    # sample: the first `sample` global samples, split over two simulated ranks as m=1 each
+    micro = [(1, sample // 2), (1, sample - sample // 2)]
+    from paper_2411_01075_b200.data import tokens
+    done, t_total, n = 0, 0.0, 0
+    while True:
+        toks = tokens(np.arange(sample), arch.seq, arch.vocab, SEED, n)
+        parts = [toks[:micro[0][1]], toks[micro[0][1]:]]
+        t0 = time.perf_counter()
+        st.step(parts, micro)
+        t_total += time.perf_counter() - t0
+        done += sample
+        n += 1
+        if (steps is not None and n >= steps) or (steps is None and t_total >= max_seconds):
+            break
+    return {"value": done / t_total, "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{n} CPU steps x {sample} samples of {job.config.name} (seq {arch.seq}) "
+                      f"over 2 simulated ranks, torch CPU fp32 oracle (oracle/model_oracle.py)",
+            "seconds": t_total}
+
+
+def run_reference(args) -> None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    job = build_job(args.config, max(args.gpus, world))
+    ref = cpu_reference_rate(job, steps=args.warmup + args.steps)
+    line = {"metric": "train samples/s", "value": ref["value"], "unit": "samples/s",
+            "impl": "reference", "n_gpus": max(args.gpus, world), "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": job.config.name,
+                                            "description": job.config.description},
+            "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": ref["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="gpt2_small", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--algo", type=int, default=K.ALGO_AUTO)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    world, rank, local = setup_dist()
+    dev = torch.device("cuda", local)
+    job = build_job(args.config, world)
+    comm_ag, comm_rs = make_comms(world, rank)
+    tr = UnevenFSDPTrainer(job.arch, job.plan, rank, comm_ag=comm_ag, comm_rs=comm_rs, opt=OPT,
+                           device=dev, algo=args.algo)
+    tr.init_params(seed=0)
+    arch, plan = job.arch, job.plan
+    nsteps = args.warmup + args.steps
+    host = [torch.from_numpy(rank_tokens(plan, rank, arch.seq, arch.vocab, SEED, s)).pin_memory()
+            for s in range(nsteps)]
+    resident = [h.to(dev) for h in host]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    # ---- device-resident timing (value) ------------------------------------
+    for s in range(args.warmup):
+        tr.step(resident[s])
+    barrier()
+    tr.timers.enabled = True
+    tr.timers.reset()
+    launches0 = tr.launches
+    comp = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        t0.record(comp)
+        for s in range(args.warmup, nsteps):
+            tr.step(resident[s])
+        t1.record(comp)
+        barrier()
+    launches = tr.launches - launches0
+    ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
+    adam_ms = tr.timers.mean_ms("adamw")
+    acc_ms_each = tr.timers.mean_ms("accumulate")
+    acc_n = len(tr.timers.accumulate)
+    tr.timers.enabled = False
+
+    # ---- end to end through the public API with host buffers (e2e) --------
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    loss_val = 0.0
+    for s in range(args.warmup, nsteps):
+        x = host[s].to(dev, non_blocking=True)
+        loss_val = float(tr.step(x))          # D2H read of the step's loss
+    e1.record(comp)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+
+    B = plan.total_batch
+    hbm, hbm_kind = peaks()
+    # algorithmic bytes: AdamW 30 B/param (p,g,m,v read; p,m,v write; bf16 shadow)
+    adam_bytes = 30.0 * tr.L.local_len
+    acc_elems = sum(arch.unit_params for _ in range(arch.layers)) * tr.l + \
+        arch.root_params * 0  # root accounted below
+    adam_total = adam_ms
+    acc_total = acc_ms_each * acc_n / max(args.steps, 1)
+    # per-launch accumulate bytes: units dominate; FIRST 6 B, ADD 10 B per param
+    first_frac = 1.0 / tr.l if tr.l else 1.0
+    acc_bytes_per_launch = arch.unit_params * (6.0 * first_frac + 10.0 * (1 - first_frac))
+    kernels = {
+        "adamw": {"ms": adam_ms, "bytes": adam_bytes,
+                  "gbs": adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None},
+        "accumulate": {"ms_per_launch": acc_ms_each, "launches_per_step": acc_n / args.steps,
+                       "bytes_per_launch_unit": acc_bytes_per_launch},
+    }
+    dominant = "adamw" if adam_total >= acc_total else "accumulate"
+    if dominant == "adamw":
+        achieved = kernels["adamw"]["gbs"]
+        traffic = None
+    else:
+        achieved = acc_bytes_per_launch / (acc_ms_each * 1e-3) / 1e9 if acc_ms_each else None
+        traffic = None
+    del acc_elems
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            ref = cpu_reference_rate(job)
+            cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        tok_bytes = sum(h.numel() * h.element_size() for h in host[:1]) * world
+        line = {
+            "metric": "train samples/s", "value": B / (ms * 1e-3), "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens (splitmix64), random-init weights",
+            "config": {"workload": job.config.name, "description": job.config.description,
+                       "global_batch": B, "seq_len": arch.seq,
+                       "plan": [[a.microbatch, a.num_microbatches, a.state_ratio]
+                                for a in plan.assignments],
+                       "uneven_units": plan.unit_shards.uneven_units,
+                       "parallelism": f"uneven-fsdp{world}",
+                       "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
+            "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
+                    "h2d_bytes_per_step": tok_bytes, "d2h_bytes_per_step": 4 * world},
+            "roofline": {"kernel": f"het_{dominant}", "bound": "hbm", "achieved": achieved,
+                         "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
+                         "frac": achieved / hbm if achieved else None, "traffic": traffic},
+            "kernels": kernels,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "loss": loss_val,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        comm_ag.close()
+        comm_rs.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

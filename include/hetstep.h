@@ -1,0 +1,115 @@
+/*
+ * hetstep.h — C-ABI of the B200-native Cephalo uneven-FSDP train step.
+ *
+ * The reference (`hetplan`, /root/reference/pkg/src/hetplan) is pure Python and
+ * has no FFI; its trainer exists only as the contract feeding it (planner
+ * output, unit shards/offsets), the Eq. 1 math and the schedule. Each entry
+ * point below implements one piece of that contract on sm_100a and cites what
+ * it replaces. All calls are asynchronous and stream-ordered on the caller's
+ * CUDA stream; buffers are owned by the caller (torch caching allocator);
+ * nothing here allocates device memory except NCCL's own communicator state.
+ *
+ * Return codes: HET_OK, HET_EARG (bad sizes/pointers/alignment → Python
+ * InputError), HET_ECUDA / HET_ENCCL (→ RuntimeError with het_last_error()).
+ */
+#ifndef HETSTEP_H_
+#define HETSTEP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HET_OK 0
+#define HET_EARG 1
+#define HET_ECUDA 2
+#define HET_ENCCL 3
+
+#define HET_MAX_SEGS 64
+
+/* One gradient tensor landing in a unit-sized fp32 accumulator. */
+typedef struct {
+  const void* src;    /* bf16 gradient, contiguous, n elements */
+  int64_t dst_off;    /* element offset inside the unit accumulator */
+  int64_t n;          /* elements */
+} het_seg_t;
+
+/* Accumulate modes (layered gradient accumulation, PAPER.md:653-660;
+ * schedule sim.py:278-322: all l_i microbatches of a unit, then one RS).
+ * Every contribution is pre-scaled by the rank's Eq. 1 weight w = m_i / B
+ * (gradcheck.py:30-46), so acc ends as sum_k w*g_k and the reduce-scatter is
+ * a plain SUM; with l_i == 1 the FIRST pass is the bf16->fp32 scale-cast. */
+#define HET_ACC_ADD 0   /* acc += w*g  (microbatches 1..l_i-1, or a zeroed acc) */
+#define HET_ACC_FIRST 1 /* acc  = w*g  (microbatch 0: no read of acc)           */
+
+/* Library identity: returns a static string "hetstep <version> sm_100a". */
+const char* het_version(void);
+/* Thread-local text of the last non-OK return. */
+const char* het_last_error(void);
+
+/* ---- kernels --------------------------------------------------------- */
+
+/* (1) pack: fp32 master shard -> bf16 all-gather send buffer, RNE.
+ * Replaces: FSDP shard->flat-param cast before unshard;
+ * the layout is sharding.py:89-95 offsets. 6 B/param. */
+int het_pack_bf16(const float* src, void* dst_bf16, int64_t n, void* stream);
+
+/* (4) layered accumulate-and-release over a segment table (one entry per
+ * parameter gradient of a unit) into the unit's fp32 accumulator:
+ * acc[dst_off + e] (=|+=) scale * bf16(src[e]). scale = m_i / B.
+ * 6 B/param for HET_ACC_FIRST, 10 B/param for HET_ACC_ADD. The caller drops
+ * its reference to the bf16 gradients after the call (release). */
+int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float scale,
+                   void* stream);
+
+/* (5) sharded AdamW over one rank's flat local shard (torch.optim.AdamW
+ * formula, decoupled weight decay). Optional bf16 shadow write (the next
+ * step's all-gather send buffer; fuses kernel (1)). 28 B/param, 30 with
+ * shadow. step >= 1. Replaces: the paper's per-GPU Adam on the FSDP shard
+ * (core.py:151-154 "16 B/param"). */
+int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
+              float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
+              void* stream);
+
+/* fill / zero helpers used by the step driver (idle ranks, pads) */
+int het_fill_f32(float* dst, float value, int64_t n, void* stream);
+
+/* ---- collectives (NCCL 2.28 over NVLink 5 / NVSwitch) ----------------- */
+
+/* 128-byte NCCL unique id produced on rank 0 and broadcast by the host. */
+int het_comm_unique_id(uint8_t out_id[128]);
+int het_comm_init(void** comm_out, const uint8_t id[128], int nranks, int rank);
+int het_comm_destroy(void* comm);
+
+#define HET_DT_BF16 0
+#define HET_DT_F32 1
+
+#define HET_ALGO_AUTO 0      /* even -> AllGather/ReduceScatter, else per-owner */
+#define HET_ALGO_P2P 1       /* grouped ncclSend/ncclRecv (north_star baseline)  */
+#define HET_ALGO_OWNER 2     /* grouped per-owner ncclBroadcast / ncclReduce     */
+#define HET_ALGO_EVEN 3      /* require even: ncclAllGather / ncclReduceScatter  */
+
+/* (2) uneven all-gather of one unit: rank j contributes counts[j] elements
+ * from `send` into unit[offsets[j] : offsets[j]+counts[j]] on every rank.
+ * counts/offsets are host arrays of length nranks (UnitShardPlan row,
+ * core.py:229-240). Replaces FSDP's generalized AllGather
+ * (PAPER.md:549, 648-651); schedule sim.py:344-363. */
+int het_allgather_uneven(const void* send, void* unit, const int64_t* counts,
+                         const int64_t* offsets, int nranks, int rank, int dtype, int algo,
+                         void* comm, void* stream);
+
+/* (3) uneven reduce-scatter of a unit: shard_out[0:counts[rank]] =
+ * sum_j src_j[offsets[rank] : +counts[rank]] where every rank's src was
+ * pre-scaled by its Eq. 1 weight in het_accumulate. fp32 in, fp32 out.
+ * Replaces FSDP's generalized ReduceScatter + Cephalo's reweighting
+ * (gradcheck.py:30-46); issue point sim.py:364-368. */
+int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t* counts,
+                              const int64_t* offsets, int nranks, int rank, int algo,
+                              void* comm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETSTEP_H_ */

@@ -1,0 +1,16 @@
+// Shared helpers of the hetstep C-ABI translation units (not installed).
+#pragma once
+#include <cstdarg>
+#include <cstdint>
+#include <string>
+
+namespace het {
+extern thread_local std::string g_last_error;
+// Record a printf-style message for het_last_error() and return `code`.
+int fail(int code, const char* fmt, ...);
+// HET_ECUDA with the launch error text if the last launch failed.
+int check_launch(const char* what);
+// Grid size for a grid-stride loop over `work_items` (x threads per CTA),
+// capped at 8 resident 256-thread CTAs per SM.
+int grid_for(int64_t work_items, int threads);
+}  // namespace het

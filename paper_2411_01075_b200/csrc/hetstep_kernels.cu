@@ -1,0 +1,358 @@
+// sm_100a streaming kernels of the uneven-FSDP train step.
+//
+// All four are HBM-bound elementwise passes (no data reuse, no tensor-core
+// work — see DESIGN.md "Kernels"): the design levers are 16-byte vector
+// accesses, several independent 16-byte requests in flight per thread
+// (loads issued before use), and a grid sized in multiples of the 148 SMs
+// with a grid-stride loop. Inputs touched once are loaded with the
+// streaming/evict-first hint so they do not displace the next unit's
+// gathered parameters in the 126 MB L2.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "hetstep.h"
+#include "hetstep_internal.cuh"
+
+namespace het {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HET_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HET_OK;
+}
+
+int grid_for(int64_t work_items, int threads) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  int64_t need = (work_items + threads - 1) / threads;
+  int64_t cap = static_cast<int64_t>(sms) * 8;  // 8 x 256-thread CTAs resident per SM
+  if (need < 1) need = 1;
+  return static_cast<int>(need < cap ? need : cap);
+}
+
+}  // namespace het
+
+using het::fail;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint32_t bits16) {
+  return __uint_as_float(bits16 << 16);
+}
+
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&f)[8]) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = bf16_bits_to_f32(w[i] & 0xffffu);
+    f[2 * i + 1] = bf16_bits_to_f32(w[i] >> 16);
+  }
+}
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---------------------------------------------------------------- pack
+
+__global__ void __launch_bounds__(kThreads) pack_vec_kernel(const float4* __restrict__ src,
+                                                            uint2* __restrict__ dst,
+                                                            int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += 2 * stride) {
+    const bool two = i + stride < n4;
+    float4 a = __ldcs(src + i);
+    float4 b = two ? __ldcs(src + i + stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+    dst[i] = make_uint2(pack2(a.x, a.y), pack2(a.z, a.w));
+    if (two) dst[i + stride] = make_uint2(pack2(b.x, b.y), pack2(b.z, b.w));
+  }
+}
+
+__global__ void pack_scalar_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                   int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+// ---------------------------------------------------------------- accumulate
+
+struct SegTable {
+  het_seg_t seg[HET_MAX_SEGS];
+  int64_t first_block[HET_MAX_SEGS + 1];  // prefix sum of blocks per segment
+  int nseg;
+};
+
+constexpr int kAccVec = 8;                 // bf16 elements per 16-byte load
+constexpr int kAccIters = 4;               // 16-byte requests in flight per thread
+constexpr int64_t kAccChunk = static_cast<int64_t>(kThreads) * kAccVec * kAccIters;
+
+template <int MODE>
+__device__ __forceinline__ float acc_op(float a, float g, float w) {
+  return MODE == HET_ACC_FIRST ? w * g : fmaf(w, g, a);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict__ acc,
+                                                              const __grid_constant__ SegTable t,
+                                                              float w) {
+  // locate this block's segment (<= 64 entries; warp-uniform scan)
+  const int64_t b = blockIdx.x;
+  int s = 0;
+  while (s + 1 < t.nseg && t.first_block[s + 1] <= b) ++s;
+  const het_seg_t sg = t.seg[s];
+  const int64_t base = (b - t.first_block[s]) * kAccChunk;
+  const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(sg.src);
+  float* dst = acc + sg.dst_off;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+  if (vec_ok && base + kAccChunk <= sg.n) {
+    uint4 raw[kAccIters];
+    float4 lo[kAccIters], hi[kAccIters];
+#pragma unroll
+    for (int it = 0; it < kAccIters; ++it) {
+      const int64_t e = base + (static_cast<int64_t>(it) * kThreads + threadIdx.x) * kAccVec;
+      raw[it] = __ldcs(reinterpret_cast<const uint4*>(src + e));
+      if (MODE & HET_ACC_FIRST) {
+        lo[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+        hi[it] = lo[it];
+      } else {
+        lo[it] = *reinterpret_cast<const float4*>(dst + e);
+        hi[it] = *reinterpret_cast<const float4*>(dst + e + 4);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kAccIters; ++it) {
+      const int64_t e = base + (static_cast<int64_t>(it) * kThreads + threadIdx.x) * kAccVec;
+      float g[8];
+      unpack8(raw[it], g);
+      float4 o0 = make_float4(acc_op<MODE>(lo[it].x, g[0], w), acc_op<MODE>(lo[it].y, g[1], w),
+                              acc_op<MODE>(lo[it].z, g[2], w), acc_op<MODE>(lo[it].w, g[3], w));
+      float4 o1 = make_float4(acc_op<MODE>(hi[it].x, g[4], w), acc_op<MODE>(hi[it].y, g[5], w),
+                              acc_op<MODE>(hi[it].z, g[6], w), acc_op<MODE>(hi[it].w, g[7], w));
+      *reinterpret_cast<float4*>(dst + e) = o0;
+      *reinterpret_cast<float4*>(dst + e + 4) = o1;
+    }
+    return;
+  }
+  // ragged tail of a segment (or unaligned segment): scalar, coalesced
+  const int64_t end = base + kAccChunk < sg.n ? base + kAccChunk : sg.n;
+  for (int64_t e = base + threadIdx.x; e < end; e += kThreads) {
+    const float g = __bfloat162float(src[e]);
+    const float a = (MODE & HET_ACC_FIRST) ? 0.f : dst[e];
+    dst[e] = acc_op<MODE>(a, g, w);
+  }
+}
+
+// ---------------------------------------------------------------- AdamW
+
+struct AdamCoef {
+  float decay;        // 1 - lr * wd
+  float one_m_b1;     // 1 - beta1
+  float beta2;
+  float one_m_b2;     // 1 - beta2
+  float bc2_sqrt;  // sqrt(1 - beta2^t)  (divisor, as torch)
+  float eps;
+  float neg_step;     // -lr / (1 - beta1^t)
+};
+
+__device__ __forceinline__ void adam1(float& p, float g, float& m, float& v, const AdamCoef& c) {
+  p = p * c.decay;
+  m = m + c.one_m_b1 * (g - m);               // exp_avg.lerp_(grad, 1 - beta1)
+  v = v * c.beta2 + c.one_m_b2 * g * g;       // mul_(beta2).addcmul_(g, g, 1 - beta2)
+  const float denom = sqrtf(v) / c.bc2_sqrt + c.eps;
+  p = p + c.neg_step * (m / denom);           // addcdiv_(m, denom, -step_size)
+}
+
+template <bool SHADOW>
+__global__ void __launch_bounds__(kThreads) adamw_vec_kernel(float4* __restrict__ p,
+                                                             const float4* __restrict__ g,
+                                                             float4* __restrict__ m,
+                                                             float4* __restrict__ v,
+                                                             uint2* __restrict__ shadow,
+                                                             int64_t n4, AdamCoef c) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += 2 * stride) {
+    const int64_t j = i + stride;
+    const bool two = j < n4;
+    float4 p0 = p[i], g0 = __ldcs(g + i), m0 = m[i], v0 = v[i];
+    float4 p1, g1, m1, v1;
+    if (two) {
+      p1 = p[j];
+      g1 = __ldcs(g + j);
+      m1 = m[j];
+      v1 = v[j];
+    }
+    adam1(p0.x, g0.x, m0.x, v0.x, c);
+    adam1(p0.y, g0.y, m0.y, v0.y, c);
+    adam1(p0.z, g0.z, m0.z, v0.z, c);
+    adam1(p0.w, g0.w, m0.w, v0.w, c);
+    p[i] = p0;
+    m[i] = m0;
+    v[i] = v0;
+    if (SHADOW) shadow[i] = make_uint2(pack2(p0.x, p0.y), pack2(p0.z, p0.w));
+    if (two) {
+      adam1(p1.x, g1.x, m1.x, v1.x, c);
+      adam1(p1.y, g1.y, m1.y, v1.y, c);
+      adam1(p1.z, g1.z, m1.z, v1.z, c);
+      adam1(p1.w, g1.w, m1.w, v1.w, c);
+      p[j] = p1;
+      m[j] = m1;
+      v[j] = v1;
+      if (SHADOW) shadow[j] = make_uint2(pack2(p1.x, p1.y), pack2(p1.z, p1.w));
+    }
+  }
+}
+
+__global__ void adamw_scalar_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                    float* __restrict__ m, float* __restrict__ v,
+                                    __nv_bfloat16* __restrict__ shadow, int64_t n, AdamCoef c) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    float pp = p[i], mm = m[i], vv = v[i];
+    adam1(pp, g[i], mm, vv, c);
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+    if (shadow) shadow[i] = __float2bfloat16_rn(pp);
+  }
+}
+
+__global__ void fill_kernel(float* __restrict__ dst, float value, int64_t n) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride)
+    dst[i] = value;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* het_version(void) { return "hetstep 0.1.0 sm_100a"; }
+
+const char* het_last_error(void) { return het::g_last_error.c_str(); }
+
+int het_pack_bf16(const float* src, void* dst_bf16, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst_bf16))) return fail(HET_EARG, "het_pack_bf16: bad args");
+  if (n == 0) return HET_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (aligned16(src) && (reinterpret_cast<uintptr_t>(dst_bf16) & 7) == 0 && n % 4 == 0) {
+    const int64_t n4 = n / 4;
+    pack_vec_kernel<<<het::grid_for((n4 + 1) / 2, kThreads), kThreads, 0, st>>>(
+        reinterpret_cast<const float4*>(src), static_cast<uint2*>(dst_bf16), n4);
+  } else {
+    pack_scalar_kernel<<<het::grid_for(n, kThreads), kThreads, 0, st>>>(
+        src, static_cast<__nv_bfloat16*>(dst_bf16), n);
+  }
+  return het::check_launch("het_pack_bf16");
+}
+
+int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float scale,
+                   void* stream) {
+  if (!acc || !segs || nseg < 1 || nseg > HET_MAX_SEGS || (mode != HET_ACC_ADD && mode != HET_ACC_FIRST))
+    return fail(HET_EARG, "het_accumulate: bad args (nseg=%d mode=%d)", nseg, mode);
+  SegTable t;
+  t.nseg = nseg;
+  int64_t blocks = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (segs[s].n < 0 || segs[s].dst_off < 0 || (segs[s].n > 0 && !segs[s].src))
+      return fail(HET_EARG, "het_accumulate: bad segment %d", s);
+    t.seg[s] = segs[s];
+    t.first_block[s] = blocks;
+    blocks += (segs[s].n + kAccChunk - 1) / kAccChunk;
+  }
+  t.first_block[nseg] = blocks;
+  for (int s = nseg + 1; s <= HET_MAX_SEGS; ++s) t.first_block[s] = blocks;
+  if (blocks == 0) return HET_OK;
+  if (blocks > 0x7fffffff) return fail(HET_EARG, "het_accumulate: too large");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const dim3 grid(static_cast<unsigned>(blocks));
+  if (mode == HET_ACC_FIRST)
+    accumulate_kernel<HET_ACC_FIRST><<<grid, kThreads, 0, st>>>(acc, t, scale);
+  else
+    accumulate_kernel<HET_ACC_ADD><<<grid, kThreads, 0, st>>>(acc, t, scale);
+  return het::check_launch("het_accumulate");
+}
+
+int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
+              float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
+              void* stream) {
+  if (n < 0 || step < 1 || (n > 0 && (!p || !g || !m || !v)))
+    return fail(HET_EARG, "het_adamw: bad args (n=%lld step=%lld)", (long long)n,
+                (long long)step);
+  if (n == 0) return HET_OK;
+  // scalar coefficients in double, as torch's _single_tensor_adamw computes them
+  const double bc1 = 1.0 - std::pow(static_cast<double>(beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(beta2), static_cast<double>(step));
+  AdamCoef c;
+  c.decay = static_cast<float>(1.0 - static_cast<double>(lr) * weight_decay);
+  c.one_m_b1 = static_cast<float>(1.0 - static_cast<double>(beta1));
+  c.beta2 = beta2;
+  c.one_m_b2 = static_cast<float>(1.0 - static_cast<double>(beta2));
+  c.bc2_sqrt = static_cast<float>(std::sqrt(bc2));
+  c.eps = eps;
+  c.neg_step = static_cast<float>(-(static_cast<double>(lr) / bc1));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec = n % 4 == 0 && aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
+                   (!p_bf16_or_null || (reinterpret_cast<uintptr_t>(p_bf16_or_null) & 7) == 0);
+  if (vec) {
+    const int64_t n4 = n / 4;
+    const int grid = het::grid_for((n4 + 1) / 2, kThreads);
+    if (p_bf16_or_null)
+      adamw_vec_kernel<true><<<grid, kThreads, 0, st>>>(
+          reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+          reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
+          static_cast<uint2*>(p_bf16_or_null), n4, c);
+    else
+      adamw_vec_kernel<false><<<grid, kThreads, 0, st>>>(
+          reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+          reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), nullptr, n4, c);
+  } else {
+    adamw_scalar_kernel<<<het::grid_for(n, kThreads), kThreads, 0, st>>>(
+        p, g, m, v, static_cast<__nv_bfloat16*>(p_bf16_or_null), n, c);
+  }
+  return het::check_launch("het_adamw");
+}
+
+int het_fill_f32(float* dst, float value, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && !dst)) return fail(HET_EARG, "het_fill_f32: bad args");
+  if (n == 0) return HET_OK;
+  fill_kernel<<<het::grid_for(n, kThreads), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      dst, value, n);
+  return het::check_launch("het_fill_f32");
+}
+
+}  // extern "C"

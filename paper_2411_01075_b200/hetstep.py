@@ -1,0 +1,208 @@
+"""ctypes binding of the sm_100a C-ABI (``include/hetstep.h``).
+
+Every function takes torch CUDA tensors, checks dtype/contiguity/device, and
+launches on the caller's current CUDA stream (or an explicit one). There is
+no CPU or PyTorch fallback: if ``libhetstep.so`` cannot be loaded, or a tensor
+is not on a CUDA device, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from ._build import STEP_LIB, build_step
+from .core import InputError
+
+HET_OK, HET_EARG, HET_ECUDA, HET_ENCCL = 0, 1, 2, 3
+HET_MAX_SEGS = 64
+ACC_ADD, ACC_FIRST = 0, 1
+DT_BF16, DT_F32 = 0, 1
+ALGO_AUTO, ALGO_P2P, ALGO_OWNER, ALGO_EVEN = 0, 1, 2, 3
+
+EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
+           "het_fill_f32", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_allgather_uneven", "het_reduce_scatter_uneven")
+
+
+class HetSeg(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst_off", ctypes.c_int64), ("n", ctypes.c_int64)]
+
+
+_lib: ctypes.CDLL | None = None
+
+
+def load(build: bool = False) -> ctypes.CDLL:
+    """Load (optionally building first) the in-tree libhetstep.so."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build or not STEP_LIB.exists():
+        build_step()
+    lib = ctypes.CDLL(str(STEP_LIB))
+    vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    sig = {
+        "het_version": ([], ctypes.c_char_p),
+        "het_last_error": ([], ctypes.c_char_p),
+        "het_pack_bf16": ([vp, vp, i64, vp], i32),
+        "het_accumulate": ([vp, ctypes.POINTER(HetSeg), i32, i32, f32, vp], i32),
+        "het_adamw": ([vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, i64, vp], i32),
+        "het_fill_f32": ([vp, f32, i64, vp], i32),
+        "het_comm_unique_id": ([ctypes.c_char_p], i32),
+        "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
+        "het_comm_destroy": ([vp], i32),
+        "het_allgather_uneven": ([vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64), i32, i32, i32,
+                                  i32, vp, vp], i32),
+        "het_reduce_scatter_uneven": ([vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64), i32, i32,
+                                       i32, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def version() -> str:
+    return load().het_version().decode()
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == HET_OK:
+        return
+    msg = load().het_last_error().decode()
+    if rc == HET_EARG:
+        raise InputError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed ({'CUDA' if rc == HET_ECUDA else 'NCCL'}): {msg}")
+
+
+def _cuda(t: torch.Tensor, dtype: torch.dtype, name: str) -> int:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InputError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise InputError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise InputError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def pack_bf16(src: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
+    n = src.numel()
+    if dst.numel() != n:
+        raise InputError("pack_bf16: size mismatch")
+    _check(load().het_pack_bf16(_cuda(src, torch.float32, "src"),
+                                _cuda(dst, torch.bfloat16, "dst"), n, _stream(stream)),
+           "het_pack_bf16")
+
+
+def accumulate(acc: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]], first: bool,
+               scale: float, stream=None) -> None:
+    """acc[off:off+g.numel()] (=|+=) scale * g for every (g, off); g bf16."""
+    if not grads:
+        return
+    if len(grads) > HET_MAX_SEGS:
+        for i in range(0, len(grads), HET_MAX_SEGS):
+            accumulate(acc, grads[i:i + HET_MAX_SEGS], first, scale, stream)
+        return
+    cap = acc.numel()
+    segs = (HetSeg * len(grads))()
+    for i, (g, off) in enumerate(grads):
+        if off < 0 or off + g.numel() > cap:
+            raise InputError(f"accumulate: segment {i} [{off}, {off + g.numel()}) outside {cap}")
+        segs[i].src = _cuda(g, torch.bfloat16, f"grad[{i}]")
+        segs[i].dst_off = off
+        segs[i].n = g.numel()
+    _check(load().het_accumulate(_cuda(acc, torch.float32, "acc"), segs, len(grads),
+                                 ACC_FIRST if first else ACC_ADD, float(scale), _stream(stream)),
+           "het_accumulate")
+
+
+def adamw(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,
+          shadow: torch.Tensor | None, *, lr: float, beta1: float, beta2: float, eps: float,
+          weight_decay: float, step: int, stream=None) -> None:
+    n = p.numel()
+    if not (g.numel() == m.numel() == v.numel() == n) or (shadow is not None and
+                                                        shadow.numel() != n):
+        raise InputError("adamw: size mismatch")
+    sh = _cuda(shadow, torch.bfloat16, "shadow") if shadow is not None else None
+    _check(load().het_adamw(_cuda(p, torch.float32, "p"), _cuda(g, torch.float32, "g"),
+                            _cuda(m, torch.float32, "m"), _cuda(v, torch.float32, "v"), sh, n,
+                            lr, beta1, beta2, eps, weight_decay, int(step), _stream(stream)),
+           "het_adamw")
+
+
+def fill(dst: torch.Tensor, value: float, stream=None) -> None:
+    _check(load().het_fill_f32(_cuda(dst, torch.float32, "dst"), float(value), dst.numel(),
+                               _stream(stream)), "het_fill_f32")
+
+
+# ---------------------------------------------------------------------------
+# NCCL communicators
+
+def unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().het_comm_unique_id(buf), "het_comm_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """One NCCL communicator owned by this process (rank i == cluster.gpus[i])."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        if len(uid) != 128:
+            raise InputError("NCCL unique id must be 128 bytes")
+        self.nranks, self.rank = nranks, rank
+        h = ctypes.c_void_p()
+        _check(load().het_comm_init(ctypes.byref(h), uid, nranks, rank), "het_comm_init")
+        self.handle = h
+
+    def close(self) -> None:
+        if self.handle:
+            _check(load().het_comm_destroy(self.handle), "het_comm_destroy")
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self) -> None:  # best effort; explicit close() is preferred
+        try:
+            if getattr(self, "handle", None):
+                load().het_comm_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _i64(vals: Sequence[int]):
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def allgather_uneven(send: torch.Tensor, unit: torch.Tensor, counts: Sequence[int],
+                     offsets: Sequence[int], comm: Comm | None, rank: int,
+                     algo: int = ALGO_AUTO, stream=None) -> None:
+    if unit.dtype not in (torch.bfloat16, torch.float32) or send.dtype != unit.dtype:
+        raise InputError("allgather_uneven: bf16 or fp32, matching dtypes")
+    n = len(counts)
+    if sum(counts) != unit.numel() or send.numel() < counts[rank]:
+        raise InputError("allgather_uneven: buffer sizes do not match the shard table")
+    dt = DT_BF16 if unit.dtype == torch.bfloat16 else DT_F32
+    _check(load().het_allgather_uneven(
+        _cuda(send, send.dtype, "send") if send.numel() else None, _cuda(unit, unit.dtype, "unit"),
+        _i64(counts), _i64(offsets), n, rank, dt, algo, comm.handle if comm else None,
+        _stream(stream)), "het_allgather_uneven")
+
+
+def reduce_scatter_uneven(src: torch.Tensor, shard: torch.Tensor, counts: Sequence[int],
+                          offsets: Sequence[int], comm: Comm | None, rank: int,
+                          algo: int = ALGO_AUTO, stream=None) -> None:
+    n = len(counts)
+    if sum(counts) != src.numel() or shard.numel() < counts[rank]:
+        raise InputError("reduce_scatter_uneven: buffer sizes do not match the shard table")
+    _check(load().het_reduce_scatter_uneven(
+        _cuda(src, torch.float32, "src"),
+        _cuda(shard, torch.float32, "shard") if shard.numel() else None,
+        _i64(counts), _i64(offsets), n, rank, algo, comm.handle if comm else None,
+        _stream(stream)), "het_reduce_scatter_uneven")

@@ -1,0 +1,335 @@
+"""The train-step entry point: one Cephalo layered-gradient-accumulation
+iteration on one rank (one process per GPU).
+
+Schedule (the reference's executable spec, sim.py:342-368):
+
+  FWD  AG(root), AG(unit 0)                                  [ag stream]
+       for u in 0..L-1:  prefetch AG(u+1) into the other buffer once unit
+                         u-1 has released it                  [ag stream]
+                         all l_i microbatches through unit u, keeping only
+                         the unit-boundary activations (checkpoints)
+       head: loss_k and dL/dh_L for every microbatch; root grads accumulate
+  BWD  for u in L-1..0:  prefetch AG(u-1) (units L-1 and L-2 are still
+                         resident from the forward: no re-gather)
+                         for each microbatch: recompute unit u, backward,
+                         het_accumulate(acc_u, grads, w = m_i/B)  (kernel 4)
+                         then RS(acc_u -> rank's fp32 grad shard)  [rs stream]
+       embedding backward into the root accumulator, RS(root)
+  OPT  one het_adamw over the rank's whole flat shard, writing the bf16
+       shadow that the next step all-gathers                 (kernel 5 + 1)
+
+Eq. 1 weighting (gradcheck.py:30-46) is the w = m_i/B pre-scale inside
+het_accumulate, so RS is a plain SUM. Idle ranks (m_i = 0, core.py:224-226)
+skip compute but still take part in every AG/RS with zero contributions.
+On one GPU the unit views point straight into the bf16 shadow and the
+accumulator is the grad shard itself: no collectives, no copies.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import hetstep as K
+from .core import InputError, TrainPlan
+from .layout import RankLayout
+from .model import ArchSpec, block_forward, embed_forward, head_loss, init_flat, segment_offsets, views
+
+
+@dataclass(frozen=True)
+class AdamWConfig:
+    lr: float = 1e-3
+    betas: tuple[float, float] = (0.9, 0.95)
+    eps: float = 1e-8
+    weight_decay: float = 0.1
+
+
+@dataclass
+class StepTimers:
+    """CUDA events around the owned kernels (enabled for roofline runs)."""
+    enabled: bool = False
+    adamw: list = field(default_factory=list)
+    accumulate: list = field(default_factory=list)
+
+    def pair(self, kind: str):
+        if not self.enabled:
+            return None, None
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        getattr(self, kind).append((a, b))
+        return a, b
+
+    def reset(self) -> None:
+        self.adamw.clear()
+        self.accumulate.clear()
+
+    def mean_ms(self, kind: str) -> float:
+        ev = getattr(self, kind)
+        if not ev:
+            return 0.0
+        return sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+
+
+class _NoStream:
+    """Stand-in for CUDA streams/events when a test drives the schedule on CPU
+    with injected kernels; the real kernels reject CPU tensors, so this is not
+    a compute fallback."""
+    cuda_stream = 0
+
+    def wait_event(self, ev) -> None:
+        pass
+
+    def wait_stream(self, other) -> None:
+        pass
+
+    def record(self, stream=None) -> None:
+        pass
+
+
+class UnevenFSDPTrainer:
+    """Per-rank state (uneven flat shards in HBM) plus the step driver."""
+
+    def __init__(self, arch: ArchSpec, plan: TrainPlan, rank: int, *,
+                 comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
+                 opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
+                 algo: int = K.ALGO_AUTO):
+        if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
+            raise InputError("plan unit_shards must have one row per transformer block")
+        self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.cuda = self.device.type == "cuda"
+        if self.cuda:
+            K.load()
+        self.L = RankLayout.from_plan(plan, arch.unit_params, arch.root_params, rank)
+        self.N = self.L.nranks
+        if self.N > 1 and (comm_ag is None or comm_rs is None):
+            raise InputError("multi-rank plan needs the AG and RS communicators")
+        self.comm_ag, self.comm_rs = comm_ag, comm_rs
+        a = plan.assignments[rank]
+        self.m, self.l = a.microbatch, a.num_microbatches
+        self.B = plan.total_batch
+        self.w = self.m / self.B
+        dev, n = self.device, self.L.local_len
+        self.p32 = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.g32 = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.m32 = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.v32 = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.p16 = torch.zeros(n, dtype=torch.bfloat16, device=dev)
+        U, E = arch.unit_params, arch.root_params
+        if self.N > 1:
+            self.ubuf = [torch.empty(U, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+            self.rbuf = torch.empty(E, dtype=torch.bfloat16, device=dev)
+            self.acc = [torch.zeros(U, dtype=torch.float32, device=dev) for _ in range(2)]
+            self.racc = torch.zeros(E, dtype=torch.float32, device=dev)
+        self.ag_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
+        self.rs_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
+        self.unit_seg = segment_offsets(arch.unit_layout())
+        self.root_seg = segment_offsets(arch.root_layout())
+        self.steps = 0
+        self.timers = StepTimers()
+        self.launches = 0          # owned-kernel launches (hetstep.so), this process
+
+    # ------------------------------------------------------------------ params
+    def _local(self, buf: torch.Tensor, u: int) -> torch.Tensor:
+        off, cnt = self.L.local_range(u)
+        return buf[off:off + cnt]
+
+    def load_full_units(self, units: list[torch.Tensor]) -> None:
+        """Install full fp32 unit vectors (L blocks then the root) and take this
+        rank's shards; refreshes the bf16 shadow."""
+        if len(units) != self.L.blocks + 1:
+            raise InputError("need one tensor per block plus the root")
+        for u, full in enumerate(units):
+            if full.numel() != self.L.unit_size(u):
+                raise InputError(f"unit {u}: wrong size")
+            o = self.L.offsets[u][self.rank]
+            c = self.L.counts[u][self.rank]
+            self._local(self.p32, u).copy_(full.reshape(-1)[o:o + c].to(self.device,
+                                                                        torch.float32))
+        K.pack_bf16(self.p32, self.p16)
+        self.launches += 1
+        self.m32.zero_()
+        self.v32.zero_()
+        self.steps = 0
+
+    def init_params(self, seed: int = 0) -> None:
+        """Deterministic N(0, 0.02) init; every rank derives the same full
+        units (seeded per unit) and keeps its own ranges."""
+        units = []
+        for u in range(self.L.blocks + 1):
+            gen = torch.Generator(device=self.device)
+            gen.manual_seed(seed * 100003 + u)
+            layout = self.arch.root_layout() if u == self.L.root else self.arch.unit_layout()
+            units.append(init_flat(layout, gen, self.device))
+        self.load_full_units(units)
+
+    # ------------------------------------------------------------------ comm
+    def _event(self, stream):
+        ev = torch.cuda.Event() if self.cuda else _NoStream()
+        ev.record(stream)
+        return ev
+
+    def _current(self):
+        return torch.cuda.current_stream(self.device) if self.cuda else _NoStream()
+
+    def _ag(self, u: int, dst: torch.Tensor) -> torch.cuda.Event:
+        K.allgather_uneven(self._local(self.p16, u), dst, self.L.counts[u],
+                           self.L.offsets[u], self.comm_ag, self.rank, self.algo,
+                           stream=self.ag_stream)
+        return self._event(self.ag_stream)
+
+    def _rs(self, u: int, src: torch.Tensor, after: torch.cuda.Event) -> torch.cuda.Event:
+        self.rs_stream.wait_event(after)
+        K.reduce_scatter_uneven(src, self._local(self.g32, u), self.L.counts[u],
+                                self.L.offsets[u], self.comm_rs, self.rank, self.algo,
+                                stream=self.rs_stream)
+        return self._event(self.rs_stream)
+
+    def _unit_flat(self, u: int) -> torch.Tensor:
+        if self.N == 1:
+            off = self.L.local_off[u]
+            return self.p16[off:off + self.L.unit_size(u)]
+        return self.rbuf if u == self.L.root else self.ubuf[u % 2]
+
+    def _acc(self, u: int) -> torch.Tensor:
+        if self.N == 1:
+            return self._local(self.g32, u)
+        return self.racc if u == self.L.root else self.acc[u % 2]
+
+    def _accumulate(self, acc, grads, names, seg, first):
+        a, b = self.timers.pair("accumulate")
+        if a is not None:
+            a.record()
+        K.accumulate(acc, [(g, seg[nm]) for g, nm in zip(grads, names)], first, self.w)
+        if b is not None:
+            b.record()
+        self.launches += 1
+
+    # ------------------------------------------------------------------ step
+    def step(self, tok: torch.Tensor) -> torch.Tensor:
+        """One iteration on this rank's [b_i, seq+1] int32 token block (device).
+        Returns this rank's Eq. 1-weighted loss contribution sum_k (m_i/B) loss_k
+        (a device scalar; the global loss is its sum over ranks)."""
+        arch, L, comp = self.arch, self.L, self._current()
+        nb, root = L.blocks, L.root
+        if self.m > 0 and (tok.shape[0] != self.m * self.l or tok.shape[1] != arch.seq + 1):
+            raise InputError(f"rank {self.rank} expects tokens [{self.m * self.l}, {arch.seq + 1}]")
+        multi = self.N > 1
+        unit_names = [nm for nm, _ in arch.unit_layout()]
+        root_names = [nm for nm, _ in arch.root_layout()]
+        loss = torch.zeros((), dtype=torch.float32, device=self.device)
+
+        # ---- forward -------------------------------------------------------
+        ag_ev: dict[int, torch.cuda.Event] = {}
+        done_ev: dict[int, torch.cuda.Event] = {}
+        if multi:
+            self.ag_stream.wait_stream(comp)      # previous step's AdamW wrote p16
+            ag_ev[root] = self._ag(root, self.rbuf)
+            ag_ev[0] = self._ag(0, self.ubuf[0])
+        racc = self._acc(root)
+        if multi:
+            comp.wait_stream(self.rs_stream)     # racc no longer read by last step's RS
+        K.fill(racc, 0.0)
+        self.launches += 1
+
+        active = self.m > 0
+        mb = [(tok[k * self.m:(k + 1) * self.m, :-1], tok[k * self.m:(k + 1) * self.m, 1:])
+              for k in range(self.l)] if active else []
+        h: list[list[torch.Tensor | None]] = [[None] * (nb + 1) for _ in mb]
+        if multi:
+            comp.wait_event(ag_ev[root])
+        rp = views(self._unit_flat(root), arch.root_layout())
+        with torch.no_grad():
+            for k, (x_tok, _) in enumerate(mb):
+                h[k][0] = embed_forward(arch, rp, x_tok)
+            for u in range(nb):
+                if multi:
+                    if u + 1 < nb:
+                        if u >= 1:
+                            self.ag_stream.wait_event(done_ev[u - 1])
+                        ag_ev[u + 1] = self._ag(u + 1, self.ubuf[(u + 1) % 2])
+                    comp.wait_event(ag_ev[u])
+                p = views(self._unit_flat(u), arch.unit_layout())
+                for k in range(len(mb)):
+                    h[k][u + 1] = block_forward(arch, p, h[k][u])
+                done_ev[u] = self._event(comp)
+
+        # ---- head + loss ---------------------------------------------------
+        dy: list[torch.Tensor | None] = [None] * len(mb)
+        leaves = {nm: t.requires_grad_(True) for nm, t in
+                  views(self._unit_flat(root), arch.root_layout()).items()}
+        head_names = [nm for nm in root_names if nm != "wpe"]
+        for k, (_, tgt) in enumerate(mb):
+            x = h[k][nb].requires_grad_(True)
+            with torch.enable_grad():
+                lk = head_loss(arch, leaves, x, tgt)
+            grads = torch.autograd.grad(lk, [leaves[nm] for nm in head_names] + [x])
+            dy[k] = grads[-1]
+            h[k][nb] = None
+            self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
+            loss += lk.detach() * self.w
+
+        # ---- backward --------------------------------------------------------
+        rs_ev: dict[int, torch.cuda.Event] = {}
+        for u in reversed(range(nb)):
+            if multi:
+                # prefetch u-1 unless it is still resident from the forward
+                if u - 1 >= 0 and u - 1 < nb - 2:
+                    self.ag_stream.wait_event(done_ev[u + 1])
+                    ag_ev[u - 1] = self._ag(u - 1, self.ubuf[(u - 1) % 2])
+                if u < nb - 2:
+                    comp.wait_event(ag_ev[u])
+                if u + 2 in rs_ev:                  # acc[u % 2] last read by RS(u+2)
+                    comp.wait_event(rs_ev[u + 2])
+            acc = self._acc(u)
+            flat = self._unit_flat(u)
+            pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}
+            plist = [pl[nm] for nm in unit_names]
+            for k in range(len(mb)):
+                x = h[k][u].requires_grad_(True)
+                with torch.enable_grad():
+                    y = block_forward(arch, pl, x)
+                grads = torch.autograd.grad(y, plist + [x], dy[k])
+                dy[k] = grads[-1]
+                h[k][u] = None
+                self._accumulate(acc, grads[:-1], unit_names, self.unit_seg, first=(k == 0))
+            done_ev[u] = self._event(comp)
+            if multi:                                # an idle rank's acc holds zeros
+                rs_ev[u] = self._rs(u, acc, done_ev[u])
+
+        # ---- embedding backward + root RS -----------------------------------
+        emb_names = ["wte"] if arch.kind == "llama" else ["wte", "wpe"]
+        for k, (x_tok, _) in enumerate(mb):
+            with torch.enable_grad():
+                e = embed_forward(arch, leaves, x_tok)
+            grads = torch.autograd.grad(e, [leaves[nm] for nm in emb_names], dy[k])
+            dy[k] = None
+            self._accumulate(racc, grads, emb_names, self.root_seg, first=False)
+        if multi:
+            rs_ev[root] = self._rs(root, racc, self._event(comp))
+            comp.wait_event(rs_ev[root])            # RS stream is in order: all shards ready
+
+        # ---- optimizer -------------------------------------------------------
+        self.steps += 1
+        a, b = self.timers.pair("adamw")
+        if a is not None:
+            a.record()
+        K.adamw(self.p32, self.g32, self.m32, self.v32, self.p16, lr=self.opt.lr,
+                beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
+                weight_decay=self.opt.weight_decay, step=self.steps)
+        if b is not None:
+            b.record()
+        self.launches += 1
+        return loss
+
+    # ------------------------------------------------------------------ views for tests
+    def full_units(self, which: str = "p32") -> list[torch.Tensor]:
+        """All-gather the full fp32 vectors of `which` (p32/g32/m32/v32) for
+        every unit (test/debug helper; a collective on multi-rank)."""
+        src = getattr(self, which)
+        out = []
+        for u in range(self.L.blocks + 1):
+            full = torch.empty(self.L.unit_size(u), dtype=torch.float32, device=self.device)
+            K.allgather_uneven(self._local(src, u).contiguous(), full, self.L.counts[u],
+                               self.L.offsets[u], self.comm_ag, self.rank)
+            out.append(full)
+        return out

@@ -1,0 +1,130 @@
+"""Parity of the owned sm_100a kernels against the CPU oracle, called through
+the C-ABI (paper_2411_01075_b200.hetstep -> libhetstep.so).
+
+Tolerances (north_star): pack is bit-exact (integer bf16 bit patterns);
+accumulate and AdamW are fp32 elementwise and must match within a max
+relative error of 1e-5 (element-wise, |gpu - ref| <= 1e-5 * max(|ref|, tiny)).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import step_oracle as O
+from paper_2411_01075_b200 import hetstep as K
+from paper_2411_01075_b200.core import InputError
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-5
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _rel(a: np.ndarray, b: np.ndarray) -> float:
+    scale = np.maximum(np.abs(b), 1e-30)
+    return float(np.max(np.abs(a - b) / scale)) if a.size else 0.0
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 1000, 4099, 1 << 20, (1 << 22) + 5])
+def test_pack_bit_exact(cuda, n):
+    g = torch.Generator().manual_seed(n)
+    x = (torch.randn(n, generator=g) * 3).float()
+    if n > 8:
+        x[:4] = torch.tensor([float("inf"), -float("inf"), 0.0, -0.0])
+    src = x.to(cuda)
+    dst = torch.empty(n, dtype=torch.bfloat16, device=cuda)
+    K.pack_bf16(src, dst)
+    torch.cuda.synchronize()
+    assert np.array_equal(_bits(dst), O.pack(x.numpy()))
+
+
+def test_pack_unaligned_tail(cuda):
+    x = torch.randn(1001, generator=torch.Generator().manual_seed(1))
+    src = x.to(cuda)[1:]                     # 4-byte aligned only -> scalar path
+    dst = torch.empty(1000, dtype=torch.bfloat16, device=cuda)
+    K.pack_bf16(src, dst)
+    torch.cuda.synchronize()
+    assert np.array_equal(_bits(dst), O.pack(x.numpy()[1:]))
+
+
+def _segments(sizes, seed):
+    g = torch.Generator().manual_seed(seed)
+    grads = [torch.randn(s, generator=g).to(torch.bfloat16) for s in sizes]
+    offs, pos = [], 0
+    for s in sizes:
+        offs.append(pos)
+        pos += s
+    return grads, offs, pos
+
+
+@pytest.mark.parametrize("sizes", [[8], [3, 5, 7], [768 * 2304, 2304, 768 * 768, 768, 3072 * 768, 3072,
+                                                    768 * 3072, 768, 768, 768, 768, 768],
+                                   [1, 8191, 8192, 8193, 33000]])
+def test_accumulate_layered(cuda, sizes):
+    grads, offs, total = _segments(sizes, len(sizes))
+    w = 3.0 / 97.0
+    acc = torch.empty(total, dtype=torch.float32, device=cuda)
+    ref = np.zeros(total, dtype=np.float32)
+    for k in range(3):                       # l_i = 3 microbatches
+        gk = [(g * (k + 1)).to(torch.bfloat16) for g in grads]
+        K.accumulate(acc, [(g.to(cuda), o) for g, o in zip(gk, offs)], first=(k == 0), scale=w)
+        full = np.zeros(total, dtype=np.uint16)
+        for g, o in zip(gk, offs):
+            full[o:o + g.numel()] = _bits(g)
+        ref = O.accumulate(ref, full, k == 0, w)
+    torch.cuda.synchronize()
+    got = acc.cpu().numpy()
+    assert _rel(got, ref) <= RTOL
+
+
+def test_accumulate_rejects_out_of_range(cuda):
+    acc = torch.zeros(10, device=cuda)
+    with pytest.raises(InputError):
+        K.accumulate(acc, [(torch.zeros(8, dtype=torch.bfloat16, device=cuda), 4)], True, 1.0)
+
+
+@pytest.mark.parametrize("n,shadow", [(1, True), (7, False), (4096, True), (3_000_003, True),
+                                      (1 << 22, False)])
+def test_adamw_matches_oracle(cuda, n, shadow):
+    g = torch.Generator().manual_seed(n)
+    p, gr = torch.randn(n, generator=g) * 0.02, torch.randn(n, generator=g) * 1e-3
+    m, v = torch.randn(n, generator=g) * 1e-4, torch.rand(n, generator=g) * 1e-6
+    opt = dict(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+    tp, tg, tm, tv = (t.to(cuda).contiguous() for t in (p, gr, m, v))
+    sh = torch.empty(n, dtype=torch.bfloat16, device=cuda) if shadow else None
+    K.adamw(tp, tg, tm, tv, sh, step=7, **opt)
+    torch.cuda.synchronize()
+    rp, rm, rv = O.adamw(p.numpy(), gr.numpy(), m.numpy(), v.numpy(), step=7, **opt)
+    assert _rel(tp.cpu().numpy(), rp) <= RTOL
+    assert _rel(tm.cpu().numpy(), rm) <= RTOL
+    assert _rel(tv.cpu().numpy(), rv) <= RTOL
+    if shadow:
+        assert np.array_equal(_bits(sh), O.pack(tp.cpu().numpy()))
+
+
+def test_adamw_matches_torch_adamw(cuda):
+    """Independent pin: the kernel against torch.optim.AdamW (CUDA, foreach=False)."""
+    n = 100_003
+    g = torch.Generator().manual_seed(5)
+    p0 = torch.randn(n, generator=g) * 0.02
+    grads = [torch.randn(n, generator=g) * 1e-3 for _ in range(3)]
+    ref = torch.nn.Parameter(p0.clone().to(cuda))
+    opt = torch.optim.AdamW([ref], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1,
+                            foreach=False, fused=False)
+    p, m, v = p0.clone().to(cuda), torch.zeros(n, device=cuda), torch.zeros(n, device=cuda)
+    for step, gr in enumerate(grads, 1):
+        ref.grad = gr.to(cuda)
+        opt.step()
+        K.adamw(p, gr.to(cuda), m, v, None, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8,
+                weight_decay=0.1, step=step)
+    torch.cuda.synchronize()
+    assert _rel(p.cpu().numpy(), ref.detach().cpu().numpy()) <= RTOL
+
+
+def test_fill(cuda):
+    t = torch.empty(12345, device=cuda)
+    K.fill(t, 0.0)
+    torch.cuda.synchronize()
+    assert float(t.abs().max()) == 0.0

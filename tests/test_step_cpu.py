@@ -1,0 +1,58 @@
+"""Host-side logic of the step driver on CPU: schedule, layout, autograd
+plumbing and the Eq. 1 weighting, with the CUDA kernels replaced by the
+oracle-backed test double (tests/fake_kernels.py). N=1 here; world_size 2
+over gloo in tests/test_multirank_cpu.py."""
+import numpy as np
+import pytest
+import torch
+
+import fake_kernels
+from oracle import model_oracle as MO
+from paper_2411_01075_b200 import GpuAssignment, ModelSpec, TrainPlan, assign_unit_shards
+from paper_2411_01075_b200 import step as S
+from paper_2411_01075_b200.data import rank_tokens
+from paper_2411_01075_b200.model import ARCHS, init_flat
+
+
+@pytest.fixture
+def fake(monkeypatch):
+    monkeypatch.setattr(S, "K", fake_kernels)
+    fake_kernels.calls.clear()
+    return fake_kernels
+
+
+def _plan(arch, m, l):
+    model = ModelSpec(arch.layers, arch.unit_params, m * l)
+    return TrainPlan((GpuAssignment("g0", m, l, m * l, 1.0, 0.0, float(model.state_bytes)),),
+                     1.0, 1.0, 2.0 * arch.layers, False, assign_unit_shards([1.0], model))
+
+
+def _units(arch):
+    out = []
+    for u in range(arch.layers + 1):
+        g = torch.Generator().manual_seed(u)
+        out.append(init_flat(arch.root_layout() if u == arch.layers else arch.unit_layout(), g,
+                             "cpu"))
+    return out
+
+
+@pytest.mark.parametrize("m,l", [(2, 1), (1, 3)])
+def test_single_rank_step_gradients(fake, m, l):
+    arch = ARCHS["tiny_gpt"]
+    plan = _plan(arch, m, l)
+    units = _units(arch)
+    tr = S.UnevenFSDPTrainer(arch, plan, 0, device=torch.device("cpu"))
+    tr.load_full_units(units)
+    tok = rank_tokens(plan, 0, arch.seq, arch.vocab, seed=5, step=0)
+    loss = float(tr.step(torch.from_numpy(tok)))
+    gu, gr, ref = MO.weighted_gradient(arch, units[:-1], units[-1], [tok], [(m, l)])
+    assert abs(loss - ref) <= 2e-2 * abs(ref)
+    for u, g in enumerate(gu + [gr]):
+        off, cnt = tr.L.local_range(u)
+        got = tr.g32[off:off + cnt].double()
+        assert float((got - g.double()).norm() / g.double().norm()) <= 2e-2
+    # one accumulate per (unit, microbatch) + head and embedding passes, one AdamW
+    n_acc = fake.calls.count("accumulate")
+    assert n_acc == arch.layers * l + 2 * l
+    assert fake.calls.count("adamw") == 1
+    assert "allgather" not in fake.calls and "reduce_scatter" not in fake.calls
