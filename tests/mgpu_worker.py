@@ -1,0 +1,121 @@
+"""torchrun worker for the multi-GPU parity tests (real kernels + NCCL).
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_worker.py OUT_DIR
+
+Rank r checks the uneven all-gather (bit-exact, every algorithm) and the
+uneven reduce-scatter (fp32, vs the oracle sum) on a set of shard shapes —
+even, ragged-even, single-owner, mixed, zero-count ranks — then runs one
+train step of tiny GPT under a mixed uneven plan and writes its results to
+OUT_DIR/rank{r}.npz for the parent test to compare with the CPU oracle.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import step_oracle as O  # noqa: E402
+from oracle.tolerances import max_rel  # noqa: E402
+from paper_2411_01075_b200 import (GpuAssignment, ModelSpec, TrainPlan,  # noqa: E402
+                                   assign_unit_shards)
+from paper_2411_01075_b200 import hetstep as K  # noqa: E402
+from paper_2411_01075_b200.data import rank_tokens  # noqa: E402
+from paper_2411_01075_b200.model import ARCHS, init_flat  # noqa: E402
+from paper_2411_01075_b200.step import UnevenFSDPTrainer  # noqa: E402
+
+
+def shard_cases(n: int) -> list[list[int]]:
+    cases = [[1000] * n, [1001] * (n - 1) + [999], [4096 * 7 + 3] + [0] * (n - 1),
+             [0] * (n - 1) + [12345], [3_571_623] + [3_516_249] * (n - 1)]
+    rng = np.random.default_rng(n)
+    cases.append([int(x) for x in rng.integers(0, 50_000, size=n)])
+    return [c for c in cases if sum(c) > 0]
+
+
+def offsets(c):
+    return [int(sum(c[:j])) for j in range(len(c))]
+
+
+def main(out_dir: str) -> None:
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ids = [K.unique_id(), K.unique_id()] if rank == 0 else [None, None]
+    dist.broadcast_object_list(ids, src=0)
+    cag, crs = K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
+    report = {}
+    try:
+        for ci, counts in enumerate(shard_cases(world)):
+            offs = offsets(counts)
+            total = sum(counts)
+            full = np.random.default_rng(ci).standard_normal(total).astype(np.float32)
+            bits = O.pack(full)
+            mine = torch.from_numpy(full[offs[rank]:offs[rank] + counts[rank]]).to(dev)
+            send = torch.empty(counts[rank], dtype=torch.bfloat16, device=dev)
+            K.pack_bf16(mine, send)
+            for algo in (K.ALGO_AUTO, K.ALGO_P2P, K.ALGO_OWNER):
+                unit = torch.empty(total, dtype=torch.bfloat16, device=dev)
+                K.allgather_uneven(send, unit, counts, offs, cag, rank, algo)
+                torch.cuda.synchronize()
+                got = unit.view(torch.int16).cpu().numpy().view(np.uint16)
+                report[f"ag{ci}_{algo}"] = int(np.array_equal(got, bits))
+            srcs = [np.random.default_rng(100 * ci + r).standard_normal(total).astype(np.float32)
+                    for r in range(world)]
+            want = O.reduce_scatter(srcs, counts, offs)[rank]
+            for algo in (K.ALGO_AUTO, K.ALGO_OWNER):
+                out = torch.empty(counts[rank], dtype=torch.float32, device=dev)
+                K.reduce_scatter_uneven(torch.from_numpy(srcs[rank]).to(dev), out, counts, offs,
+                                        crs, rank, algo)
+                torch.cuda.synchronize()
+                err = max_rel(out.cpu().numpy(), want) if counts[rank] else 0.0
+                report[f"rs{ci}_{algo}"] = float(err)
+
+        # one train step under a mixed uneven plan with l_i > 1 on some ranks
+        arch = ARCHS["tiny_gpt"]
+        micro = [(2, 2), (1, 3), (3, 1), (0, 0), (2, 1), (1, 1), (4, 1), (1, 2)][:world]
+        if world == 2:
+            micro = [(2, 2), (1, 3)]
+        raw = [683, 341, 0, 512, 100, 7, 300, 81][:world]
+        ratios = [r / sum(raw) for r in raw]
+        ratios[-1] = 1.0 - sum(ratios[:-1])
+        B = sum(m * l for m, l in micro)
+        model = ModelSpec(arch.layers, arch.unit_params, B)
+        plan = TrainPlan(tuple(GpuAssignment(f"g{i}", m, l, m * l, r, 0.0, r * model.state_bytes)
+                               for i, ((m, l), r) in enumerate(zip(micro, ratios))),
+                         1.0, 1.0, 2.0 * arch.layers, True, assign_unit_shards(ratios, model))
+        units = []
+        for u in range(arch.layers + 1):
+            g = torch.Generator().manual_seed(17 + u)
+            units.append(init_flat(arch.root_layout() if u == arch.layers else
+                                   arch.unit_layout(), g, "cpu"))
+        tr = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev)
+        tr.load_full_units(units)
+        tok = rank_tokens(plan, rank, arch.seq, arch.vocab, seed=11, step=0)
+        loss = tr.step(torch.from_numpy(tok).to(dev))
+        dist.all_reduce(loss)
+        g = [t.cpu().numpy() for t in tr.full_units("g32")]
+        p = [t.cpu().numpy() for t in tr.full_units("p32")]
+        torch.cuda.synchronize()
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), loss=float(loss),
+                 micro=np.array(micro), ratios=np.array(ratios),
+                 report_keys=np.array(list(report.keys())),
+                 report_vals=np.array(list(report.values()), dtype=np.float64),
+                 **{f"g{u}": x for u, x in enumerate(g)}, **{f"p{u}": x for u, x in enumerate(p)})
+    finally:
+        cag.close()
+        crs.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

@@ -13,6 +13,8 @@ import torch
 
 from oracle import model_oracle as MO
 from oracle import step_oracle as SO
+from oracle.tolerances import max_rel as _mrel
+from oracle.tolerances import norm_rel as _nrel
 from paper_2411_01075_b200 import GpuAssignment, ModelSpec, TrainPlan, assign_unit_shards
 from paper_2411_01075_b200.data import rank_tokens
 from paper_2411_01075_b200.model import ARCHS, init_flat
@@ -40,16 +42,6 @@ def cpu_units(arch, seed=0):
     return units
 
 
-def _nrel(a, b):
-    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
-    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
-
-
-def _mrel(a, b):
-    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
-    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)))
-
-
 @pytest.mark.parametrize("m,l", [(4, 1), (2, 3)])
 def test_single_gpu_step_matches_cpu_oracle(cuda, m, l):
     arch = ARCHS["tiny_gpt"]
@@ -75,7 +67,8 @@ def test_single_gpu_step_matches_cpu_oracle(cuda, m, l):
                           np.zeros(tr.L.local_len, np.float32), np.zeros(tr.L.local_len, np.float32),
                           step=1, **OPT_D)
     assert _mrel(tr.p32.cpu().numpy(), rp) <= 1e-5
-    assert _mrel(tr.m32.cpu().numpy()[rm != 0], rm[rm != 0]) <= 1e-5
+    assert _mrel(tr.m32.cpu().numpy(), rm) <= 1e-5
+    assert _mrel(tr.v32.cpu().numpy(), rv) <= 1e-5
     shadow = tr.p16.view(torch.int16).cpu().numpy().view(np.uint16)
     assert np.array_equal(shadow, SO.pack(tr.p32.cpu().numpy()))
 
