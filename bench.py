@@ -94,6 +94,20 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def traffic_from_profile(kernel: str, algo_bytes: float):
+    """DRAM bytes per launch of the kernel from the committed ncu --set full
+    summary (profiles/ncu_summary.json), or None when not captured."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())[f"het_{kernel}"]
+        return {"dram_bytes_per_launch": d["dram_bytes"], "config": d.get("config"),
+                "ratio_to_algorithmic_at_capture": d["dram_bytes"] / d["algorithmic_bytes"]}
+    except Exception:
+        return None
+
+
 def setup_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -227,9 +241,7 @@ def main() -> None:
         barrier()
     launches = tr.launches - launches0
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
-    adam_ms = tr.timers.mean_ms("adamw")
-    acc_ms_each = tr.timers.mean_ms("accumulate")
-    acc_n = len(tr.timers.accumulate)
+    kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate")}
     tr.timers.enabled = False
 
     # ---- end to end through the public API with host buffers (e2e) --------
@@ -246,29 +258,10 @@ def main() -> None:
 
     B = plan.total_batch
     hbm, hbm_kind = peaks()
-    # algorithmic bytes: AdamW 30 B/param (p,g,m,v read; p,m,v write; bf16 shadow)
-    adam_bytes = 30.0 * tr.L.local_len
-    acc_elems = sum(arch.unit_params for _ in range(arch.layers)) * tr.l + \
-        arch.root_params * 0  # root accounted below
-    adam_total = adam_ms
-    acc_total = acc_ms_each * acc_n / max(args.steps, 1)
-    # per-launch accumulate bytes: units dominate; FIRST 6 B, ADD 10 B per param
-    first_frac = 1.0 / tr.l if tr.l else 1.0
-    acc_bytes_per_launch = arch.unit_params * (6.0 * first_frac + 10.0 * (1 - first_frac))
-    kernels = {
-        "adamw": {"ms": adam_ms, "bytes": adam_bytes,
-                  "gbs": adam_bytes / (adam_ms * 1e-3) / 1e9 if adam_ms else None},
-        "accumulate": {"ms_per_launch": acc_ms_each, "launches_per_step": acc_n / args.steps,
-                       "bytes_per_launch_unit": acc_bytes_per_launch},
-    }
-    dominant = "adamw" if adam_total >= acc_total else "accumulate"
-    if dominant == "adamw":
-        achieved = kernels["adamw"]["gbs"]
-        traffic = None
-    else:
-        achieved = acc_bytes_per_launch / (acc_ms_each * 1e-3) / 1e9 if acc_ms_each else None
-        traffic = None
-    del acc_elems
+    # dominant owned kernel = the one with the largest share of the timed steps
+    dom = max(kern, key=lambda k: kern[k]["ms_total"])
+    achieved = kern[dom]["gbs"]
+    traffic = traffic_from_profile(dom, kern[dom]["bytes_per_launch"])
 
     if rank == 0:
         cpu = None
@@ -290,10 +283,13 @@ def main() -> None:
                        "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": tok_bytes, "d2h_bytes_per_step": 4 * world},
-            "roofline": {"kernel": f"het_{dominant}", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": f"het_{dom}", "bound": "hbm", "achieved": achieved,
                          "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
-                         "frac": achieved / hbm if achieved else None, "traffic": traffic},
-            "kernels": kernels,
+                         "frac": achieved / hbm if achieved else None, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": kern[dom]["bytes_per_launch"],
+                         "step_share": kern[dom]["ms_total"] / args.steps / ms},
+            "kernels": {k: dict(v, ms_per_step=v["ms_total"] / args.steps)
+                        for k, v in kern.items()},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

@@ -51,22 +51,28 @@ class StepTimers:
     adamw: list = field(default_factory=list)
     accumulate: list = field(default_factory=list)
 
-    def pair(self, kind: str):
+    def pair(self, kind: str, nbytes: float):
+        """Start/end events for one launch moving `nbytes` algorithmic bytes."""
         if not self.enabled:
             return None, None
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        getattr(self, kind).append((a, b))
+        getattr(self, kind).append((a, b, nbytes))
         return a, b
 
     def reset(self) -> None:
         self.adamw.clear()
         self.accumulate.clear()
 
-    def mean_ms(self, kind: str) -> float:
+    def summary(self, kind: str) -> dict:
+        """launches, total ms, algorithmic bytes and GB/s over the recorded launches."""
         ev = getattr(self, kind)
-        if not ev:
-            return 0.0
-        return sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+        ms = [a.elapsed_time(b) for a, b, _ in ev]
+        nbytes = sum(x for _, _, x in ev)
+        tot = sum(ms)
+        return {"launches": len(ev), "ms_total": tot, "ms_mean": tot / len(ev) if ev else 0.0,
+                "bytes_total": nbytes,
+                "bytes_per_launch": nbytes / len(ev) if ev else 0.0,
+                "gbs": nbytes / (tot * 1e-3) / 1e9 if tot > 0 else None}
 
 
 class _NoStream:
@@ -196,7 +202,8 @@ class UnevenFSDPTrainer:
         return self.racc if u == self.L.root else self.acc[u % 2]
 
     def _accumulate(self, acc, grads, names, seg, first):
-        a, b = self.timers.pair("accumulate")
+        n = sum(g.numel() for g in grads)
+        a, b = self.timers.pair("accumulate", n * (6.0 if first else 10.0))
         if a is not None:
             a.record()
         K.accumulate(acc, [(g, seg[nm]) for g, nm in zip(grads, names)], first, self.w)
@@ -310,7 +317,7 @@ class UnevenFSDPTrainer:
 
         # ---- optimizer -------------------------------------------------------
         self.steps += 1
-        a, b = self.timers.pair("adamw")
+        a, b = self.timers.pair("adamw", 30.0 * self.L.local_len)
         if a is not None:
             a.record()
         K.adamw(self.p32, self.g32, self.m32, self.v32, self.p16, lr=self.opt.lr,
