@@ -184,12 +184,14 @@ struct AdamCoef {
   float neg_step;     // -lr / (1 - beta1^t)
 };
 
+// Rounding is pinned with explicit intrinsics (no compiler contraction), so
+// the oracle (oracle/step_oracle.adamw) can mirror it operation for operation.
 __device__ __forceinline__ void adam1(float& p, float g, float& m, float& v, const AdamCoef& c) {
-  p = p * c.decay;
-  m = m + c.one_m_b1 * (g - m);               // exp_avg.lerp_(grad, 1 - beta1)
-  v = v * c.beta2 + c.one_m_b2 * g * g;       // mul_(beta2).addcmul_(g, g, 1 - beta2)
-  const float denom = sqrtf(v) / c.bc2_sqrt + c.eps;
-  p = p + c.neg_step * (m / denom);           // addcdiv_(m, denom, -step_size)
+  p = __fmul_rn(p, c.decay);                                  // p *= 1 - lr*wd
+  m = __fmaf_rn(c.one_m_b1, __fsub_rn(g, m), m);              // m.lerp_(g, 1 - b1)
+  v = __fmaf_rn(__fmul_rn(c.one_m_b2, g), g, __fmul_rn(v, c.beta2));  // v*b2 + (1-b2) g^2
+  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.bc2_sqrt), c.eps);
+  p = __fmaf_rn(c.neg_step, __fdiv_rn(m, denom), p);          // p.addcdiv_(m, denom, -lr/bc1)
 }
 
 template <bool SHADOW>

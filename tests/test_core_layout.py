@@ -1,0 +1,127 @@
+"""Plan contract (JSON schemas, validation, errors) and the per-rank HBM
+layout derived from it. CPU only."""
+import json
+import re
+from pathlib import Path
+
+import pytest
+
+import paper_2411_01075_b200 as H
+from paper_2411_01075_b200.configs import build_job
+from paper_2411_01075_b200.layout import ALIGN, RankLayout, root_shard_plan
+from paper_2411_01075_b200.model import ARCHS
+
+GOLD = Path(__file__).resolve().parent / "golden"
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_plan_json_roundtrip_and_unknown_fields(tmp_path):
+    job = build_job("bert_large", 4)
+    p = tmp_path / "plan.json"
+    H.save_plan(job.plan, p)
+    again = H.load_plan(p)
+    assert H.plan_to_dict(again) == H.plan_to_dict(job.plan)
+    doc = json.loads(p.read_text())
+    doc["surprise"] = 1
+    with pytest.raises(H.InputError, match="unknown fields"):
+        H.plan_from_dict(doc)
+    doc.pop("surprise")
+    doc["assignments"][0]["microbatch"] = 1.5
+    with pytest.raises(H.InputError, match="integer"):
+        H.plan_from_dict(doc)
+
+
+def test_cluster_and_model_schema_errors():
+    with pytest.raises(H.InputError, match="missing"):
+        H.cluster_from_dict({"gpus": []})
+    with pytest.raises(H.InputError, match="non-empty"):
+        H.cluster_from_dict({"gpus": [], "comm": {"allgather_ms": 1, "reducescatter_ms": 1}})
+    with pytest.raises(H.InputError, match="unique"):
+        H.cluster_from_dict({"gpus": [{"id": "a", "memory_gib": 1, "profile_key": "k"}] * 2,
+                             "comm": {"allgather_ms": 1, "reducescatter_ms": 1}})
+    with pytest.raises(H.InputError, match=">= 1"):
+        H.model_from_dict({"layers": 0, "params_per_layer": 1, "global_batch": 1})
+    c = H.cluster_from_dict({"gpus": [{"id": "a", "memory_gib": 1.5, "profile_key": "k"}],
+                             "comm": {"allgather_ms": 1, "reducescatter_ms": 2}})
+    assert c.gpus[0].memory_capacity == int(round(1.5 * 2 ** 30))
+    assert c.mem_cap_fraction == 0.8 and c.comm.uneven_overhead == 0.15
+    assert H.cluster_from_dict(H.cluster_to_dict(c)) == c
+
+
+def test_error_hierarchy():
+    assert issubclass(H.InputError, H.HetplanError)
+    assert issubclass(H.InfeasibleError, H.HetplanError)
+    assert issubclass(H.FitError, H.InputError)
+    assert issubclass(H.SizeGuardError, H.InputError)
+
+
+def test_validator_catches_each_constraint():
+    job = build_job("llama_1b3", 4)
+    mm = job.perf.memory_models()
+    assert H.validate_plan(job.plan, job.cluster, job.model, mm) == []
+    d = H.plan_to_dict(job.plan)
+    d["assignments"][0]["batch"] += 1
+    v = H.validate_plan(H.plan_from_dict(d), job.cluster, job.model, mm)
+    assert {x.constraint for x in v} >= {"I"}
+    d = H.plan_to_dict(job.plan)
+    d["assignments"] = d["assignments"][:-1]
+    with pytest.raises(H.InputError):
+        H.validate_plan(H.plan_from_dict(d), job.cluster, job.model, mm)
+
+
+@pytest.mark.parametrize("case", range(0, 150, 7))
+def test_rank_layouts_partition_every_unit(case):
+    c = json.loads((GOLD / "sharding.json").read_text())["cases"][case]
+    n = len(c["ratios"])
+    md = H.ModelSpec(c["layers"], c["unit_params"], 1)
+    shards = H.assign_unit_shards(c["ratios"], md)
+    root = H.assign_unit_shards(c["ratios"], H.ModelSpec(1, 1000 + case, 1))
+    lays = [RankLayout.build(shards, root, c["unit_params"], 1000 + case, r) for r in range(n)]
+    for u in range(c["layers"] + 1):
+        size = c["unit_params"] if u < c["layers"] else 1000 + case
+        covered = sorted((lay.offsets[u][r], lay.counts[u][r]) for r, lay in enumerate(lays))
+        pos = 0
+        for off, cnt in covered:
+            assert off == pos
+            pos += cnt
+        assert pos == size
+    for lay in lays:
+        assert all(o % ALIGN == 0 for o in lay.local_off)       # 256 B aligned fp32 ranges
+        ends = [o + lay.counts[u][lay.rank] for u, o in enumerate(lay.local_off)]
+        assert all(e <= nxt for e, nxt in zip(ends, list(lay.local_off[1:]) + [lay.local_len]))
+        assert lay.owned_params == sum(cnt[lay.rank] for cnt in lay.counts)
+
+
+def test_layout_rejects_bad_plans():
+    arch = ARCHS["tiny_gpt"]
+    job = build_job("tiny_gpt", 2)
+    with pytest.raises(H.InputError):
+        RankLayout.from_plan(job.plan, arch.unit_params + 1, arch.root_params, 0)
+    with pytest.raises(H.InputError):
+        RankLayout.from_plan(job.plan, arch.unit_params, arch.root_params, 5)
+    rs = root_shard_plan(job.plan, arch.root_params)
+    assert sum(rs.shards[0]) == arch.root_params
+
+
+def test_unit_param_counts_match_survey():
+    # U = 12d^2+13d (GPT/BERT), 4d^2+3 d ffn+2d (Llama)
+    assert ARCHS["tiny_gpt"].unit_params == 789_760
+    assert ARCHS["gpt2_small"].unit_params == 7_087_872
+    assert ARCHS["bert_large"].unit_params == 12_596_224
+    assert ARCHS["llama_1b3"].unit_params == 51_384_320
+
+
+def test_header_symbols_are_exported():
+    """The C-ABI library loads on a CPU-only host and exports every entry
+    point include/hetstep.h declares (no compute calls without a GPU)."""
+    import ctypes
+
+    from paper_2411_01075_b200 import _build, hetstep
+    lib = ctypes.CDLL(str(_build.build_step()))
+    hdr = (ROOT / "include" / "hetstep.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(het_\w+)\(", hdr, re.M))
+    assert declared == set(hetstep.EXPORTS)
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    lib.het_version.restype = ctypes.c_char_p
+    assert lib.het_version().decode().startswith("hetstep")
