@@ -66,11 +66,13 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
 /* (5) sharded AdamW over one rank's flat local shard (torch.optim.AdamW
  * formula, decoupled weight decay). Optional bf16 shadow write (the next
  * step's all-gather send buffer; fuses kernel (1)). 28 B/param, 30 with
- * shadow. step >= 1. Replaces: the paper's per-GPU Adam on the FSDP shard
+ * shadow. step >= 1. Hyper-parameters are doubles: the fp32 coefficients
+ * (1-b1, 1-b2, lr/(1-b1^t), ...) are derived in double exactly as torch
+ * derives them from Python floats. Replaces: the paper's per-GPU Adam on the FSDP shard
  * (core.py:151-154 "16 B/param"). */
 int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
-              float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
-              void* stream);
+              double lr, double beta1, double beta2, double eps, double weight_decay,
+              int64_t step, void* stream);
 
 /* fill / zero helpers used by the step driver (idle ranks, pads) */
 int het_fill_f32(float* dst, float value, int64_t n, void* stream);

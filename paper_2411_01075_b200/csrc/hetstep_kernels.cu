@@ -310,23 +310,23 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
 }
 
 int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
-              float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
-              void* stream) {
+              double lr, double beta1, double beta2, double eps, double weight_decay,
+              int64_t step, void* stream) {
   if (n < 0 || step < 1 || (n > 0 && (!p || !g || !m || !v)))
     return fail(HET_EARG, "het_adamw: bad args (n=%lld step=%lld)", (long long)n,
                 (long long)step);
   if (n == 0) return HET_OK;
   // scalar coefficients in double, as torch's _single_tensor_adamw computes them
-  const double bc1 = 1.0 - std::pow(static_cast<double>(beta1), static_cast<double>(step));
-  const double bc2 = 1.0 - std::pow(static_cast<double>(beta2), static_cast<double>(step));
+  const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
   AdamCoef c;
-  c.decay = static_cast<float>(1.0 - static_cast<double>(lr) * weight_decay);
-  c.one_m_b1 = static_cast<float>(1.0 - static_cast<double>(beta1));
-  c.beta2 = beta2;
-  c.one_m_b2 = static_cast<float>(1.0 - static_cast<double>(beta2));
+  c.decay = static_cast<float>(1.0 - lr * weight_decay);
+  c.one_m_b1 = static_cast<float>(1.0 - beta1);
+  c.beta2 = static_cast<float>(beta2);
+  c.one_m_b2 = static_cast<float>(1.0 - beta2);
   c.bc2_sqrt = static_cast<float>(std::sqrt(bc2));
-  c.eps = eps;
-  c.neg_step = static_cast<float>(-(static_cast<double>(lr) / bc1));
+  c.eps = static_cast<float>(eps);
+  c.neg_step = static_cast<float>(-(lr / bc1));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec = n % 4 == 0 && aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
                    (!p_bf16_or_null || (reinterpret_cast<uintptr_t>(p_bf16_or_null) & 7) == 0);

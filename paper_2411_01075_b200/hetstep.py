@@ -41,13 +41,14 @@ def load(build: bool = False) -> ctypes.CDLL:
     if build or not STEP_LIB.exists():
         build_step()
     lib = ctypes.CDLL(str(STEP_LIB))
-    vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    f32, f64 = ctypes.c_float, ctypes.c_double
     sig = {
         "het_version": ([], ctypes.c_char_p),
         "het_last_error": ([], ctypes.c_char_p),
         "het_pack_bf16": ([vp, vp, i64, vp], i32),
         "het_accumulate": ([vp, ctypes.POINTER(HetSeg), i32, i32, f32, vp], i32),
-        "het_adamw": ([vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, i64, vp], i32),
+        "het_adamw": ([vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, i64, vp], i32),
         "het_fill_f32": ([vp, f32, i64, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
