@@ -110,6 +110,45 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
                               const int64_t* offsets, int nranks, int rank, int algo,
                               void* comm, void* stream);
 
+/* ---- fused collectives on a symmetric buffer (NVLS multicast / peer) ---- */
+
+#define HET_MAX_RANKS 8
+#define HET_SYMM_MAX_CTAS 64
+#define HET_SYMM_CHANNELS 2   /* independent barrier channels: 0 = AG stream, 1 = RS stream */
+#define HET_SYMM_TIMEOUT 17   /* het_symm_status(): a cross-rank barrier timed out */
+
+/* A buffer allocated at the same byte layout on every rank (torch symmetric
+ * memory is the plumbing): peer_base[j] = its address on rank j mapped into
+ * this process (UVA peer mapping), mc_base = NVLS multicast address or 0.
+ * signal_off = byte offset of a zeroed area of het_symm_signal_bytes(). */
+typedef struct {
+  int32_t nranks;
+  int32_t rank;
+  uint64_t peer_base[HET_MAX_RANKS];
+  uint64_t mc_base;
+  uint64_t signal_off;
+} het_symm_t;
+
+int64_t het_symm_signal_bytes(void);
+/* Sticky device status of the symmetric kernels (0 or HET_SYMM_TIMEOUT). */
+int het_symm_status(int reset);
+
+/* (1)+(2) fused: rank r rounds its fp32 master range src[0:counts[r]] to bf16
+ * and stores it at unit_off + 2*offsets[r] on EVERY rank with one multicast
+ * store (NVLS) or per-peer stores. In-kernel start/end barriers; `epoch`
+ * must increase by one per call on `channel` on every rank. */
+int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit_off,
+                            const int64_t* counts, const int64_t* offsets, uint32_t epoch,
+                            int channel, int ctas, void* stream);
+
+/* (3) fused: out[0:counts[r]] = sum_j acc_j[offsets[r] : +counts[r]] where
+ * acc_j is the fp32 accumulator at acc_off on rank j (already Eq. 1-scaled),
+ * summed in the switch by multimem.ld_reduce (or peer loads). end_barrier=1
+ * additionally waits until every rank finished reading this rank's acc. */
+int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
+                            const int64_t* counts, const int64_t* offsets, uint32_t epoch,
+                            int channel, int end_barrier, int ctas, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,300 @@
+// Fused uneven collectives over NVLink 5 / NVSwitch on a symmetric buffer
+// (same byte offset on every rank; peer-mapped and, when the fabric supports
+// it, bound to an NVLS multicast object).
+//
+//   het_symm_allgather_pack  — rank r reads its fp32 master range, rounds to
+//     bf16 and stores it ONCE through the multicast address: the switch
+//     replicates it into every rank's gathered unit (owner egress = s_r, not
+//     (N-1) s_r). Fuses kernel (1) "pack" with collective (2).
+//   het_symm_reduce_scatter  — rank r reads its own range of the unit
+//     accumulator with multimem.ld_reduce: the switch sums the N ranks' (Eq. 1
+//     pre-scaled) fp32 accumulators in flight and returns one stream, which
+//     is written straight into r's fp32 grad shard. Collective (3) as a
+//     single kernel, no staging.
+//   Without multicast both fall back to peer-pointer stores/loads in the same
+//   kernel (push AG, pull RS).
+//
+// Synchronisation is in-kernel: CTA b of every rank meets CTA b of every
+// other rank on a per-(channel, kind, cta, src) signal slot carrying a
+// monotonically increasing epoch (release/acquire at system scope). The
+// start barrier orders "every rank finished producing / released the buffer"
+// before the first remote access; the end barrier orders "all stores
+// landed" (AG) or "all peers finished reading" (RS, optional). Spins are
+// bounded: on timeout the kernel records HET_SYMM_TIMEOUT and exits instead of
+// hanging the GPU.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hetstep.h"
+#include "hetstep_internal.cuh"
+
+using het::fail;
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
+constexpr long long kSpinLimit = 1ll << 31;   // ~ seconds of polling
+
+__device__ int g_symm_status = 0;
+
+struct Args {
+  het_symm_t s;
+  uint64_t data_off;       // byte offset of the unit (AG: bf16 unit, RS: fp32 acc)
+  int64_t count;           // this rank's element count
+  int64_t offset;          // this rank's element offset inside the unit
+  uint32_t epoch;
+  int channel;
+  int end_barrier;
+};
+
+__device__ __forceinline__ uint32_t* slot(const het_symm_t& s, int owner, int channel, int kind,
+                                          int cta, int src) {
+  const uint64_t idx =
+      ((static_cast<uint64_t>(channel) * 2 + kind) * kMaxCtas + cta) * HET_MAX_RANKS + src;
+  return reinterpret_cast<uint32_t*>(s.peer_base[owner] + s.signal_off + idx * 4);
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// CTA-pairwise cross-rank barrier (see file comment).
+__device__ void cross_barrier(const het_symm_t& s, int channel, int kind, uint32_t epoch) {
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < s.nranks) {
+    __threadfence_system();
+    st_release_sys(slot(s, t, channel, kind, blockIdx.x, s.rank), epoch);
+    const uint32_t* mine = slot(s, s.rank, channel, kind, blockIdx.x, t);
+    long long spins = 0;
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+      if (++spins > kSpinLimit) {
+        atomicExch(&g_symm_status, HET_SYMM_TIMEOUT);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void mc_st_v4(uint64_t addr, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr),
+               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+               "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+__device__ __forceinline__ void mc_st_b32(uint64_t addr, uint32_t v) {
+  asm volatile("multimem.st.relaxed.sys.global.bf16x2 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ float4 mc_ldr_v4(uint64_t addr) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(addr)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ float mc_ldr_f32(uint64_t addr) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];"
+               : "=f"(r)
+               : "l"(addr)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---------------------------------------------------------------- all-gather
+
+__global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restrict__ src,
+                                                           const Args a) {
+  const het_symm_t& s = a.s;
+  cross_barrier(s, a.channel, 0, a.epoch);   // every rank released its copy of the unit
+  const int64_t n = a.count;
+  const uint64_t dst0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;  // byte offset
+  const bool mc = s.mc_base != 0;
+  // element ranges: [0,h1) 2-byte edge, [h1,h2) 4-byte words, body 16-byte vectors, tail
+  int64_t h1 = (dst0 & 3) ? 1 : 0;
+  if (h1 > n) h1 = n;
+  int64_t h2 = h1 + static_cast<int64_t>(((16 - ((dst0 + h1 * 2) & 15)) & 15) / 2);
+  if (h2 > n) h2 = n;
+  const int64_t nvec = (n - h2) / 8;
+  const int64_t body_end = h2 + nvec * 8;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  // body: 8 bf16 per 16-byte multicast store
+  for (int64_t v = gtid; v < nvec; v += gsz) {
+    const int64_t e = h2 + v * 8;
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = src[e + i];
+    const uint4 w = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+    const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
+    if (mc) {
+      mc_st_v4(s.mc_base + off, w);
+    } else {
+      for (int p = 0; p < s.nranks; ++p)
+        *reinterpret_cast<uint4*>(s.peer_base[p] + off) = w;
+    }
+  }
+  // edges (CTA 0): 4-byte pairs via multicast, a lone 2-byte element via peer stores
+  if (blockIdx.x == 0) {
+    auto pair = [&](int64_t e) {
+      const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
+      const uint32_t w = pack_bf16x2(src[e], src[e + 1]);
+      if (mc)
+        mc_st_b32(s.mc_base + off, w);
+      else
+        for (int p = 0; p < s.nranks; ++p) *reinterpret_cast<uint32_t*>(s.peer_base[p] + off) = w;
+    };
+    auto single = [&](int64_t e) {
+      const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
+      const __nv_bfloat16 h = __float2bfloat16_rn(src[e]);
+      for (int p = 0; p < s.nranks; ++p) *reinterpret_cast<__nv_bfloat16*>(s.peer_base[p] + off) = h;
+    };
+    const int t = threadIdx.x;
+    if (t == 0 && h1 == 1) single(0);
+    for (int64_t e = h1 + 2 * t; e + 1 < h2; e += 2 * blockDim.x) pair(e);
+    if (t == 0 && (h2 - h1) % 2 == 1) single(h2 - 1);
+    // tail after the body: pairs from an even (4-byte aligned) start, then a lone element
+    for (int64_t e = body_end + 2 * t; e + 1 < n; e += 2 * blockDim.x) pair(e);
+    if (t == 0 && (n - body_end) % 2 == 1) single(n - 1);
+  }
+  cross_barrier(s, a.channel, 1, a.epoch);   // every rank's stores have landed
+}
+
+// ---------------------------------------------------------------- reduce-scatter
+
+__global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const Args a) {
+  const het_symm_t& s = a.s;
+  cross_barrier(s, a.channel, 0, a.epoch);   // every rank's accumulator is final
+  const int64_t n = a.count;
+  const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 4;
+  const bool mc = s.mc_base != 0;
+  int64_t head = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / 4);
+  if (head > n) head = n;
+  const int64_t nvec = (n - head) / 4;
+  const int64_t body_end = head + nvec * 4;
+  const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t v = gtid; v < nvec; v += gsz) {
+    const int64_t e = head + v * 4;
+    const uint64_t off = src0 + static_cast<uint64_t>(e) * 4;
+    float4 r;
+    if (mc) {
+      r = mc_ldr_v4(s.mc_base + off);
+    } else {
+      r = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 0; p < s.nranks; ++p) {
+        const float4 x = *reinterpret_cast<const float4*>(s.peer_base[p] + off);
+        r.x += x.x;
+        r.y += x.y;
+        r.z += x.z;
+        r.w += x.w;
+      }
+    }
+    if (out_vec) {
+      *reinterpret_cast<float4*>(out + e) = r;
+    } else {
+      out[e] = r.x;
+      out[e + 1] = r.y;
+      out[e + 2] = r.z;
+      out[e + 3] = r.w;
+    }
+  }
+  if (blockIdx.x == 0) {
+    auto one = [&](int64_t e) {
+      const uint64_t off = src0 + static_cast<uint64_t>(e) * 4;
+      float r = 0.f;
+      if (mc) {
+        r = mc_ldr_f32(s.mc_base + off);
+      } else {
+        for (int p = 0; p < s.nranks; ++p) r += *reinterpret_cast<const float*>(s.peer_base[p] + off);
+      }
+      out[e] = r;
+    };
+    for (int64_t e = threadIdx.x; e < head; e += blockDim.x) one(e);
+    for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
+  }
+  if (a.end_barrier) cross_barrier(s, a.channel, 1, a.epoch);  // peers done reading my acc
+}
+
+int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offsets, int ctas) {
+  if (!s || s->nranks < 1 || s->nranks > HET_MAX_RANKS || s->rank < 0 || s->rank >= s->nranks)
+    return fail(HET_EARG, "het_symm: bad rank table");
+  if (!counts || !offsets) return fail(HET_EARG, "het_symm: null shard table");
+  if (ctas < 1 || ctas > kMaxCtas) return fail(HET_EARG, "het_symm: ctas must be 1..%d", kMaxCtas);
+  int64_t pos = 0;
+  for (int j = 0; j < s->nranks; ++j) {
+    if (counts[j] < 0 || offsets[j] != pos)
+      return fail(HET_EARG, "het_symm: shard table not contiguous at rank %d", j);
+    pos += counts[j];
+  }
+  for (int j = 0; j < s->nranks; ++j)
+    if (!s->peer_base[j]) return fail(HET_EARG, "het_symm: missing peer base %d", j);
+  return HET_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t het_symm_signal_bytes(void) {
+  return static_cast<int64_t>(HET_SYMM_CHANNELS) * 2 * kMaxCtas * HET_MAX_RANKS * 4;
+}
+
+int het_symm_status(int reset) {
+  int v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_symm_status, sizeof(int)) != cudaSuccess)
+    return fail(HET_ECUDA, "het_symm_status: %s", cudaGetErrorString(cudaGetLastError()));
+  if (reset) {
+    const int z = 0;
+    cudaMemcpyToSymbol(g_symm_status, &z, sizeof(int));
+  }
+  return v;
+}
+
+int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit_off,
+                            const int64_t* counts, const int64_t* offsets, uint32_t epoch,
+                            int channel, int ctas, void* stream) {
+  int rc = check_symm(s, counts, offsets, ctas);
+  if (rc != HET_OK) return rc;
+  if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
+  if (counts[s->rank] > 0 && !src) return fail(HET_EARG, "het_symm_allgather_pack: null src");
+  if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
+  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1};
+  symm_ag_kernel<<<ctas, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, a);
+  return het::check_launch("het_symm_allgather_pack");
+}
+
+int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
+                            const int64_t* counts, const int64_t* offsets, uint32_t epoch,
+                            int channel, int end_barrier, int ctas, void* stream) {
+  int rc = check_symm(s, counts, offsets, ctas);
+  if (rc != HET_OK) return rc;
+  if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
+  if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter: null out");
+  if (acc_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter: acc offset not 16B aligned");
+  Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
+  symm_rs_kernel<<<ctas, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(out, a);
+  return het::check_launch("het_symm_reduce_scatter");
+}
+
+}  // extern "C"

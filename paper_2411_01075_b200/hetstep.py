@@ -20,14 +20,25 @@ HET_MAX_SEGS = 64
 ACC_ADD, ACC_FIRST = 0, 1
 DT_BF16, DT_F32 = 0, 1
 ALGO_AUTO, ALGO_P2P, ALGO_OWNER, ALGO_EVEN = 0, 1, 2, 3
+ALGO_SYMM = 4            # fused kernels on a symmetric buffer (NVLS multicast / peer)
+HET_MAX_RANKS = 8
+HET_SYMM_MAX_CTAS = 64
+HET_SYMM_TIMEOUT = 17
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
-           "het_allgather_uneven", "het_reduce_scatter_uneven")
+           "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
+           "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
 
 class HetSeg(ctypes.Structure):
     _fields_ = [("src", ctypes.c_void_p), ("dst_off", ctypes.c_int64), ("n", ctypes.c_int64)]
+
+
+class HetSymm(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("peer_base", ctypes.c_uint64 * HET_MAX_RANKS), ("mc_base", ctypes.c_uint64),
+                ("signal_off", ctypes.c_uint64)]
 
 
 _lib: ctypes.CDLL | None = None
@@ -57,6 +68,14 @@ def load(build: bool = False) -> ctypes.CDLL:
                                   i32, vp, vp], i32),
         "het_reduce_scatter_uneven": ([vp, vp, ctypes.POINTER(i64), ctypes.POINTER(i64), i32, i32,
                                        i32, vp, vp], i32),
+        "het_symm_signal_bytes": ([], i64),
+        "het_symm_status": ([i32], i32),
+        "het_symm_allgather_pack": ([ctypes.POINTER(HetSymm), vp, ctypes.c_uint64,
+                                     ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
+                                     i32, i32, vp], i32),
+        "het_symm_reduce_scatter": ([ctypes.POINTER(HetSymm), ctypes.c_uint64, vp,
+                                     ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
+                                     i32, i32, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -207,3 +226,87 @@ def reduce_scatter_uneven(src: torch.Tensor, shard: torch.Tensor, counts: Sequen
         _cuda(shard, torch.float32, "shard") if shard.numel() else None,
         _i64(counts), _i64(offsets), n, rank, algo, comm.handle if comm else None,
         _stream(stream)), "het_reduce_scatter_uneven")
+
+
+# ---------------------------------------------------------------------------
+# symmetric workspace + fused collectives
+
+SYMM_ALIGN = 256
+
+
+class SymmWorkspace:
+    """One allocation with the same layout on every rank (torch symmetric
+    memory = plumbing: allocation, peer mapping, NVLS multicast binding),
+    carved into named typed regions plus the barrier signal area. The fused
+    kernels address regions by byte offset from the peer / multicast bases."""
+
+    def __init__(self, regions: Sequence[tuple[str, int, torch.dtype]], group_name: str,
+                 device: torch.device, rank: int, nranks: int, ctas: int = 32,
+                 use_multicast: bool = True):
+        import torch.distributed._symmetric_memory as symm
+        if nranks > HET_MAX_RANKS:
+            raise InputError(f"symmetric collectives support up to {HET_MAX_RANKS} ranks")
+        lib = load()
+        self.offsets: dict[str, int] = {}
+        pos = 0
+        for name, numel, dtype in regions:
+            self.offsets[name] = pos
+            pos += (numel * torch.tensor([], dtype=dtype).element_size() + SYMM_ALIGN - 1) \
+                // SYMM_ALIGN * SYMM_ALIGN
+        self.signal_off = pos
+        total = pos + int(lib.het_symm_signal_bytes())
+        self.raw = symm.empty(total, dtype=torch.uint8, device=device)
+        self.raw.zero_()
+        self.handle = symm.rendezvous(self.raw, group_name)
+        base_off = int(getattr(self.handle, "offset", 0) or 0)
+        peers = [int(p) + base_off for p in self.handle.buffer_ptrs]
+        mc = 0
+        if use_multicast and self.handle.has_multicast_support():
+            mc = int(self.handle.multicast_ptr) + base_off
+        self.multicast = mc != 0
+        d = HetSymm()
+        d.nranks, d.rank = nranks, rank
+        for j, p in enumerate(peers):
+            d.peer_base[j] = p
+        d.mc_base = mc
+        d.signal_off = self.signal_off
+        self.desc = d
+        self.views: dict[str, torch.Tensor] = {}
+        for name, numel, dtype in regions:
+            o = self.offsets[name]
+            nbytes = numel * torch.tensor([], dtype=dtype).element_size()
+            self.views[name] = self.raw[o:o + nbytes].view(dtype)
+        self.epoch = [0, 0]
+        self.ctas = ctas
+        torch.cuda.synchronize(device)
+        self.handle.barrier()
+
+    def __getitem__(self, name: str) -> torch.Tensor:
+        return self.views[name]
+
+    def allgather_pack(self, src_f32: torch.Tensor, region: str, elem_off: int,
+                       counts: Sequence[int], offsets: Sequence[int], stream=None) -> None:
+        """bf16 unit at `region`[elem_off:] <- every rank's fp32 range (fused pack+AG)."""
+        self.epoch[0] += 1
+        src = _cuda(src_f32, torch.float32, "src") if src_f32.numel() else None
+        byte_off = self.offsets[region] + 2 * elem_off
+        _check(load().het_symm_allgather_pack(ctypes.byref(self.desc), src, byte_off,
+                                              _i64(counts), _i64(offsets), self.epoch[0], 0,
+                                              self.ctas, _stream(stream)),
+               "het_symm_allgather_pack")
+
+    def reduce_scatter(self, region: str, elem_off: int, out: torch.Tensor,
+                       counts: Sequence[int], offsets: Sequence[int], end_barrier: bool = False,
+                       stream=None) -> None:
+        """out <- sum over ranks of the fp32 accumulator at `region`[elem_off:] (my range)."""
+        self.epoch[1] += 1
+        o = _cuda(out, torch.float32, "out") if out.numel() else None
+        byte_off = self.offsets[region] + 4 * elem_off
+        _check(load().het_symm_reduce_scatter(ctypes.byref(self.desc), byte_off, o, _i64(counts),
+                                              _i64(offsets), self.epoch[1], 1, int(end_barrier),
+                                              self.ctas, _stream(stream)),
+               "het_symm_reduce_scatter")
+
+    @staticmethod
+    def status(reset: bool = False) -> int:
+        return int(load().het_symm_status(int(reset)))

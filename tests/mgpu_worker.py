@@ -80,6 +80,38 @@ def main(out_dir: str) -> None:
                 err = max_rel(out.cpu().numpy(), want) if counts[rank] else 0.0
                 report[f"rs{ci}_{algo}"] = float(err)
 
+        # fused symmetric-memory collectives (NVLS multicast when available, then peer)
+        maxu = max(sum(c) for c in shard_cases(world)) + 64
+        for use_mc in (True, False):
+            ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32)],
+                                 dist.group.WORLD.group_name, dev, rank, world,
+                                 use_multicast=use_mc)
+            report[f"symm_mc_available_{int(use_mc)}"] = float(ws.multicast)
+            for ci, counts in enumerate(shard_cases(world)):
+                offs = offsets(counts)
+                total = sum(counts)
+                full = np.random.default_rng(ci).standard_normal(total).astype(np.float32)
+                mine = torch.from_numpy(full[offs[rank]:offs[rank] + counts[rank]]).to(dev)
+                for shift in (0, 3):        # unit placed at an odd element offset too
+                    ws["unit"].zero_()
+                    ws.allgather_pack(mine, "unit", 8 * shift, counts, offs)
+                    torch.cuda.synchronize()
+                    got = ws["unit"][8 * shift:8 * shift + total].view(torch.int16).cpu().numpy()
+                    report[f"symm_ag{ci}_{int(use_mc)}_{shift}"] = int(
+                        np.array_equal(got.view(np.uint16), O.pack(full)))
+                srcs = [np.random.default_rng(100 * ci + r).standard_normal(total).astype(np.float32)
+                        for r in range(world)]
+                want = O.reduce_scatter(srcs, counts, offs)[rank]
+                ws["acc"][:total].copy_(torch.from_numpy(srcs[rank]))
+                out = torch.empty(counts[rank], dtype=torch.float32, device=dev)
+                ws.reduce_scatter("acc", 0, out, counts, offs, end_barrier=True)
+                torch.cuda.synchronize()
+                report[f"symm_rs{ci}_{int(use_mc)}"] = float(
+                    max_rel(out.cpu().numpy(), want) if counts[rank] else 0.0)
+            report[f"symm_status_{int(use_mc)}"] = float(K.SymmWorkspace.status(reset=True))
+            dist.barrier()
+            del ws
+
         # one train step under a mixed uneven plan with l_i > 1 on some ranks
         arch = ARCHS["tiny_gpt"]
         micro = [(2, 2), (1, 3), (3, 1), (0, 0), (2, 1), (1, 1), (4, 1), (1, 2)][:world]

@@ -119,7 +119,7 @@ def test_header_symbols_are_exported():
     from paper_2411_01075_b200 import _build, hetstep
     lib = ctypes.CDLL(str(_build.build_step()))
     hdr = (ROOT / "include" / "hetstep.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(het_\w+)\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(het_\w+)\(", hdr, re.M))
     assert declared == set(hetstep.EXPORTS)
     for sym in declared:
         assert hasattr(lib, sym), sym

@@ -41,10 +41,12 @@ def test_multigpu_collectives_and_step(tmp_path):
     r = [np.load(tmp_path / f"rank{i}.npz") for i in range(world)]
     for d in r:
         for k, v in zip(d["report_keys"], d["report_vals"]):
-            if k.startswith("ag"):
+            if k.startswith("ag") or k.startswith("symm_ag"):
                 assert v == 1.0, f"all-gather {k} not bit-exact"
-            else:
+            elif k.startswith("rs") or k.startswith("symm_rs"):
                 assert v <= FP32_RTOL, f"reduce-scatter {k}: {v}"
+            elif k.startswith("symm_status"):
+                assert v == 0.0, f"symmetric barrier timed out ({k})"
     arch = ARCHS["tiny_gpt"]
     micro = [tuple(int(x) for x in mi) for mi in r[0]["micro"]]
     ratios = [float(x) for x in r[0]["ratios"]]
