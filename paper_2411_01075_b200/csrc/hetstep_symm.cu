@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
-constexpr long long kSpinLimit = 1ll << 31;   // ~ seconds of polling
+constexpr uint64_t kSpinTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s wall clock
 
 __device__ int g_symm_status = 0;
 
@@ -60,6 +60,12 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -74,9 +80,9 @@ __device__ void cross_barrier(const het_symm_t& s, int channel, int kind, uint32
     __threadfence_system();
     st_release_sys(slot(s, t, channel, kind, blockIdx.x, s.rank), epoch);
     const uint32_t* mine = slot(s, s.rank, channel, kind, blockIdx.x, t);
-    long long spins = 0;
+    const uint64_t t0 = globaltimer_ns();
     while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
-      if (++spins > kSpinLimit) {
+      if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
         atomicExch(&g_symm_status, HET_SYMM_TIMEOUT);
         break;
       }
