@@ -30,7 +30,8 @@ sys.path.insert(0, str(ROOT))
 from paper_2411_01075_b200 import hetstep as K  # noqa: E402
 from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
-ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER}
+ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
+         "symm": "symm", "symm_peer": "symm_peer"}
 
 
 def skew_counts(skew: str, total: int, n: int) -> list[int]:
@@ -84,10 +85,11 @@ def main() -> None:
     ap.add_argument("--sizes-mb", type=float, nargs="*", default=[1, 4, 16, 64, 256, 1024])
     ap.add_argument("--skews", nargs="*",
                     default=["even", "two_to_one", "geometric", "single_owner", "planner"])
-    ap.add_argument("--algos", nargs="*", default=["auto", "owner", "p2p"])
+    ap.add_argument("--algos", nargs="*", default=["auto", "owner", "p2p", "symm", "symm_peer"])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--planner-config", default="llama_1b3")
+    ap.add_argument("--ctas", type=int, default=32)
     args = ap.parse_args()
 
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), \
@@ -101,6 +103,16 @@ def main() -> None:
     job = build_job(args.planner_config, world)
     planner_ratio = [a.state_ratio for a in job.plan.assignments]
     best: dict[str, float] = {}
+    maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
+    ws = {}
+    for an, mc in (("symm", True), ("symm_peer", False)):
+        if an in args.algos:
+            ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
+                                                                         torch.float32)],
+                                     dist.group.WORLD.group_name, dev, rank, world,
+                                     ctas=args.ctas, use_multicast=mc)
+            if rank == 0:
+                print(json.dumps({"workspace": an, "multicast": ws[an].multicast}), flush=True)
     try:
         for op in ("allgather", "reduce_scatter"):
             esize = 2 if op == "allgather" else 4
@@ -117,9 +129,16 @@ def main() -> None:
                         algo = ALGOS[an]
                         if op == "reduce_scatter" and algo == K.ALGO_P2P:
                             continue
-                        if an == "auto" and len(set(c)) > 1:
-                            pass  # auto == owner on uneven units
-                        if op == "allgather":
+                        if isinstance(algo, str):
+                            w = ws[algo]
+                            if op == "allgather":
+                                src32 = torch.randn(c[rank], device=dev)
+                                fn = lambda: w.allgather_pack(src32, "unit", 0, c, o)  # noqa: E731
+                            else:
+                                w["acc"][:total].normal_()
+                                out = torch.empty(c[rank], device=dev)
+                                fn = lambda: w.reduce_scatter("acc", 0, out, c, o)  # noqa: E731
+                        elif op == "allgather":
                             send = torch.randn(c[rank], device=dev).to(torch.bfloat16)
                             unit = torch.empty(total, dtype=torch.bfloat16, device=dev)
                             fn = lambda: K.allgather_uneven(send, unit, c, o, comm, rank, algo)  # noqa: E731
@@ -141,8 +160,10 @@ def main() -> None:
                                               "bus_gbs": bus, "nccl_tests_bus_gbs": nccl_bus,
                                               "counts": c if world <= 8 else None}), flush=True)
                         del fn
+        status = K.SymmWorkspace.status() if ws else 0
         if rank == 0:
             print(json.dumps({"summary": "best bus GB/s at >= 256 MB", "n_gpus": world,
+                              "symm_status": status,
                               "best": best,
                               "frac_of_770": {k: v / 770.0 for k, v in best.items()}}),
                   flush=True)

@@ -113,7 +113,7 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
 /* ---- fused collectives on a symmetric buffer (NVLS multicast / peer) ---- */
 
 #define HET_MAX_RANKS 8
-#define HET_SYMM_MAX_CTAS 64
+#define HET_SYMM_MAX_CTAS 256
 #define HET_SYMM_CHANNELS 2   /* independent barrier channels: 0 = AG stream, 1 = RS stream */
 #define HET_SYMM_TIMEOUT 17   /* het_symm_status(): a cross-rank barrier timed out */
 

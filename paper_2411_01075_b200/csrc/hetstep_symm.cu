@@ -34,6 +34,7 @@ using het::fail;
 namespace {
 
 constexpr int kThreads = 512;
+constexpr int kUnroll = 8;                   // independent 16-byte remote ops per thread
 constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
 constexpr uint64_t kSpinTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s wall clock
 
@@ -49,11 +50,11 @@ struct Args {
   int end_barrier;
 };
 
-__device__ __forceinline__ uint32_t* slot(const het_symm_t& s, int owner, int channel, int kind,
-                                          int cta, int src) {
+__device__ __forceinline__ uint32_t* slot(uint64_t owner_base, uint64_t signal_off, int channel,
+                                          int kind, int cta, int src) {
   const uint64_t idx =
       ((static_cast<uint64_t>(channel) * 2 + kind) * kMaxCtas + cta) * HET_MAX_RANKS + src;
-  return reinterpret_cast<uint32_t*>(s.peer_base[owner] + s.signal_off + idx * 4);
+  return reinterpret_cast<uint32_t*>(owner_base + signal_off + idx * 4);
 }
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -72,14 +73,30 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+// Copy the peer table from parameter space with compile-time indices (a
+// dynamic index into a kernel parameter would force a local-memory copy).
+#define HET_STAGE_PEERS(args, peer)                                   \
+  do {                                                                \
+    _Pragma("unroll") for (int i_ = 0; i_ < HET_MAX_RANKS; ++i_)       \
+      if (threadIdx.x == i_) (peer)[i_] = (args).s.peer_base[i_];       \
+  } while (0)
+
 // CTA-pairwise cross-rank barrier (see file comment).
-__device__ void cross_barrier(const het_symm_t& s, int channel, int kind, uint32_t epoch) {
+// Scalar view of het_symm_t held in registers (the peer table lives in smem).
+struct Sym {
+  int nranks, rank;
+  uint64_t mc_base, signal_off;
+};
+
+// `peer` is the CTA's shared copy of the peer base table.
+__device__ void cross_barrier(const Sym& s, const uint64_t* peer, int channel, int kind,
+                              uint32_t epoch) {
   __syncthreads();
   const int t = threadIdx.x;
   if (t < s.nranks) {
     __threadfence_system();
-    st_release_sys(slot(s, t, channel, kind, blockIdx.x, s.rank), epoch);
-    const uint32_t* mine = slot(s, s.rank, channel, kind, blockIdx.x, t);
+    st_release_sys(slot(peer[t], s.signal_off, channel, kind, blockIdx.x, s.rank), epoch);
+    const uint32_t* mine = slot(peer[s.rank], s.signal_off, channel, kind, blockIdx.x, t);
     const uint64_t t0 = globaltimer_ns();
     while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
       if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
@@ -106,8 +123,7 @@ __device__ __forceinline__ float4 mc_ldr_v4(uint64_t addr) {
   float4 r;
   asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "l"(addr)
-               : "memory");
+               : "l"(addr));
   return r;
 }
 
@@ -127,13 +143,16 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 // ---------------------------------------------------------------- all-gather
 
+template <bool MC>
 __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restrict__ src,
-                                                           const Args a) {
-  const het_symm_t& s = a.s;
-  cross_barrier(s, a.channel, 0, a.epoch);   // every rank released its copy of the unit
+                                                           const __grid_constant__ Args a) {
+  __shared__ uint64_t peer[HET_MAX_RANKS];
+  HET_STAGE_PEERS(a, peer);
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off};
+  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank released its copy of the unit
   const int64_t n = a.count;
   const uint64_t dst0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;  // byte offset
-  const bool mc = s.mc_base != 0;
+  const int nr = s.nranks;
   // element ranges: [0,h1) 2-byte edge, [h1,h2) 4-byte words, body 16-byte vectors, tail
   int64_t h1 = (dst0 & 3) ? 1 : 0;
   if (h1 > n) h1 = n;
@@ -143,20 +162,41 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
   const int64_t body_end = h2 + nvec * 8;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  // body: 8 bf16 per 16-byte multicast store
-  for (int64_t v = gtid; v < nvec; v += gsz) {
-    const int64_t e = h2 + v * 8;
-    float f[8];
+  // body: 8 bf16 per 16-byte multicast store; kUnroll vectors per thread in
+  // flight (all local loads issued before the remote stores)
+  const bool src_vec = ((reinterpret_cast<uintptr_t>(src + h2)) & 15) == 0;
+  for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
+    uint4 w[kUnroll];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = src[e + i];
-    const uint4 w = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
-                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
-    const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
-    if (mc) {
-      mc_st_v4(s.mc_base + off, w);
-    } else {
-      for (int p = 0; p < s.nranks; ++p)
-        *reinterpret_cast<uint4*>(s.peer_base[p] + off) = w;
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < nvec) {
+        const float* p = src + h2 + v * 8;
+        float f[8];
+        if (src_vec) {
+          const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+          const float4 y = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+          f[0] = x.x; f[1] = x.y; f[2] = x.z; f[3] = x.w;
+          f[4] = y.x; f[5] = y.y; f[6] = y.z; f[7] = y.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = p[i];
+        }
+        w[u] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                          pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < nvec) {
+        const uint64_t off = dst0 + static_cast<uint64_t>(h2 + v * 8) * 2;
+        if (MC) {
+          mc_st_v4(s.mc_base + off, w[u]);
+        } else {
+          for (int p = 0; p < nr; ++p) *reinterpret_cast<uint4*>(peer[p] + off) = w[u];
+        }
+      }
     }
   }
   // edges (CTA 0): 4-byte pairs via multicast, a lone 2-byte element via peer stores
@@ -164,15 +204,15 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
     auto pair = [&](int64_t e) {
       const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
       const uint32_t w = pack_bf16x2(src[e], src[e + 1]);
-      if (mc)
+      if (MC)
         mc_st_b32(s.mc_base + off, w);
       else
-        for (int p = 0; p < s.nranks; ++p) *reinterpret_cast<uint32_t*>(s.peer_base[p] + off) = w;
+        for (int p = 0; p < nr; ++p) *reinterpret_cast<uint32_t*>(peer[p] + off) = w;
     };
     auto single = [&](int64_t e) {
       const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
       const __nv_bfloat16 h = __float2bfloat16_rn(src[e]);
-      for (int p = 0; p < s.nranks; ++p) *reinterpret_cast<__nv_bfloat16*>(s.peer_base[p] + off) = h;
+      for (int p = 0; p < nr; ++p) *reinterpret_cast<__nv_bfloat16*>(peer[p] + off) = h;
     };
     const int t = threadIdx.x;
     if (t == 0 && h1 == 1) single(0);
@@ -182,17 +222,20 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
     for (int64_t e = body_end + 2 * t; e + 1 < n; e += 2 * blockDim.x) pair(e);
     if (t == 0 && (n - body_end) % 2 == 1) single(n - 1);
   }
-  cross_barrier(s, a.channel, 1, a.epoch);   // every rank's stores have landed
+  cross_barrier(s, peer, a.channel, 1, a.epoch);   // every rank's stores have landed
 }
 
 // ---------------------------------------------------------------- reduce-scatter
 
-__global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const Args a) {
-  const het_symm_t& s = a.s;
-  cross_barrier(s, a.channel, 0, a.epoch);   // every rank's accumulator is final
+template <bool MC>
+__global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const __grid_constant__ Args a) {
+  __shared__ uint64_t peer[HET_MAX_RANKS];
+  HET_STAGE_PEERS(a, peer);
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off};
+  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's accumulator is final
   const int64_t n = a.count;
   const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 4;
-  const bool mc = s.mc_base != 0;
+  const int nr = s.nranks;
   int64_t head = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / 4);
   if (head > n) head = n;
   const int64_t nvec = (n - head) / 4;
@@ -200,46 +243,58 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t v = gtid; v < nvec; v += gsz) {
-    const int64_t e = head + v * 4;
-    const uint64_t off = src0 + static_cast<uint64_t>(e) * 4;
-    float4 r;
-    if (mc) {
-      r = mc_ldr_v4(s.mc_base + off);
-    } else {
-      r = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int p = 0; p < s.nranks; ++p) {
-        const float4 x = *reinterpret_cast<const float4*>(s.peer_base[p] + off);
-        r.x += x.x;
-        r.y += x.y;
-        r.z += x.z;
-        r.w += x.w;
+  for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
+    float4 r[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {          // kUnroll reductions in flight
+      const int64_t v = v0 + u * gsz;
+      if (v < nvec) {
+        const uint64_t off = src0 + static_cast<uint64_t>(head + v * 4) * 4;
+        if (MC) {
+          r[u] = mc_ldr_v4(s.mc_base + off);
+        } else {
+          r[u] = *reinterpret_cast<const float4*>(peer[0] + off);
+          for (int p = 1; p < nr; ++p) {
+            const float4 x = *reinterpret_cast<const float4*>(peer[p] + off);
+            r[u].x += x.x;
+            r[u].y += x.y;
+            r[u].z += x.z;
+            r[u].w += x.w;
+          }
+        }
       }
     }
-    if (out_vec) {
-      *reinterpret_cast<float4*>(out + e) = r;
-    } else {
-      out[e] = r.x;
-      out[e + 1] = r.y;
-      out[e + 2] = r.z;
-      out[e + 3] = r.w;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < nvec) {
+        const int64_t e = head + v * 4;
+        if (out_vec) {
+          __stcs(reinterpret_cast<float4*>(out + e), r[u]);
+        } else {
+          out[e] = r[u].x;
+          out[e + 1] = r[u].y;
+          out[e + 2] = r[u].z;
+          out[e + 3] = r[u].w;
+        }
+      }
     }
   }
   if (blockIdx.x == 0) {
     auto one = [&](int64_t e) {
       const uint64_t off = src0 + static_cast<uint64_t>(e) * 4;
       float r = 0.f;
-      if (mc) {
+      if (MC) {
         r = mc_ldr_f32(s.mc_base + off);
       } else {
-        for (int p = 0; p < s.nranks; ++p) r += *reinterpret_cast<const float*>(s.peer_base[p] + off);
+        for (int p = 0; p < nr; ++p) r += *reinterpret_cast<const float*>(peer[p] + off);
       }
       out[e] = r;
     };
     for (int64_t e = threadIdx.x; e < head; e += blockDim.x) one(e);
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
-  if (a.end_barrier) cross_barrier(s, a.channel, 1, a.epoch);  // peers done reading my acc
+  if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading my acc
 }
 
 int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offsets, int ctas) {
@@ -286,7 +341,11 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   if (counts[s->rank] > 0 && !src) return fail(HET_EARG, "het_symm_allgather_pack: null src");
   if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
   Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1};
-  symm_ag_kernel<<<ctas, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(src, a);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->mc_base)
+    symm_ag_kernel<true><<<ctas, kThreads, 0, st>>>(src, a);
+  else
+    symm_ag_kernel<false><<<ctas, kThreads, 0, st>>>(src, a);
   return het::check_launch("het_symm_allgather_pack");
 }
 
@@ -299,7 +358,11 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter: null out");
   if (acc_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter: acc offset not 16B aligned");
   Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
-  symm_rs_kernel<<<ctas, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(out, a);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s->mc_base)
+    symm_rs_kernel<true><<<ctas, kThreads, 0, st>>>(out, a);
+  else
+    symm_rs_kernel<false><<<ctas, kThreads, 0, st>>>(out, a);
   return het::check_launch("het_symm_reduce_scatter");
 }
 

@@ -22,7 +22,7 @@ DT_BF16, DT_F32 = 0, 1
 ALGO_AUTO, ALGO_P2P, ALGO_OWNER, ALGO_EVEN = 0, 1, 2, 3
 ALGO_SYMM = 4            # fused kernels on a symmetric buffer (NVLS multicast / peer)
 HET_MAX_RANKS = 8
-HET_SYMM_MAX_CTAS = 64
+HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
@@ -260,9 +260,9 @@ class SymmWorkspace:
         self.handle = symm.rendezvous(self.raw, group_name)
         base_off = int(getattr(self.handle, "offset", 0) or 0)
         peers = [int(p) + base_off for p in self.handle.buffer_ptrs]
-        mc = 0
-        if use_multicast and self.handle.has_multicast_support():
-            mc = int(self.handle.multicast_ptr) + base_off
+        mc = int(self.handle.multicast_ptr or 0) if use_multicast else 0
+        if mc:
+            mc += base_off
         self.multicast = mc != 0
         d = HetSymm()
         d.nranks, d.rank = nranks, rank

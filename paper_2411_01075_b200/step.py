@@ -97,7 +97,7 @@ class UnevenFSDPTrainer:
     def __init__(self, arch: ArchSpec, plan: TrainPlan, rank: int, *,
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
-                 algo: int = K.ALGO_AUTO):
+                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 32):
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
         self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo
@@ -121,7 +121,21 @@ class UnevenFSDPTrainer:
         self.v32 = torch.zeros(n, dtype=torch.float32, device=dev)
         self.p16 = torch.zeros(n, dtype=torch.bfloat16, device=dev)
         U, E = arch.unit_params, arch.root_params
-        if self.N > 1:
+        self.symm = None
+        if self.N > 1 and algo == K.ALGO_SYMM:
+            # fused NVLS collectives: unit buffers and accumulators live in one
+            # symmetric allocation; the AG reads the fp32 master directly
+            import torch.distributed as dist
+            gname = group_name or dist.group.WORLD.group_name
+            self.symm = K.SymmWorkspace(
+                [("ub0", U, torch.bfloat16), ("ub1", U, torch.bfloat16), ("rbuf", E, torch.bfloat16),
+                 ("acc0", U, torch.float32), ("acc1", U, torch.float32), ("racc", E, torch.float32)],
+                gname, dev, rank, self.N, ctas=symm_ctas)
+            self.ubuf = [self.symm["ub0"], self.symm["ub1"]]
+            self.rbuf = self.symm["rbuf"]
+            self.acc = [self.symm["acc0"], self.symm["acc1"]]
+            self.racc = self.symm["racc"]
+        elif self.N > 1:
             self.ubuf = [torch.empty(U, dtype=torch.bfloat16, device=dev) for _ in range(2)]
             self.rbuf = torch.empty(E, dtype=torch.bfloat16, device=dev)
             self.acc = [torch.zeros(U, dtype=torch.float32, device=dev) for _ in range(2)]
@@ -177,17 +191,34 @@ class UnevenFSDPTrainer:
     def _current(self):
         return torch.cuda.current_stream(self.device) if self.cuda else _NoStream()
 
+    def _region(self, t: torch.Tensor) -> str:
+        for name, v in self.symm.views.items():
+            if v.data_ptr() == t.data_ptr():
+                return name
+        raise InputError("buffer is not in the symmetric workspace")
+
     def _ag(self, u: int, dst: torch.Tensor) -> torch.cuda.Event:
-        K.allgather_uneven(self._local(self.p16, u), dst, self.L.counts[u],
-                           self.L.offsets[u], self.comm_ag, self.rank, self.algo,
-                           stream=self.ag_stream)
+        if self.symm is not None:    # fused pack + multicast all-gather from the fp32 master
+            self.symm.allgather_pack(self._local(self.p32, u), self._region(dst), 0,
+                                     self.L.counts[u], self.L.offsets[u], stream=self.ag_stream)
+        else:
+            K.allgather_uneven(self._local(self.p16, u), dst, self.L.counts[u],
+                               self.L.offsets[u], self.comm_ag, self.rank, self.algo,
+                               stream=self.ag_stream)
+        self.launches += self.symm is not None
         return self._event(self.ag_stream)
 
     def _rs(self, u: int, src: torch.Tensor, after: torch.cuda.Event) -> torch.cuda.Event:
         self.rs_stream.wait_event(after)
-        K.reduce_scatter_uneven(src, self._local(self.g32, u), self.L.counts[u],
-                                self.L.offsets[u], self.comm_rs, self.rank, self.algo,
-                                stream=self.rs_stream)
+        if self.symm is not None:    # multimem.ld_reduce straight into the fp32 grad shard
+            self.symm.reduce_scatter(self._region(src), 0, self._local(self.g32, u),
+                                     self.L.counts[u], self.L.offsets[u],
+                                     end_barrier=(u == self.L.root), stream=self.rs_stream)
+            self.launches += 1
+        else:
+            K.reduce_scatter_uneven(src, self._local(self.g32, u), self.L.counts[u],
+                                    self.L.offsets[u], self.comm_rs, self.rank, self.algo,
+                                    stream=self.rs_stream)
         return self._event(self.rs_stream)
 
     def _unit_flat(self, u: int) -> torch.Tensor:
@@ -287,6 +318,10 @@ class UnevenFSDPTrainer:
                     comp.wait_event(ag_ev[u])
                 if u + 2 in rs_ev:                  # acc[u % 2] last read by RS(u+2)
                     comp.wait_event(rs_ev[u + 2])
+                if self.symm is not None and u + 1 in rs_ev:
+                    # peers read acc[u % 2] remotely during RS(u+2): my RS(u+1) having
+                    # passed its start barrier proves every rank finished RS(u+2)
+                    comp.wait_event(rs_ev[u + 1])
             acc = self._acc(u)
             flat = self._unit_flat(u)
             pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}
@@ -317,10 +352,12 @@ class UnevenFSDPTrainer:
 
         # ---- optimizer -------------------------------------------------------
         self.steps += 1
-        a, b = self.timers.pair("adamw", 30.0 * self.L.local_len)
+        a, b = self.timers.pair("adamw", (28.0 if self.symm is not None else 30.0) *
+                                self.L.local_len)
         if a is not None:
             a.record()
-        K.adamw(self.p32, self.g32, self.m32, self.v32, self.p16, lr=self.opt.lr,
+        shadow = None if self.symm is not None else self.p16   # symm AG reads p32 itself
+        K.adamw(self.p32, self.g32, self.m32, self.v32, shadow, lr=self.opt.lr,
                 beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
                 weight_decay=self.opt.weight_decay, step=self.steps)
         if b is not None:

@@ -15,7 +15,7 @@ import torch.distributed as dist
 from oracle import step_oracle as O
 
 ACC_ADD, ACC_FIRST = 0, 1
-ALGO_AUTO, ALGO_P2P, ALGO_OWNER, ALGO_EVEN = 0, 1, 2, 3
+ALGO_AUTO, ALGO_P2P, ALGO_OWNER, ALGO_EVEN, ALGO_SYMM = 0, 1, 2, 3, 4
 calls: list[str] = []
 
 

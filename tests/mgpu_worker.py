@@ -137,12 +137,24 @@ def main(out_dir: str) -> None:
         dist.all_reduce(loss)
         g = [t.cpu().numpy() for t in tr.full_units("g32")]
         p = [t.cpu().numpy() for t in tr.full_units("p32")]
+        # the same step through the fused symmetric-memory (NVLS) collectives
+        trs = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev,
+                                algo=K.ALGO_SYMM)
+        trs.load_full_units(units)
+        loss_s = trs.step(torch.from_numpy(tok).to(dev))
+        dist.all_reduce(loss_s)
+        gs = [t.cpu().numpy() for t in trs.full_units("g32")]
+        ps = [t.cpu().numpy() for t in trs.full_units("p32")]
+        report["symm_status_step"] = float(K.SymmWorkspace.status(reset=True))
         torch.cuda.synchronize()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), loss=float(loss),
                  micro=np.array(micro), ratios=np.array(ratios),
                  report_keys=np.array(list(report.keys())),
                  report_vals=np.array(list(report.values()), dtype=np.float64),
-                 **{f"g{u}": x for u, x in enumerate(g)}, **{f"p{u}": x for u, x in enumerate(p)})
+                 loss_symm=float(loss_s),
+                 **{f"g{u}": x for u, x in enumerate(g)}, **{f"p{u}": x for u, x in enumerate(p)},
+                 **{f"gs{u}": x for u, x in enumerate(gs)},
+                 **{f"ps{u}": x for u, x in enumerate(ps)})
     finally:
         cag.close()
         crs.close()

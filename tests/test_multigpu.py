@@ -74,3 +74,9 @@ def test_multigpu_collectives_and_step(tmp_path):
         z = np.zeros(got.size, np.float32)
         rp, _, _ = SO.adamw(units[u].numpy(), got, z, z, step=1, **opt)
         assert max_rel(r[0][f"p{u}"], rp) <= FP32_RTOL
+        # fused NVLS path: same gradients up to summation order, same AdamW arithmetic
+        gs = r[0][f"gs{u}"]
+        assert norm_rel(gs, got) <= 1e-5, f"symm unit {u}"
+        rps, _, _ = SO.adamw(units[u].numpy(), gs, z, z, step=1, **opt)
+        assert max_rel(r[0][f"ps{u}"], rps) <= FP32_RTOL
+    assert abs(float(r[0]["loss_symm"]) - float(r[0]["loss"])) <= 1e-5 * abs(loss)

@@ -54,6 +54,8 @@ def _run(plan, arch, units, steps=1):
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
+    for r, d in res.items():
+        assert "error" not in d, f"rank {r} failed:\n{d['error']}"
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

@@ -11,7 +11,7 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
 t = symm.empty(1 << 20, dtype=torch.float32, device="cuda")
 h = symm.rendezvous(t, dist.group.WORLD.group_name)
 print(rank, "backend", symm.get_backend("cuda") if hasattr(symm, "get_backend") else "?",
-      "mc", h.has_multicast_support(), hex(h.multicast_ptr or 0),
+      "mc", hex(h.multicast_ptr or 0),
       "peers", [hex(p) for p in h.buffer_ptrs], "sig", h.signal_pad_size,
       "bufsize", h.buffer_size, "offset", getattr(h, "offset", None), flush=True)
 t2 = symm.empty(3 << 20, dtype=torch.bfloat16, device="cuda")
