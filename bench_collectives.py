@@ -31,7 +31,9 @@ from paper_2411_01075_b200 import hetstep as K  # noqa: E402
 from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
-         "symm": "symm", "symm_peer": "symm_peer"}
+         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer"}
+SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
+        "symm_peer": (False, K.SYMM_PEER)}
 
 
 def skew_counts(skew: str, total: int, n: int) -> list[int]:
@@ -85,11 +87,12 @@ def main() -> None:
     ap.add_argument("--sizes-mb", type=float, nargs="*", default=[1, 4, 16, 64, 256, 1024])
     ap.add_argument("--skews", nargs="*",
                     default=["even", "two_to_one", "geometric", "single_owner", "planner"])
-    ap.add_argument("--algos", nargs="*", default=["auto", "owner", "p2p", "symm", "symm_peer"])
+    ap.add_argument("--algos", nargs="*", default=["auto", "owner", "p2p", "symm", "symm_mc",
+                                                   "symm_peer"])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--planner-config", default="llama_1b3")
-    ap.add_argument("--ctas", type=int, default=32)
+    ap.add_argument("--ctas", type=int, default=128)
     args = ap.parse_args()
 
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), \
@@ -105,12 +108,12 @@ def main() -> None:
     best: dict[str, float] = {}
     maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
     ws = {}
-    for an, mc in (("symm", True), ("symm_peer", False)):
+    for an, (mc, policy) in SYMM.items():
         if an in args.algos:
             ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
                                                                          torch.float32)],
                                      dist.group.WORLD.group_name, dev, rank, world,
-                                     ctas=args.ctas, use_multicast=mc)
+                                     ctas=args.ctas, use_multicast=mc, policy=policy)
             if rank == 0:
                 print(json.dumps({"workspace": an, "multicast": ws[an].multicast}), flush=True)
     try:
@@ -152,8 +155,8 @@ def main() -> None:
                         bus = ingest / (ms * 1e-3) / 1e9
                         nccl_bus = (world - 1) / world * S / (ms * 1e-3) / 1e9
                         key = f"{op}/{skew}"
-                        if mb >= 256:
-                            best[key] = max(best.get(key, 0.0), bus)
+                        if mb >= 256 and bus > best.get(key, (0.0, ""))[0]:
+                            best[key] = (bus, an)
                         if rank == 0:
                             print(json.dumps({"op": op, "n_gpus": world, "size_mb": mb,
                                               "skew": skew, "algo": an, "ms": ms,
@@ -165,7 +168,7 @@ def main() -> None:
             print(json.dumps({"summary": "best bus GB/s at >= 256 MB", "n_gpus": world,
                               "symm_status": status,
                               "best": best,
-                              "frac_of_770": {k: v / 770.0 for k, v in best.items()}}),
+                              "frac_of_770": {k: v[0] / 770.0 for k, v in best.items()}}),
                   flush=True)
     finally:
         comm.close()

@@ -117,6 +117,13 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
 #define HET_SYMM_CHANNELS 2   /* independent barrier channels: 0 = AG stream, 1 = RS stream */
 #define HET_SYMM_TIMEOUT 17   /* het_symm_status(): a cross-rank barrier timed out */
 
+/* Route policy of the fused collectives. AUTO picks per call from the shard
+ * vector: NVLS multicast moves S bytes over every GPU's link, peer push/pull
+ * moves max((N-1) max_j s_j, S - min_i s_i); the cheaper one runs. */
+#define HET_SYMM_AUTO 0
+#define HET_SYMM_MULTICAST 1
+#define HET_SYMM_PEER 2
+
 /* A buffer allocated at the same byte layout on every rank (torch symmetric
  * memory is the plumbing): peer_base[j] = its address on rank j mapped into
  * this process (UVA peer mapping), mc_base = NVLS multicast address or 0.
@@ -139,7 +146,7 @@ int het_symm_status(int reset);
  * must increase by one per call on `channel` on every rank. */
 int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit_off,
                             const int64_t* counts, const int64_t* offsets, uint32_t epoch,
-                            int channel, int ctas, void* stream);
+                            int channel, int policy, int ctas, void* stream);
 
 /* (3) fused: out[0:counts[r]] = sum_j acc_j[offsets[r] : +counts[r]] where
  * acc_j is the fp32 accumulator at acc_off on rank j (already Eq. 1-scaled),
@@ -147,7 +154,7 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
  * additionally waits until every rank finished reading this rank's acc. */
 int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
                             const int64_t* counts, const int64_t* offsets, uint32_t epoch,
-                            int channel, int end_barrier, int ctas, void* stream);
+                            int channel, int end_barrier, int policy, int ctas, void* stream);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <climits>
+
 #include "hetstep.h"
 #include "hetstep_internal.cuh"
 
@@ -143,7 +145,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 // ---------------------------------------------------------------- all-gather
 
-template <bool MC>
+template <bool MC, int NR>
 __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restrict__ src,
                                                            const __grid_constant__ Args a) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
   cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank released its copy of the unit
   const int64_t n = a.count;
   const uint64_t dst0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;  // byte offset
-  const int nr = s.nranks;
+  const int nr = NR > 0 ? NR : s.nranks;   // compile-time for 2/4/8 ranks: loops unroll
   // element ranges: [0,h1) 2-byte edge, [h1,h2) 4-byte words, body 16-byte vectors, tail
   int64_t h1 = (dst0 & 3) ? 1 : 0;
   if (h1 > n) h1 = n;
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
         if (MC) {
           mc_st_v4(s.mc_base + off, w[u]);
         } else {
+#pragma unroll
           for (int p = 0; p < nr; ++p) *reinterpret_cast<uint4*>(peer[p] + off) = w[u];
         }
       }
@@ -227,7 +230,18 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
 
 // ---------------------------------------------------------------- reduce-scatter
 
-template <bool MC>
+__device__ __forceinline__ void store4(float* out, int64_t e, const float4& r, bool vec) {
+  if (vec) {
+    __stcs(reinterpret_cast<float4*>(out + e), r);
+  } else {
+    out[e] = r.x;
+    out[e + 1] = r.y;
+    out[e + 2] = r.z;
+    out[e + 3] = r.w;
+  }
+}
+
+template <bool MC, int NR>
 __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const __grid_constant__ Args a) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's accumulator is final
   const int64_t n = a.count;
   const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 4;
-  const int nr = s.nranks;
+  const int nr = NR > 0 ? NR : s.nranks;   // compile-time for 2/4/8 ranks: loops unroll
   int64_t head = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / 4);
   if (head > n) head = n;
   const int64_t nvec = (n - head) / 4;
@@ -243,39 +257,50 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
-    float4 r[kUnroll];
+  if (MC) {
+    for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
+      float4 r[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {          // kUnroll reductions in flight
-      const int64_t v = v0 + u * gsz;
-      if (v < nvec) {
-        const uint64_t off = src0 + static_cast<uint64_t>(head + v * 4) * 4;
-        if (MC) {
-          r[u] = mc_ldr_v4(s.mc_base + off);
-        } else {
-          r[u] = *reinterpret_cast<const float4*>(peer[0] + off);
-          for (int p = 1; p < nr; ++p) {
-            const float4 x = *reinterpret_cast<const float4*>(peer[p] + off);
-            r[u].x += x.x;
-            r[u].y += x.y;
-            r[u].z += x.z;
-            r[u].w += x.w;
-          }
-        }
+      for (int u = 0; u < kUnroll; ++u) {        // kUnroll switch reductions in flight
+        const int64_t v = v0 + u * gsz;
+        if (v < nvec) r[u] = mc_ldr_v4(s.mc_base + src0 + static_cast<uint64_t>(head + v * 4) * 4);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t v = v0 + u * gsz;
+        if (v < nvec) store4(out, head + v * 4, r[u], out_vec);
       }
     }
+  } else {
+    // peer pull: all (vector, rank) loads of a batch issued before any add
+    constexpr int kB = NR > 0 ? (16 / NR > 1 ? 16 / NR : 2) : 2;
+    for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kB) {
+      float4 x[kB][NR > 0 ? NR : HET_MAX_RANKS];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t v = v0 + u * gsz;
-      if (v < nvec) {
-        const int64_t e = head + v * 4;
-        if (out_vec) {
-          __stcs(reinterpret_cast<float4*>(out + e), r[u]);
-        } else {
-          out[e] = r[u].x;
-          out[e + 1] = r[u].y;
-          out[e + 2] = r[u].z;
-          out[e + 3] = r[u].w;
+      for (int u = 0; u < kB; ++u) {
+        const int64_t v = v0 + u * gsz;
+        if (v < nvec) {
+          const uint64_t off = src0 + static_cast<uint64_t>(head + v * 4) * 4;
+#pragma unroll
+          for (int p = 0; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p)
+            if (p < nr) x[u][p] = __ldcg(reinterpret_cast<const float4*>(peer[p] + off));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int64_t v = v0 + u * gsz;
+        if (v < nvec) {
+          float4 r = x[u][0];
+#pragma unroll
+          for (int p = 1; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p) {
+            if (p < nr) {
+              r.x += x[u][p].x;
+              r.y += x[u][p].y;
+              r.z += x[u][p].z;
+              r.w += x[u][p].w;
+            }
+          }
+          store4(out, head + v * 4, r, out_vec);
         }
       }
     }
@@ -295,6 +320,39 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
   if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading my acc
+}
+
+// multicast kernels do not loop over ranks; peer kernels get the rank count
+// as a template constant for 2/4/8 ranks so their per-rank loops unroll
+#define HET_DISPATCH_NR(mc, n, LAUNCH) \
+  do {                                 \
+    if (mc) {                          \
+      LAUNCH(true, 0);                 \
+    } else if ((n) == 2) {             \
+      LAUNCH(false, 2);                \
+    } else if ((n) == 4) {             \
+      LAUNCH(false, 4);                \
+    } else if ((n) == 8) {             \
+      LAUNCH(false, 8);                \
+    } else {                           \
+      LAUNCH(false, 0);                \
+    }                                  \
+  } while (0)
+
+// Per-call route: NVLS multicast costs every GPU S bytes of link traffic
+// (the switch loops a GPU's own range back to it), peer push/pull costs
+// max((N-1) * max_j s_j, S - min_i s_i). Pick the cheaper one.
+bool pick_multicast(const het_symm_t* s, const int64_t* counts, int policy) {
+  if (!s->mc_base || policy == HET_SYMM_PEER) return false;
+  if (policy == HET_SYMM_MULTICAST) return true;
+  int64_t total = 0, mx = 0, mn = INT64_MAX;
+  for (int j = 0; j < s->nranks; ++j) {
+    total += counts[j];
+    mx = counts[j] > mx ? counts[j] : mx;
+    mn = counts[j] < mn ? counts[j] : mn;
+  }
+  const int64_t push = (s->nranks - 1) * mx > total - mn ? (s->nranks - 1) * mx : total - mn;
+  return total < push;
 }
 
 int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offsets, int ctas) {
@@ -334,7 +392,7 @@ int het_symm_status(int reset) {
 
 int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit_off,
                             const int64_t* counts, const int64_t* offsets, uint32_t epoch,
-                            int channel, int ctas, void* stream) {
+                            int channel, int policy, int ctas, void* stream) {
   int rc = check_symm(s, counts, offsets, ctas);
   if (rc != HET_OK) return rc;
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
@@ -342,16 +400,16 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
   Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (s->mc_base)
-    symm_ag_kernel<true><<<ctas, kThreads, 0, st>>>(src, a);
-  else
-    symm_ag_kernel<false><<<ctas, kThreads, 0, st>>>(src, a);
+  const bool mc = pick_multicast(s, counts, policy);
+#define HET_AG(MCV, NRV) symm_ag_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(src, a)
+  HET_DISPATCH_NR(mc, s->nranks, HET_AG);
+#undef HET_AG
   return het::check_launch("het_symm_allgather_pack");
 }
 
 int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
                             const int64_t* counts, const int64_t* offsets, uint32_t epoch,
-                            int channel, int end_barrier, int ctas, void* stream) {
+                            int channel, int end_barrier, int policy, int ctas, void* stream) {
   int rc = check_symm(s, counts, offsets, ctas);
   if (rc != HET_OK) return rc;
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
@@ -359,10 +417,10 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   if (acc_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter: acc offset not 16B aligned");
   Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (s->mc_base)
-    symm_rs_kernel<true><<<ctas, kThreads, 0, st>>>(out, a);
-  else
-    symm_rs_kernel<false><<<ctas, kThreads, 0, st>>>(out, a);
+  const bool mc = pick_multicast(s, counts, policy);
+#define HET_RS(MCV, NRV) symm_rs_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(out, a)
+  HET_DISPATCH_NR(mc, s->nranks, HET_RS);
+#undef HET_RS
   return het::check_launch("het_symm_reduce_scatter");
 }
 

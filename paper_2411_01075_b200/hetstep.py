@@ -24,6 +24,7 @@ ALGO_SYMM = 4            # fused kernels on a symmetric buffer (NVLS multicast /
 HET_MAX_RANKS = 8
 HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
+SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
@@ -72,10 +73,10 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_symm_status": ([i32], i32),
         "het_symm_allgather_pack": ([ctypes.POINTER(HetSymm), vp, ctypes.c_uint64,
                                      ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
-                                     i32, i32, vp], i32),
+                                     i32, i32, i32, vp], i32),
         "het_symm_reduce_scatter": ([ctypes.POINTER(HetSymm), ctypes.c_uint64, vp,
                                      ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
-                                     i32, i32, i32, vp], i32),
+                                     i32, i32, i32, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -241,8 +242,8 @@ class SymmWorkspace:
     kernels address regions by byte offset from the peer / multicast bases."""
 
     def __init__(self, regions: Sequence[tuple[str, int, torch.dtype]], group_name: str,
-                 device: torch.device, rank: int, nranks: int, ctas: int = 32,
-                 use_multicast: bool = True):
+                 device: torch.device, rank: int, nranks: int, ctas: int = 128,
+                 use_multicast: bool = True, policy: int = SYMM_AUTO):
         import torch.distributed._symmetric_memory as symm
         if nranks > HET_MAX_RANKS:
             raise InputError(f"symmetric collectives support up to {HET_MAX_RANKS} ranks")
@@ -278,6 +279,7 @@ class SymmWorkspace:
             self.views[name] = self.raw[o:o + nbytes].view(dtype)
         self.epoch = [0, 0]
         self.ctas = ctas
+        self.policy = policy
         torch.cuda.synchronize(device)
         self.handle.barrier()
 
@@ -292,7 +294,7 @@ class SymmWorkspace:
         byte_off = self.offsets[region] + 2 * elem_off
         _check(load().het_symm_allgather_pack(ctypes.byref(self.desc), src, byte_off,
                                               _i64(counts), _i64(offsets), self.epoch[0], 0,
-                                              self.ctas, _stream(stream)),
+                                              self.policy, self.ctas, _stream(stream)),
                "het_symm_allgather_pack")
 
     def reduce_scatter(self, region: str, elem_off: int, out: torch.Tensor,
@@ -304,7 +306,7 @@ class SymmWorkspace:
         byte_off = self.offsets[region] + 4 * elem_off
         _check(load().het_symm_reduce_scatter(ctypes.byref(self.desc), byte_off, o, _i64(counts),
                                               _i64(offsets), self.epoch[1], 1, int(end_barrier),
-                                              self.ctas, _stream(stream)),
+                                              self.policy, self.ctas, _stream(stream)),
                "het_symm_reduce_scatter")
 
     @staticmethod

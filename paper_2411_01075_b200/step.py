@@ -97,7 +97,7 @@ class UnevenFSDPTrainer:
     def __init__(self, arch: ArchSpec, plan: TrainPlan, rank: int, *,
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
-                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 32):
+                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64):
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
         self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo

@@ -82,11 +82,12 @@ def main(out_dir: str) -> None:
 
         # fused symmetric-memory collectives (NVLS multicast when available, then peer)
         maxu = max(sum(c) for c in shard_cases(world)) + 64
-        for use_mc in (True, False):
+        for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO)):
             ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32)],
                                  dist.group.WORLD.group_name, dev, rank, world,
-                                 use_multicast=use_mc)
-            report[f"symm_mc_available_{int(use_mc)}"] = float(ws.multicast)
+                                 use_multicast=use_mc, policy=policy)
+            use_mc = f"{int(use_mc)}{policy}"
+            report[f"symm_mc_available_{use_mc}"] = float(ws.multicast)
             for ci, counts in enumerate(shard_cases(world)):
                 offs = offsets(counts)
                 total = sum(counts)
@@ -97,7 +98,7 @@ def main(out_dir: str) -> None:
                     ws.allgather_pack(mine, "unit", 8 * shift, counts, offs)
                     torch.cuda.synchronize()
                     got = ws["unit"][8 * shift:8 * shift + total].view(torch.int16).cpu().numpy()
-                    report[f"symm_ag{ci}_{int(use_mc)}_{shift}"] = int(
+                    report[f"symm_ag{ci}_{use_mc}_{shift}"] = int(
                         np.array_equal(got.view(np.uint16), O.pack(full)))
                 srcs = [np.random.default_rng(100 * ci + r).standard_normal(total).astype(np.float32)
                         for r in range(world)]
@@ -106,9 +107,9 @@ def main(out_dir: str) -> None:
                 out = torch.empty(counts[rank], dtype=torch.float32, device=dev)
                 ws.reduce_scatter("acc", 0, out, counts, offs, end_barrier=True)
                 torch.cuda.synchronize()
-                report[f"symm_rs{ci}_{int(use_mc)}"] = float(
+                report[f"symm_rs{ci}_{use_mc}"] = float(
                     max_rel(out.cpu().numpy(), want) if counts[rank] else 0.0)
-            report[f"symm_status_{int(use_mc)}"] = float(K.SymmWorkspace.status(reset=True))
+            report[f"symm_status_{use_mc}"] = float(K.SymmWorkspace.status(reset=True))
             dist.barrier()
             del ws
 
