@@ -191,7 +191,9 @@ def main() -> None:
     ap.add_argument("--config", default="gpt2_small", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--algo", type=int, default=K.ALGO_AUTO)
+    ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
+                    help="collective route for N>1: 4 = fused symmetric-memory kernels "
+                         "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -203,7 +205,7 @@ def main() -> None:
     job = build_job(args.config, world)
     comm_ag, comm_rs = make_comms(world, rank)
     tr = UnevenFSDPTrainer(job.arch, job.plan, rank, comm_ag=comm_ag, comm_rs=comm_rs, opt=OPT,
-                           device=dev, algo=args.algo)
+                           device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO)
     tr.init_params(seed=0)
     arch, plan = job.arch, job.plan
     nsteps = args.warmup + args.steps
