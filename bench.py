@@ -33,6 +33,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2411_01075_b200 import hetstep as K  # noqa: E402
 from paper_2411_01075_b200.configs import CONFIGS, build_job  # noqa: E402
 from paper_2411_01075_b200.data import rank_tokens  # noqa: E402
+from paper_2411_01075_b200.emulate import emulate_tier  # noqa: E402
 from paper_2411_01075_b200.step import AdamWConfig, UnevenFSDPTrainer  # noqa: E402
 
 SEED = 1234
@@ -191,6 +192,9 @@ def main() -> None:
     ap.add_argument("--config", default="gpt2_small", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-emulate", action="store_true",
+                    help="run every rank on the full B200 (no green-context SM partition or "
+                         "memory cap from the cluster spec)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
                     help="collective route for N>1: 4 = fused symmetric-memory kernels "
                          "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")
@@ -204,6 +208,12 @@ def main() -> None:
     dev = torch.device("cuda", local)
     job = build_job(args.config, world)
     comm_ag, comm_rs = make_comms(world, rank)
+    # heterogeneity emulation: this rank's tier -> HBM cap + green-context SM partition
+    emu = emulate_tier(job.cluster, rank, dev, sm_partition=not args.no_emulate,
+                       memory_cap=not args.no_emulate)
+    compute_stream = emu.stream if emu.stream is not None else torch.cuda.current_stream()
+    ctx = torch.cuda.stream(compute_stream)
+    ctx.__enter__()
     tr = UnevenFSDPTrainer(job.arch, job.plan, rank, comm_ag=comm_ag, comm_rs=comm_rs, opt=OPT,
                            device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO)
     tr.init_params(seed=0)
@@ -257,6 +267,7 @@ def main() -> None:
     e1.record(comp)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    ctx.__exit__(None, None, None)
 
     B = plan.total_batch
     hbm, hbm_kind = peaks()
@@ -282,6 +293,9 @@ def main() -> None:
                                 for a in plan.assignments],
                        "uneven_units": plan.unit_shards.uneven_units,
                        "parallelism": f"uneven-fsdp{world}",
+                       "emulation_rank0": emu.describe(),
+                       "collectives": ("fused-symm" if tr.symm is not None else
+                                       "nccl" if world > 1 else "none"),
                        "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": tok_bytes, "d2h_bytes_per_step": 4 * world},
