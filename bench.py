@@ -312,10 +312,19 @@ def main() -> None:
             "loss": loss_val,
         }
         print(json.dumps(line), flush=True)
+    torch.cuda.synchronize()
     if world > 1:
+        dist.barrier()
         comm_ag.close()
         comm_rs.close()
         dist.destroy_process_group()
+    if emu.green is not None:
+        # The green context must outlive every tensor that touched its stream;
+        # interpreter teardown frees them in arbitrary order (and then records
+        # events on a destroyed context), so end the process here instead.
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
 
 
 if __name__ == "__main__":
