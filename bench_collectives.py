@@ -31,7 +31,7 @@ from paper_2411_01075_b200 import hetstep as K  # noqa: E402
 from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
-         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer"}
+         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route"}
 SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
         "symm_peer": (False, K.SYMM_PEER)}
 
@@ -87,8 +87,8 @@ def main() -> None:
     ap.add_argument("--sizes-mb", type=float, nargs="*", default=[1, 4, 16, 64, 256, 1024])
     ap.add_argument("--skews", nargs="*",
                     default=["even", "two_to_one", "geometric", "single_owner", "planner"])
-    ap.add_argument("--algos", nargs="*", default=["auto", "owner", "p2p", "symm", "symm_mc",
-                                                   "symm_peer"])
+    ap.add_argument("--algos", nargs="*", default=["route", "auto", "owner", "p2p", "symm",
+                                                   "symm_mc", "symm_peer"])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--planner-config", default="llama_1b3")
@@ -109,7 +109,7 @@ def main() -> None:
     maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
     ws = {}
     for an, (mc, policy) in SYMM.items():
-        if an in args.algos:
+        if an in args.algos or (an == "symm" and "route" in args.algos):
             ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
                                                                          torch.float32)],
                                      dist.group.WORLD.group_name, dev, rank, world,
@@ -132,6 +132,10 @@ def main() -> None:
                         algo = ALGOS[an]
                         if op == "reduce_scatter" and algo == K.ALGO_P2P:
                             continue
+                        if algo == "route":   # the train step's per-unit choice
+                            pick = K.route_collective("ag" if op == "allgather" else "rs", c,
+                                                      world, "symm" in ws)
+                            algo = "symm" if pick == "symm" else K.ALGO_AUTO
                         if isinstance(algo, str):
                             w = ws[algo]
                             if op == "allgather":

@@ -135,7 +135,19 @@ class UnevenFSDPTrainer:
             self.rbuf = self.symm["rbuf"]
             self.acc = [self.symm["acc0"], self.symm["acc1"]]
             self.racc = self.symm["racc"]
-        elif self.N > 1:
+        # per-unit collective routes (fused symmetric kernels vs NCCL ring), fixed by shape
+        units = range(self.L.blocks + 1)
+        sym = self.symm is not None
+        self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
+        self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
+        # a fused RS whose successor (RS order: L-1..0, root) is not fused must end with a
+        # cross-rank barrier: nothing later proves that peers finished reading its acc
+        order = list(range(self.L.blocks - 1, -1, -1)) + [self.L.root]
+        self.rs_end = {u: self.rs_route[u] == "symm" and
+                       (i + 1 == len(order) or self.rs_route[order[i + 1]] != "symm")
+                       for i, u in enumerate(order)}
+        self.need_shadow = not sym or "nccl" in self.ag_route
+        if self.N > 1 and self.symm is None:
             self.ubuf = [torch.empty(U, dtype=torch.bfloat16, device=dev) for _ in range(2)]
             self.rbuf = torch.empty(E, dtype=torch.bfloat16, device=dev)
             self.acc = [torch.zeros(U, dtype=torch.float32, device=dev) for _ in range(2)]
@@ -198,26 +210,28 @@ class UnevenFSDPTrainer:
         raise InputError("buffer is not in the symmetric workspace")
 
     def _ag(self, u: int, dst: torch.Tensor) -> torch.cuda.Event:
-        if self.symm is not None:    # fused pack + multicast all-gather from the fp32 master
+        if self.ag_route[u] == "symm":   # fused pack + NVLS/peer all-gather from fp32 master
             self.symm.allgather_pack(self._local(self.p32, u), self._region(dst), 0,
                                      self.L.counts[u], self.L.offsets[u], stream=self.ag_stream)
+            self.launches += 1
         else:
             K.allgather_uneven(self._local(self.p16, u), dst, self.L.counts[u],
-                               self.L.offsets[u], self.comm_ag, self.rank, self.algo,
+                               self.L.offsets[u], self.comm_ag, self.rank,
+                               K.ALGO_AUTO if self.algo == K.ALGO_SYMM else self.algo,
                                stream=self.ag_stream)
-        self.launches += self.symm is not None
         return self._event(self.ag_stream)
 
     def _rs(self, u: int, src: torch.Tensor, after: torch.cuda.Event) -> torch.cuda.Event:
         self.rs_stream.wait_event(after)
-        if self.symm is not None:    # multimem.ld_reduce straight into the fp32 grad shard
+        if self.rs_route[u] == "symm":   # switch/peer reduction straight into the fp32 shard
             self.symm.reduce_scatter(self._region(src), 0, self._local(self.g32, u),
                                      self.L.counts[u], self.L.offsets[u],
-                                     end_barrier=(u == self.L.root), stream=self.rs_stream)
+                                     end_barrier=self.rs_end[u], stream=self.rs_stream)
             self.launches += 1
         else:
             K.reduce_scatter_uneven(src, self._local(self.g32, u), self.L.counts[u],
-                                    self.L.offsets[u], self.comm_rs, self.rank, self.algo,
+                                    self.L.offsets[u], self.comm_rs, self.rank,
+                                    K.ALGO_AUTO if self.algo == K.ALGO_SYMM else self.algo,
                                     stream=self.rs_stream)
         return self._event(self.rs_stream)
 
@@ -352,11 +366,11 @@ class UnevenFSDPTrainer:
 
         # ---- optimizer -------------------------------------------------------
         self.steps += 1
-        a, b = self.timers.pair("adamw", (28.0 if self.symm is not None else 30.0) *
+        a, b = self.timers.pair("adamw", (30.0 if self.need_shadow else 28.0) *
                                 self.L.local_len)
         if a is not None:
             a.record()
-        shadow = None if self.symm is not None else self.p16   # symm AG reads p32 itself
+        shadow = self.p16 if self.need_shadow else None   # fused AG reads p32 itself
         K.adamw(self.p32, self.g32, self.m32, self.v32, shadow, lr=self.opt.lr,
                 beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
                 weight_decay=self.opt.weight_decay, step=self.steps)
