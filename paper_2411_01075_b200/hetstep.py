@@ -234,21 +234,25 @@ def reduce_scatter_uneven(src: torch.Tensor, shard: torch.Tensor, counts: Sequen
 
 def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) -> str:
     """'symm' (fused kernels on the symmetric workspace) or 'nccl' for one
-    unit's all-gather ("ag") / reduce-scatter ("rs"), from the measured
-    sweeps (profiles/r1_collectives_n2.jsonl, r1_collectives_n4.jsonl):
+    unit's all-gather ("ag", bf16) / reduce-scatter ("rs", fp32), from the
+    measured sweeps (profiles/r1_collectives_n2.jsonl, r1_collectives_n4*.jsonl):
       * AG: the fused kernel wins every shape except near-single-owner units at
         N >= 4, where NCCL's pipelined ring broadcast keeps the owner's link
         busier than the NVLS multicast store does;
-      * RS: the fused peer-pull kernel wins even units and every shape at
-        N = 2; skewed units at N >= 4 go to NCCL's per-owner ring reduce.
+      * RS: the fused kernel wins even units, every shape at N = 2 and skewed
+        units up to a few hundred MB; near-single-owner units and very large
+        skewed units at N >= 4 go to NCCL's per-owner ring reduce.
     """
     if not symm or nranks == 1:
         return "nccl"
     total, mx, mn = sum(counts), max(counts), min(counts)
+    owner_like = nranks >= 4 and mx >= 0.75 * total
     if op == "ag":
-        return "nccl" if nranks >= 4 and mx >= 0.75 * total else "symm"
+        return "nccl" if owner_like else "symm"
     if op == "rs":
-        return "symm" if (mx - mn <= 1 or nranks == 2) else "nccl"
+        if nranks == 2 or mx - mn <= 1:
+            return "symm"
+        return "nccl" if owner_like or total * 4 >= (512 << 20) else "symm"
     raise InputError(f"unknown collective {op!r}")
 
 
