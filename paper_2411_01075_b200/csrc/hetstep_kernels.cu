@@ -79,6 +79,41 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): one instruction per
+// 8 fp32, half the memory instructions of float4 at the same bytes in flight.
+struct F8 {
+  float x[8];
+};
+
+__device__ __forceinline__ F8 ld8(const float* a) {
+  F8 r;
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                 "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+               : "l"(a));
+  return r;
+}
+
+__device__ __forceinline__ F8 ld8_stream(const float* a) {   // touch-once input
+  F8 r;
+  asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                 "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+               : "l"(a));
+  return r;
+}
+
+__device__ __forceinline__ void st8(float* a, const F8& r) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(a), "f"(r.x[0]),
+               "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]), "f"(r.x[5]), "f"(r.x[6]),
+               "f"(r.x[7])
+               : "memory");
+}
+
+__host__ __device__ __forceinline__ bool aligned32(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 31) == 0;
+}
+
 // ---------------------------------------------------------------- pack
 
 __global__ void __launch_bounds__(kThreads) pack_vec_kernel(const float4* __restrict__ src,
@@ -136,17 +171,21 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict_
                       ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
   if (vec_ok && base + kAccChunk <= sg.n) {
     uint4 raw[kAccIters];
-    float4 lo[kAccIters], hi[kAccIters];
+    F8 a[kAccIters];
+    const bool wide = aligned32(dst);     // 256-bit accumulator accesses
 #pragma unroll
     for (int it = 0; it < kAccIters; ++it) {
       const int64_t e = base + (static_cast<int64_t>(it) * kThreads + threadIdx.x) * kAccVec;
       raw[it] = __ldcs(reinterpret_cast<const uint4*>(src + e));
-      if (MODE & HET_ACC_FIRST) {
-        lo[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-        hi[it] = lo[it];
+      if (MODE == HET_ACC_FIRST) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[it].x[k] = 0.f;
+      } else if (wide) {
+        a[it] = ld8(dst + e);
       } else {
-        lo[it] = *reinterpret_cast<const float4*>(dst + e);
-        hi[it] = *reinterpret_cast<const float4*>(dst + e + 4);
+        const float4 lo = *reinterpret_cast<const float4*>(dst + e);
+        const float4 hi = *reinterpret_cast<const float4*>(dst + e + 4);
+        a[it] = F8{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w}};
       }
     }
 #pragma unroll
@@ -154,12 +193,15 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict_
       const int64_t e = base + (static_cast<int64_t>(it) * kThreads + threadIdx.x) * kAccVec;
       float g[8];
       unpack8(raw[it], g);
-      float4 o0 = make_float4(acc_op<MODE>(lo[it].x, g[0], w), acc_op<MODE>(lo[it].y, g[1], w),
-                              acc_op<MODE>(lo[it].z, g[2], w), acc_op<MODE>(lo[it].w, g[3], w));
-      float4 o1 = make_float4(acc_op<MODE>(hi[it].x, g[4], w), acc_op<MODE>(hi[it].y, g[5], w),
-                              acc_op<MODE>(hi[it].z, g[6], w), acc_op<MODE>(hi[it].w, g[7], w));
-      *reinterpret_cast<float4*>(dst + e) = o0;
-      *reinterpret_cast<float4*>(dst + e + 4) = o1;
+      F8 o;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o.x[k] = acc_op<MODE>(a[it].x[k], g[k], w);
+      if (wide) {
+        st8(dst + e, o);
+      } else {
+        *reinterpret_cast<float4*>(dst + e) = make_float4(o.x[0], o.x[1], o.x[2], o.x[3]);
+        *reinterpret_cast<float4*>(dst + e + 4) = make_float4(o.x[4], o.x[5], o.x[6], o.x[7]);
+      }
     }
     return;
   }
@@ -232,6 +274,30 @@ __global__ void __launch_bounds__(kThreads) adamw_vec_kernel(float4* __restrict_
       v[j] = v1;
       if (SHADOW) shadow[j] = make_uint2(pack2(p1.x, p1.y), pack2(p1.z, p1.w));
     }
+  }
+}
+
+// 256-bit variant: 8 params per thread per iteration (32 B of each state
+// stream), shadow as one 16-byte store. Used when every stream is 32B-aligned.
+template <bool SHADOW>
+__global__ void __launch_bounds__(kThreads) adamw_v8_kernel(float* __restrict__ p,
+                                                            const float* __restrict__ g,
+                                                            float* __restrict__ m,
+                                                            float* __restrict__ v,
+                                                            uint4* __restrict__ shadow,
+                                                            int64_t n8, AdamCoef c) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += stride) {
+    F8 P = ld8(p + i * 8), G = ld8_stream(g + i * 8), M = ld8(m + i * 8), V = ld8(v + i * 8);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) adam1(P.x[k], G.x[k], M.x[k], V.x[k], c);
+    st8(p + i * 8, P);
+    st8(m + i * 8, M);
+    st8(v + i * 8, V);
+    if (SHADOW)
+      shadow[i] = make_uint4(pack2(P.x[0], P.x[1]), pack2(P.x[2], P.x[3]), pack2(P.x[4], P.x[5]),
+                             pack2(P.x[6], P.x[7]));
   }
 }
 
@@ -328,9 +394,19 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
   c.eps = static_cast<float>(eps);
   c.neg_step = static_cast<float>(-(lr / bc1));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool wide = n % 8 == 0 && aligned32(p) && aligned32(g) && aligned32(m) && aligned32(v) &&
+                    (!p_bf16_or_null || aligned16(p_bf16_or_null));
   const bool vec = n % 4 == 0 && aligned16(p) && aligned16(g) && aligned16(m) && aligned16(v) &&
                    (!p_bf16_or_null || (reinterpret_cast<uintptr_t>(p_bf16_or_null) & 7) == 0);
-  if (vec) {
+  if (wide) {
+    const int64_t n8 = n / 8;
+    const int grid = het::grid_for(n8, kThreads);
+    if (p_bf16_or_null)
+      adamw_v8_kernel<true><<<grid, kThreads, 0, st>>>(p, g, m, v,
+                                                       static_cast<uint4*>(p_bf16_or_null), n8, c);
+    else
+      adamw_v8_kernel<false><<<grid, kThreads, 0, st>>>(p, g, m, v, nullptr, n8, c);
+  } else if (vec) {
     const int64_t n4 = n / 4;
     const int grid = het::grid_for((n4 + 1) / 2, kThreads);
     if (p_bf16_or_null)
