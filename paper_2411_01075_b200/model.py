@@ -159,13 +159,24 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
         x = x + a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
         h = _rms(x, p["rms2"])
         return x + (F.silu(h @ p["w1"].t()) * (h @ p["w3"].t())) @ p["w2"].t()
-    h = F.layer_norm(x, (d,), p["ln1_w"], p["ln1_b"])
-    qkv = F.linear(h, p["qkv_w"], p["qkv_b"]).view(b, s, 3, H, dh).permute(2, 0, 3, 1, 4)
-    a = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=arch.kind == "gpt")
+    h = _ln(x, p["ln1_w"], p["ln1_b"])
+    # q/k/v as views of the fused projection in (b, s, H, dh) memory order: SDPA
+    # (cuDNN) keeps that layout for its output, so neither the head split nor
+    # the merge below copies, forward or backward
+    q, k, v = F.linear(h, p["qkv_w"], p["qkv_b"]).split(d, dim=-1)
+    q, k, v = (t.view(b, s, H, dh).transpose(1, 2) for t in (q, k, v))
+    a = F.scaled_dot_product_attention(q, k, v, is_causal=arch.kind == "gpt")
     x = x + F.linear(a.transpose(1, 2).reshape(b, s, d), p["proj_w"], p["proj_b"])
-    h = F.layer_norm(x, (d,), p["ln2_w"], p["ln2_b"])
+    h = _ln(x, p["ln2_w"], p["ln2_b"])
     h = F.gelu(F.linear(h, p["fc_w"], p["fc_b"]), approximate="tanh")
     return x + F.linear(h, p["fc2_w"], p["fc2_b"])
+
+
+def _ln(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """LayerNorm as normalize + separate affine: the affine's weight/bias
+    gradients become two row reductions instead of torch's GammaBeta backward
+    kernel (~4x slower on [m*seq, d] bf16 activations)."""
+    return torch.addcmul(b, F.layer_norm(x, (x.shape[-1],)), w)
 
 
 def embed_forward(arch: ArchSpec, p: dict[str, torch.Tensor], tokens: torch.Tensor) -> torch.Tensor:
@@ -181,6 +192,8 @@ def head_loss(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor,
     if arch.kind == "llama":
         h = _rms(x, p["normf"])
     else:
-        h = F.layer_norm(x, (arch.d,), p["lnf_w"], p["lnf_b"])
+        h = _ln(x, p["lnf_w"], p["lnf_b"])
     logits = h @ p["wte"].t()
-    return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), targets.reshape(-1).long())
+    # bf16 logits straight into the fused log-softmax/NLL (fp32 accumulation
+    # inside); no fp32 copy of the [tokens, vocab] matrix
+    return F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1).long())
