@@ -11,7 +11,9 @@ in the same schema. The planner consumes either unchanged.
 """
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
+from pathlib import Path
 
 from .core import ClusterSpec, ModelSpec, TrainPlan, cluster_from_dict, model_from_dict, profile_from_dict
 from .model import ARCHS, ArchSpec
@@ -111,12 +113,29 @@ def perf_from_docs(docs) -> ClusterPerf:
     return ClusterPerf(models)
 
 
-def build_job(name: str, n_gpus: int, global_batch: int | None = None) -> Job:
+MEASURED_DIR = Path(__file__).resolve().parent / "profiles_b200"
+
+
+def measured_profiles(name: str) -> dict[str, dict] | None:
+    """Profiles measured on a B200 by tools/profile_tiers.py, if committed."""
+    p = MEASURED_DIR / f"{name}.json"
+    if not p.exists():
+        return None
+    return {d["profile_key"]: d for d in json.loads(p.read_text())["profiles"]}
+
+
+def build_job(name: str, n_gpus: int, global_batch: int | None = None,
+              measured: bool = False) -> Job:
+    """Cluster, model, fitted perf models and the planner's plan for a config.
+    measured=True uses the B200-measured tier profiles when available (the
+    analytic ones otherwise)."""
     cfg = CONFIGS[name]
     arch = ARCHS[cfg.arch]
     tiers = list(cfg.tiers[:n_gpus]) if n_gpus <= len(cfg.tiers) else \
         [cfg.tiers[i % len(cfg.tiers)] for i in range(n_gpus)]
-    docs = tuple(tier_profile(arch, t) for t in sorted(set(tiers)))
+    meas = measured_profiles(name) if measured else None
+    docs = tuple(meas[t] if meas and t in meas else tier_profile(arch, t)
+                 for t in sorted(set(tiers)))
     cluster = cluster_from_dict(cluster_doc(arch, tiers))
     batch = global_batch if global_batch is not None else cfg.batch_per_gpu * n_gpus
     model = model_from_dict({"layers": arch.layers, "params_per_layer": arch.unit_params,
