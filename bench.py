@@ -192,6 +192,9 @@ def main() -> None:
     ap.add_argument("--config", default="gpt2_small", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--analytic-profiles", action="store_true",
+                    help="plan from the analytic tier profiles instead of the B200-measured ones "
+                         "(paper_2411_01075_b200/profiles_b200/)")
     ap.add_argument("--no-emulate", action="store_true",
                     help="run every rank on the full B200 (no green-context SM partition or "
                          "memory cap from the cluster spec)")
@@ -206,7 +209,7 @@ def main() -> None:
 
     world, rank, local = setup_dist()
     dev = torch.device("cuda", local)
-    job = build_job(args.config, world)
+    job = build_job(args.config, world, measured=not args.analytic_profiles)
     comm_ag, comm_rs = make_comms(world, rank)
     # heterogeneity emulation: this rank's tier -> HBM cap + green-context SM partition
     emu = emulate_tier(job.cluster, rank, dev, sm_partition=not args.no_emulate,
@@ -292,6 +295,9 @@ def main() -> None:
                        "plan": [[a.microbatch, a.num_microbatches, a.state_ratio]
                                 for a in plan.assignments],
                        "uneven_units": plan.unit_shards.uneven_units,
+                       "profiles": ("measured" if any(d.get("profile_key") for d in job.profile_docs)
+                                    and not args.analytic_profiles else "analytic"),
+                       "planner_predicted_iteration_ms": plan.predicted_iteration_ms,
                        "parallelism": f"uneven-fsdp{world}",
                        "emulation_rank0": emu.describe(),
                        "collectives": ("fused-symm" if tr.symm is not None else

@@ -17,7 +17,7 @@ from pathlib import Path
 
 from .core import ClusterSpec, ModelSpec, TrainPlan, cluster_from_dict, model_from_dict, profile_from_dict
 from .model import ARCHS, ArchSpec
-from .perf import ClusterPerf, fit_perf_model
+from .perf import ClusterPerf, FitError, fit_perf_model
 from .planner import dp_optimize
 
 GIB = 1 << 30
@@ -136,6 +136,11 @@ def build_job(name: str, n_gpus: int, global_batch: int | None = None,
     meas = measured_profiles(name) if measured else None
     docs = tuple(meas[t] if meas and t in meas else tier_profile(arch, t)
                  for t in sorted(set(tiers)))
+    if meas:
+        try:
+            perf_from_docs(docs)
+        except FitError:   # launch-bound tables with no linear tail: keep the analytic model
+            docs = tuple(tier_profile(arch, t) for t in sorted(set(tiers)))
     cluster = cluster_from_dict(cluster_doc(arch, tiers))
     batch = global_batch if global_batch is not None else cfg.batch_per_gpu * n_gpus
     model = model_from_dict({"layers": arch.layers, "params_per_layer": arch.unit_params,

@@ -57,7 +57,7 @@ def _time(fn, stream, reps: int) -> float:
 
 
 def unit_latencies(arch: ArchSpec, tier: str, ms: list[int], device: torch.device,
-                   reps: int = 5) -> tuple[list[float], list[float]]:
+                   reps: int = 9) -> tuple[list[float], list[float]]:
     stream, green = _tier_stream(tier, device)
     gen = torch.Generator(device=device).manual_seed(0)
     flat = init_flat(arch.unit_layout(), gen, device).to(torch.bfloat16)

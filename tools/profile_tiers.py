@@ -22,7 +22,7 @@ from paper_2411_01075_b200.profiler import compute_memory, profile_tier  # noqa:
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", nargs="*", default=sorted(CONFIGS))
-ap.add_argument("--max-m", type=int, default=8)
+ap.add_argument("--max-m", type=int, default=16)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
