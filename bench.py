@@ -192,6 +192,9 @@ def main() -> None:
     ap.add_argument("--config", default="gpt2_small", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace-dir", default=None,
+                    help="also trace one extra step per rank (CUDA events) and write "
+                         "rank<i>.jsonl / rank<i>.chrome.json / lint + per-layer report there")
     ap.add_argument("--analytic-profiles", action="store_true",
                     help="plan from the analytic tier profiles instead of the B200-measured ones "
                          "(paper_2411_01075_b200/profiles_b200/)")
@@ -270,6 +273,23 @@ def main() -> None:
     e1.record(comp)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    trace_report = None
+    if args.trace_dir:
+        from paper_2411_01075_b200 import trace as T
+        os.makedirs(args.trace_dir, exist_ok=True)
+        tr.tracer = T.StepTracer(job.cluster.gpus[rank].id)
+        tr.step(resident[-1])
+        ev = tr.tracer.collect()
+        tr.tracer = None
+        T.trace_to_jsonl(ev, os.path.join(args.trace_dir, f"rank{rank}.jsonl"))
+        T.trace_to_chrome(ev, os.path.join(args.trace_dir, f"rank{rank}.chrome.json"))
+        fwd_l, bwd_l = T.per_layer_metrics(ev, arch.layers)
+        trace_report = {"lint_problems": T.lint_measured_trace(ev, arch.layers),
+                        "measured_layer_fwd_ms": fwd_l, "measured_layer_bwd_ms": bwd_l,
+                        "predicted_layer_fwd_ms": plan.predicted_layer_fwd_ms,
+                        "predicted_layer_bwd_ms": plan.predicted_layer_bwd_ms, "events": len(ev)}
+        with open(os.path.join(args.trace_dir, f"rank{rank}.report.json"), "w") as fh:
+            json.dump(trace_report, fh, indent=1)
     ctx.__exit__(None, None, None)
 
     B = plan.total_batch
@@ -317,6 +337,8 @@ def main() -> None:
             "cpu_baseline": cpu,
             "loss": loss_val,
         }
+        if trace_report is not None:
+            line["trace_rank0"] = {k: v for k, v in trace_report.items() if k != "events"}
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
     if world > 1:

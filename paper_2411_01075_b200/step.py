@@ -26,6 +26,7 @@ accumulator is the grad shard itself: no collectives, no copies.
 """
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass, field
 
 import torch
@@ -159,6 +160,7 @@ class UnevenFSDPTrainer:
         self.steps = 0
         self.timers = StepTimers()
         self.launches = 0          # owned-kernel launches (hetstep.so), this process
+        self.tracer = None         # trace.StepTracer: per-event CUDA timelines when set
 
     # ------------------------------------------------------------------ params
     def _local(self, buf: torch.Tensor, u: int) -> torch.Tensor:
@@ -209,7 +211,19 @@ class UnevenFSDPTrainer:
                 return name
         raise InputError("buffer is not in the symmetric workspace")
 
-    def _ag(self, u: int, dst: torch.Tensor) -> torch.cuda.Event:
+    def _span(self, kind: str, u: int, mb: int, phase: str, stream):
+        """Trace span (simulator schema: blocks are units 1..L, the root is 0)."""
+        if self.tracer is None or not self.cuda:
+            return contextlib.nullcontext()
+        unit = 0 if u == self.L.root else u + 1
+        return self.tracer.span(kind, unit, mb, phase, stream)
+
+    def _ag(self, u: int, dst: torch.Tensor, phase: str = "fwd") -> torch.cuda.Event:
+        with self._span("allgather", u, 0, phase, self.ag_stream):
+            self._ag_issue(u, dst)
+        return self._event(self.ag_stream)
+
+    def _ag_issue(self, u: int, dst: torch.Tensor) -> None:
         if self.ag_route[u] == "symm":   # fused pack + NVLS/peer all-gather from fp32 master
             self.symm.allgather_pack(self._local(self.p32, u), self._region(dst), 0,
                                      self.L.counts[u], self.L.offsets[u], stream=self.ag_stream)
@@ -219,10 +233,14 @@ class UnevenFSDPTrainer:
                                self.L.offsets[u], self.comm_ag, self.rank,
                                K.ALGO_AUTO if self.algo == K.ALGO_SYMM else self.algo,
                                stream=self.ag_stream)
-        return self._event(self.ag_stream)
 
     def _rs(self, u: int, src: torch.Tensor, after: torch.cuda.Event) -> torch.cuda.Event:
         self.rs_stream.wait_event(after)
+        with self._span("reducescatter", u, 0, "bwd", self.rs_stream):
+            self._rs_issue(u, src)
+        return self._event(self.rs_stream)
+
+    def _rs_issue(self, u: int, src: torch.Tensor) -> None:
         if self.rs_route[u] == "symm":   # switch/peer reduction straight into the fp32 shard
             self.symm.reduce_scatter(self._region(src), 0, self._local(self.g32, u),
                                      self.L.counts[u], self.L.offsets[u],
@@ -233,7 +251,6 @@ class UnevenFSDPTrainer:
                                     self.L.offsets[u], self.comm_rs, self.rank,
                                     K.ALGO_AUTO if self.algo == K.ALGO_SYMM else self.algo,
                                     stream=self.rs_stream)
-        return self._event(self.rs_stream)
 
     def _unit_flat(self, u: int) -> torch.Tensor:
         if self.N == 1:
@@ -269,6 +286,8 @@ class UnevenFSDPTrainer:
         unit_names = [nm for nm, _ in arch.unit_layout()]
         root_names = [nm for nm, _ in arch.root_layout()]
         loss = torch.zeros((), dtype=torch.float32, device=self.device)
+        if self.tracer is not None and self.cuda:
+            self.tracer.begin(comp)
 
         # ---- forward -------------------------------------------------------
         ag_ev: dict[int, torch.cuda.Event] = {}
@@ -292,7 +311,8 @@ class UnevenFSDPTrainer:
         rp = views(self._unit_flat(root), arch.root_layout())
         with torch.no_grad():
             for k, (x_tok, _) in enumerate(mb):
-                h[k][0] = embed_forward(arch, rp, x_tok)
+                with self._span("fwd_compute", root, k + 1, "fwd", comp):
+                    h[k][0] = embed_forward(arch, rp, x_tok)
             for u in range(nb):
                 if multi:
                     if u + 1 < nb:
@@ -302,7 +322,8 @@ class UnevenFSDPTrainer:
                     comp.wait_event(ag_ev[u])
                 p = views(self._unit_flat(u), arch.unit_layout())
                 for k in range(len(mb)):
-                    h[k][u + 1] = block_forward(arch, p, h[k][u])
+                    with self._span("fwd_compute", u, k + 1, "fwd", comp):
+                        h[k][u + 1] = block_forward(arch, p, h[k][u])
                 done_ev[u] = self._event(comp)
 
         # ---- head + loss ---------------------------------------------------
@@ -311,14 +332,15 @@ class UnevenFSDPTrainer:
                   views(self._unit_flat(root), arch.root_layout()).items()}
         head_names = [nm for nm in root_names if nm != "wpe"]
         for k, (_, tgt) in enumerate(mb):
-            x = h[k][nb].requires_grad_(True)
-            with torch.enable_grad():
-                lk = head_loss(arch, leaves, x, tgt)
-            grads = torch.autograd.grad(lk, [leaves[nm] for nm in head_names] + [x])
-            dy[k] = grads[-1]
-            h[k][nb] = None
-            self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
-            loss += lk.detach() * self.w
+            with self._span("head", root, k + 1, "fwd", comp):
+                x = h[k][nb].requires_grad_(True)
+                with torch.enable_grad():
+                    lk = head_loss(arch, leaves, x, tgt)
+                grads = torch.autograd.grad(lk, [leaves[nm] for nm in head_names] + [x])
+                dy[k] = grads[-1]
+                h[k][nb] = None
+                self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
+                loss += lk.detach() * self.w
 
         # ---- backward --------------------------------------------------------
         rs_ev: dict[int, torch.cuda.Event] = {}
@@ -327,7 +349,7 @@ class UnevenFSDPTrainer:
                 # prefetch u-1 unless it is still resident from the forward
                 if u - 1 >= 0 and u - 1 < nb - 2:
                     self.ag_stream.wait_event(done_ev[u + 1])
-                    ag_ev[u - 1] = self._ag(u - 1, self.ubuf[(u - 1) % 2])
+                    ag_ev[u - 1] = self._ag(u - 1, self.ubuf[(u - 1) % 2], "bwd")
                 if u < nb - 2:
                     comp.wait_event(ag_ev[u])
                 if u + 2 in rs_ev:                  # acc[u % 2] last read by RS(u+2)
@@ -341,13 +363,16 @@ class UnevenFSDPTrainer:
             pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}
             plist = [pl[nm] for nm in unit_names]
             for k in range(len(mb)):
-                x = h[k][u].requires_grad_(True)
-                with torch.enable_grad():
-                    y = block_forward(arch, pl, x)
-                grads = torch.autograd.grad(y, plist + [x], dy[k])
-                dy[k] = grads[-1]
-                h[k][u] = None
-                self._accumulate(acc, grads[:-1], unit_names, self.unit_seg, first=(k == 0))
+                with self._span("recompute", u, k + 1, "bwd", comp):
+                    x = h[k][u].requires_grad_(True)
+                    with torch.enable_grad():
+                        y = block_forward(arch, pl, x)
+                with self._span("bwd_compute", u, k + 1, "bwd", comp):
+                    grads = torch.autograd.grad(y, plist + [x], dy[k])
+                    dy[k] = grads[-1]
+                    h[k][u] = None
+                    self._accumulate(acc, grads[:-1], unit_names, self.unit_seg,
+                                     first=(k == 0))
             done_ev[u] = self._event(comp)
             if multi:                                # an idle rank's acc holds zeros
                 rs_ev[u] = self._rs(u, acc, done_ev[u])
@@ -355,11 +380,12 @@ class UnevenFSDPTrainer:
         # ---- embedding backward + root RS -----------------------------------
         emb_names = ["wte"] if arch.kind == "llama" else ["wte", "wpe"]
         for k, (x_tok, _) in enumerate(mb):
-            with torch.enable_grad():
-                e = embed_forward(arch, leaves, x_tok)
-            grads = torch.autograd.grad(e, [leaves[nm] for nm in emb_names], dy[k])
-            dy[k] = None
-            self._accumulate(racc, grads, emb_names, self.root_seg, first=False)
+            with self._span("embed_bwd", root, k + 1, "bwd", comp):
+                with torch.enable_grad():
+                    e = embed_forward(arch, leaves, x_tok)
+                grads = torch.autograd.grad(e, [leaves[nm] for nm in emb_names], dy[k])
+                dy[k] = None
+                self._accumulate(racc, grads, emb_names, self.root_seg, first=False)
         if multi:
             rs_ev[root] = self._rs(root, racc, self._event(comp))
             comp.wait_event(rs_ev[root])            # RS stream is in order: all shards ready
@@ -371,9 +397,10 @@ class UnevenFSDPTrainer:
         if a is not None:
             a.record()
         shadow = self.p16 if self.need_shadow else None   # fused AG reads p32 itself
-        K.adamw(self.p32, self.g32, self.m32, self.v32, shadow, lr=self.opt.lr,
-                beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
-                weight_decay=self.opt.weight_decay, step=self.steps)
+        with self._span("optimizer", root, 0, "opt", comp):
+            K.adamw(self.p32, self.g32, self.m32, self.v32, shadow, lr=self.opt.lr,
+                    beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
+                    weight_decay=self.opt.weight_decay, step=self.steps)
         if b is not None:
             b.record()
         self.launches += 1

@@ -1,0 +1,173 @@
+"""Measured per-rank traces of the real train step in the reference
+simulator's schemas, plus a causality linter for them.
+
+The reference simulates one iteration and exports it as JSONL (one event per
+line: gpu, kind, unit, microbatch, phase, start_ms, end_ms — sim.py:549-561)
+or as a Chrome/Perfetto trace (pid = GPU, tid = stream, sim.py:564-599), and
+`lint_trace` (sim.py:459-542) checks the schedule's causality. Here the same
+event kinds are timed on the GPU with CUDA events on the stream that runs
+them (compute, all-gather, reduce-scatter), relative to a step-start event,
+so a real step can be inspected with the same tools and linted with the same
+rules:
+  * stream exclusivity: compute events of one GPU never overlap;
+  * fwd_compute(u, j) starts after the all-gather that delivered unit u;
+  * recompute(u, j) starts after unit u is resident for the backward (its
+    backward all-gather, or the forward one for the two units this step keeps
+    resident — DESIGN.md §3);
+  * bwd_compute(u, j) starts after recompute(u, j);
+  * reducescatter(u) starts after the rank's last bwd_compute(u, .).
+Units are 1-indexed like the simulator; the root unit (embeddings/head) is
+unit 0. Cross-rank rules of the simulator (identical collective windows on
+every GPU) do not apply to measured per-rank clocks and are not checked.
+"""
+from __future__ import annotations
+
+import json
+from contextlib import contextmanager
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Iterable
+
+import torch
+
+COMPUTE_KINDS = ("fwd_compute", "recompute", "bwd_compute", "head", "embed_bwd", "optimizer")
+COLLECTIVE_KINDS = ("allgather", "reducescatter")
+_TID = {"compute": 0, "h2d": 1, "d2h": 2, "network": 3}
+EPS = 1e-3          # ms; event timestamps have ~0.5 us resolution
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    gpu_id: str
+    kind: str
+    unit: int
+    microbatch: int
+    phase: str
+    start_ms: float
+    end_ms: float
+
+    @property
+    def duration_ms(self) -> float:
+        return self.end_ms - self.start_ms
+
+
+class StepTracer:
+    """Collects CUDA-event spans during one UnevenFSDPTrainer.step()."""
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self._spans: list[tuple[str, int, int, str, torch.cuda.Event, torch.cuda.Event]] = []
+        self._t0: torch.cuda.Event | None = None
+
+    def begin(self, stream) -> None:
+        self._spans.clear()
+        self._t0 = torch.cuda.Event(enable_timing=True)
+        self._t0.record(stream)
+
+    @contextmanager
+    def span(self, kind: str, unit: int, microbatch: int, phase: str, stream):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        try:
+            yield
+        finally:
+            b.record(stream)
+            self._spans.append((kind, unit, microbatch, phase, a, b))
+
+    def collect(self) -> list[TraceEvent]:
+        torch.cuda.synchronize()
+        out = [TraceEvent(self.gpu_id, k, u, j, ph, self._t0.elapsed_time(a),
+                          self._t0.elapsed_time(b)) for k, u, j, ph, a, b in self._spans]
+        return sorted(out, key=lambda e: (e.start_ms, e.kind, e.phase, e.unit, e.microbatch))
+
+
+def trace_to_jsonl(events: Iterable[TraceEvent], path: str | Path) -> None:
+    with open(path, "w") as fh:
+        for e in events:
+            fh.write(json.dumps({"gpu": e.gpu_id, "kind": e.kind, "unit": e.unit,
+                                 "microbatch": e.microbatch, "phase": e.phase,
+                                 "start_ms": e.start_ms, "end_ms": e.end_ms},
+                                sort_keys=True) + "\n")
+
+
+def _stream_of(kind: str) -> str:
+    return "network" if kind in COLLECTIVE_KINDS else "compute"
+
+
+def trace_to_chrome(events: Iterable[TraceEvent], path: str | Path) -> None:
+    events = list(events)
+    gpus = sorted({e.gpu_id for e in events})
+    pid = {g: i for i, g in enumerate(gpus)}
+    out = []
+    for g, p in pid.items():
+        out.append({"name": "process_name", "ph": "M", "pid": p, "tid": 0, "args": {"name": g}})
+        for s, t in _TID.items():
+            out.append({"name": "thread_name", "ph": "M", "pid": p, "tid": t, "args": {"name": s}})
+    for e in events:
+        tid = _TID[_stream_of(e.kind)] + (1 if e.kind == "reducescatter" else 0) * 10
+        out.append({"name": f"{e.kind} u{e.unit}" + (f" j{e.microbatch}" if e.microbatch else ""),
+                    "cat": e.phase, "ph": "X", "ts": e.start_ms * 1000.0,
+                    "dur": e.duration_ms * 1000.0, "pid": pid[e.gpu_id], "tid": tid,
+                    "args": {"unit": e.unit, "microbatch": e.microbatch}})
+    Path(path).write_text(json.dumps({"traceEvents": out, "displayTimeUnit": "ms"},
+                                     sort_keys=True) + "\n")
+
+
+def lint_measured_trace(events: Iterable[TraceEvent], blocks: int) -> list[str]:
+    """Per-GPU causality checks of a measured step (rules in the module doc)."""
+    problems: list[str] = []
+    by_gpu: dict[str, list[TraceEvent]] = {}
+    for e in events:
+        if e.end_ms < e.start_ms - EPS or e.start_ms < -EPS:
+            problems.append(f"bad interval on {e.gpu_id} {e.kind} u{e.unit} j{e.microbatch}")
+        by_gpu.setdefault(e.gpu_id, []).append(e)
+    for g, evs in by_gpu.items():
+        comp = sorted((e for e in evs if e.kind in COMPUTE_KINDS), key=lambda e: e.start_ms)
+        for a, b in zip(comp, comp[1:]):
+            if b.start_ms < a.end_ms - EPS:
+                problems.append(f"compute overlap on {g}: {a.kind} u{a.unit} / {b.kind} u{b.unit}")
+        ag = {(e.phase, e.unit): e for e in evs if e.kind == "allgather"}
+        idx = {(e.kind, e.unit, e.microbatch): e for e in evs if e.kind in COMPUTE_KINDS}
+        last_bwd: dict[int, float] = {}
+        for e in evs:
+            if e.kind == "fwd_compute":
+                c = ag.get(("fwd", e.unit))
+                if c and e.start_ms < c.end_ms - EPS:
+                    problems.append(f"F u{e.unit} j{e.microbatch} on {g} starts before its allgather")
+            elif e.kind == "recompute":
+                c = ag.get(("bwd", e.unit)) or ag.get(("fwd", e.unit))
+                if c and e.start_ms < c.end_ms - EPS:
+                    problems.append(f"RA u{e.unit} j{e.microbatch} on {g} starts before its allgather")
+            elif e.kind == "bwd_compute":
+                ra = idx.get(("recompute", e.unit, e.microbatch))
+                if ra and e.start_ms < ra.end_ms - EPS:
+                    problems.append(f"B u{e.unit} j{e.microbatch} on {g} starts before its recompute")
+                last_bwd[e.unit] = max(last_bwd.get(e.unit, 0.0), e.end_ms)
+        for e in evs:
+            if e.kind == "reducescatter" and e.unit in last_bwd and \
+                    e.start_ms < last_bwd[e.unit] - EPS:
+                problems.append(f"reducescatter u{e.unit} on {g} starts before its last backward")
+        for u in range(1, blocks + 1):
+            if ("fwd_compute", u, 1) not in idx and any(e.kind == "fwd_compute" for e in evs):
+                problems.append(f"unit {u} never ran forward on {g}")
+    return problems
+
+
+def per_layer_metrics(events: Iterable[TraceEvent], blocks: int) -> tuple[float, float]:
+    """Measured per-layer forward / backward period (the simulator's
+    definition, sim.py:412-425): max gap between consecutive units' first
+    microbatch starts, per GPU, maximised over GPUs."""
+    events = list(events)
+    fwd = bwd = 0.0
+    for g in {e.gpu_id for e in events}:
+        fs = {e.unit: e.start_ms for e in events
+              if e.gpu_id == g and e.kind == "fwd_compute" and e.microbatch == 1}
+        bs = {e.unit: e.start_ms for e in events
+              if e.gpu_id == g and e.kind == "recompute" and e.microbatch == 1}
+        for u in range(1, blocks):
+            if u in fs and u + 1 in fs:
+                fwd = max(fwd, fs[u + 1] - fs[u])
+            if u in bs and u + 1 in bs:
+                bwd = max(bwd, bs[u] - bs[u + 1])
+    return fwd, bwd

@@ -142,7 +142,12 @@ def main(out_dir: str) -> None:
         trs = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev,
                                 algo=K.ALGO_SYMM)
         trs.load_full_units(units)
+        from paper_2411_01075_b200.trace import StepTracer, lint_measured_trace
+        trs.tracer = StepTracer(f"g{rank}")
         loss_s = trs.step(torch.from_numpy(tok).to(dev))
+        report["trace_lint_problems"] = float(len(lint_measured_trace(trs.tracer.collect(),
+                                                                      arch.layers)))
+        trs.tracer = None
         dist.all_reduce(loss_s)
         gs = [t.cpu().numpy() for t in trs.full_units("g32")]
         ps = [t.cpu().numpy() for t in trs.full_units("p32")]

@@ -47,6 +47,8 @@ def test_multigpu_collectives_and_step(tmp_path):
                 assert v <= FP32_RTOL, f"reduce-scatter {k}: {v}"
             elif k.startswith("symm_status"):
                 assert v == 0.0, f"symmetric barrier timed out ({k})"
+            elif k == "trace_lint_problems":
+                assert v == 0.0, "measured multi-rank trace violates the schedule's causality"
     arch = ARCHS["tiny_gpt"]
     micro = [tuple(int(x) for x in mi) for mi in r[0]["micro"]]
     ratios = [float(x) for x in r[0]["ratios"]]
