@@ -179,11 +179,15 @@ class UnevenFSDPTrainer:
             c = self.L.counts[u][self.rank]
             self._local(self.p32, u).copy_(full.reshape(-1)[o:o + c].to(self.device,
                                                                         torch.float32))
-        K.pack_bf16(self.p32, self.p16)
-        self.launches += 1
+        self.refresh_shadow()
         self.m32.zero_()
         self.v32.zero_()
         self.steps = 0
+
+    def refresh_shadow(self) -> None:
+        """Re-derive the bf16 all-gather shadow from the fp32 master (kernel 1)."""
+        K.pack_bf16(self.p32, self.p16)
+        self.launches += 1
 
     def init_params(self, seed: int = 0) -> None:
         """Deterministic N(0, 0.02) init; every rank derives the same full

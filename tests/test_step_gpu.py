@@ -81,3 +81,21 @@ def test_loss_decreases_over_steps(cuda):
     tok = torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=7, step=0)).to(cuda)
     losses = [float(tr.step(tok)) for _ in range(8)]   # same batch: must overfit
     assert losses[-1] < losses[0] - 0.05, losses
+
+
+def test_checkpoint_resume_on_gpu(cuda, tmp_path):
+    from paper_2411_01075_b200.checkpoint import load_trainer, save_trainer
+    arch = ARCHS["tiny_gpt"]
+    plan = one_gpu_plan(arch, 2, 2)
+    a = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda)
+    a.init_params(seed=5)
+    tok = [torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=2, step=s)).to(cuda)
+           for s in range(2)]
+    a.step(tok[0])
+    save_trainer(a, tmp_path)
+    b = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda)
+    assert load_trainer(b, tmp_path) == 1
+    la, lb = a.step(tok[1]), b.step(tok[1])
+    torch.cuda.synchronize()
+    assert torch.equal(la, lb)
+    assert torch.equal(a.p32, b.p32) and torch.equal(a.p16, b.p16)
