@@ -95,7 +95,10 @@ def test_checkpoint_resume_on_gpu(cuda, tmp_path):
     save_trainer(a, tmp_path)
     b = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda)
     assert load_trainer(b, tmp_path) == 1
+    for name in ("p32", "m32", "v32", "p16"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
     la, lb = a.step(tok[1]), b.step(tok[1])
     torch.cuda.synchronize()
-    assert torch.equal(la, lb)
-    assert torch.equal(a.p32, b.p32) and torch.equal(a.p16, b.p16)
+    # the resumed step matches (attention backward may reduce in a different order)
+    assert abs(float(la) - float(lb)) <= 1e-6 * abs(float(la))
+    assert _nrel(b.p32.cpu().numpy(), a.p32.cpu().numpy()) <= 1e-5
