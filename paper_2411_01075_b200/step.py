@@ -98,7 +98,8 @@ class UnevenFSDPTrainer:
     def __init__(self, arch: ArchSpec, plan: TrainPlan, rank: int, *,
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
-                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64):
+                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64,
+                 offload_activations: bool = False):
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
         self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo
@@ -161,6 +162,15 @@ class UnevenFSDPTrainer:
         self.timers = StepTimers()
         self.launches = 0          # owned-kernel launches (hetstep.so), this process
         self.tracer = None         # trace.StepTracer: per-event CUDA timelines when set
+        # activation checkpoint offload (schedule sim.py:226-338):
+        # unit-boundary checkpoints go to pinned host memory on a D2H stream after the
+        # forward uses them and come back one unit ahead of their recompute on an H2D stream
+        self.offload = offload_activations and self.cuda
+        if self.offload:
+            self.d2h_stream = torch.cuda.Stream(device=dev)
+            self.h2d_stream = torch.cuda.Stream(device=dev)
+            self._host: dict[tuple[int, int], torch.Tensor] = {}
+            self._off_ev: dict[tuple[int, int], torch.cuda.Event] = {}
 
     # ------------------------------------------------------------------ params
     def _local(self, buf: torch.Tensor, u: int) -> torch.Tensor:
@@ -199,6 +209,32 @@ class UnevenFSDPTrainer:
             layout = self.arch.root_layout() if u == self.L.root else self.arch.unit_layout()
             units.append(init_flat(layout, gen, self.device))
         self.load_full_units(units)
+
+    # ------------------------------------------------------------------ offload
+    def _offload(self, k: int, u: int, t: torch.Tensor, comp) -> None:
+        host = self._host.get((k, u))
+        if host is None or host.shape != t.shape:
+            host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            self._host[(k, u)] = host
+        self.d2h_stream.wait_stream(comp)
+        with self._span("offload_act", u, k + 1, "fwd", self.d2h_stream):
+            with torch.cuda.stream(self.d2h_stream):
+                host.copy_(t, non_blocking=True)
+        t.record_stream(self.d2h_stream)       # GPU copy released once the D2H lands
+        ev = torch.cuda.Event()
+        ev.record(self.d2h_stream)
+        self._off_ev[(k, u)] = ev
+
+    def _prefetch(self, u: int, nmb: int) -> tuple[list[torch.Tensor], torch.cuda.Event]:
+        out = []
+        for k in range(nmb):
+            self.h2d_stream.wait_event(self._off_ev[(k, u)])
+            with self._span("prefetch_act", u, k + 1, "bwd", self.h2d_stream):
+                with torch.cuda.stream(self.h2d_stream):
+                    out.append(self._host[(k, u)].to(self.device, non_blocking=True))
+        ev = torch.cuda.Event()
+        ev.record(self.h2d_stream)
+        return out, ev
 
     # ------------------------------------------------------------------ comm
     def _event(self, stream):
@@ -329,6 +365,13 @@ class UnevenFSDPTrainer:
                     with self._span("fwd_compute", u, k + 1, "fwd", comp):
                         h[k][u + 1] = block_forward(arch, p, h[k][u])
                 done_ev[u] = self._event(comp)
+                if self.offload:                  # unit u's inputs are now only recompute inputs
+                    for k in range(len(mb)):
+                        self._offload(k, u, h[k][u], comp)
+                        h[k][u] = None
+        pref: dict[int, tuple[list[torch.Tensor], torch.cuda.Event]] = {}
+        if self.offload and mb:
+            pref[nb - 1] = self._prefetch(nb - 1, len(mb))
 
         # ---- head + loss ---------------------------------------------------
         dy: list[torch.Tensor | None] = [None] * len(mb)
@@ -362,6 +405,14 @@ class UnevenFSDPTrainer:
                     # peers read acc[u % 2] remotely during RS(u+2): my RS(u+1) having
                     # passed its start barrier proves every rank finished RS(u+2)
                     comp.wait_event(rs_ev[u + 1])
+            if self.offload and mb:
+                if u - 1 >= 0:                    # one unit of look-ahead
+                    pref[u - 1] = self._prefetch(u - 1, len(mb))
+                tensors, ev = pref.pop(u)
+                comp.wait_event(ev)
+                for k, t in enumerate(tensors):
+                    t.record_stream(comp)
+                    h[k][u] = t
             acc = self._acc(u)
             flat = self._unit_flat(u)
             pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}

@@ -15,6 +15,9 @@ rules:
     backward all-gather, or the forward one for the two units this step keeps
     resident — DESIGN.md §3);
   * bwd_compute(u, j) starts after recompute(u, j);
+  * with activation offload: the H2D and D2H copy streams are each exclusive,
+    offload_act(u, j) starts after the forward that consumed the checkpoint,
+    and recompute(u, j) starts after prefetch_act(u, j) landed;
   * reducescatter(u) starts after the rank's last bwd_compute(u, .).
 Units are 1-indexed like the simulator; the root unit (embeddings/head) is
 unit 0. Cross-rank rules of the simulator (identical collective windows on
@@ -32,6 +35,8 @@ import torch
 
 COMPUTE_KINDS = ("fwd_compute", "recompute", "bwd_compute", "head", "embed_bwd", "optimizer")
 COLLECTIVE_KINDS = ("allgather", "reducescatter")
+H2D_KINDS = ("prefetch_act", "prefetch_grad")
+D2H_KINDS = ("offload_act", "offload_grad")
 _TID = {"compute": 0, "h2d": 1, "d2h": 2, "network": 3}
 EPS = 1e-3          # ms; event timestamps have ~0.5 us resolution
 
@@ -92,6 +97,10 @@ def trace_to_jsonl(events: Iterable[TraceEvent], path: str | Path) -> None:
 
 
 def _stream_of(kind: str) -> str:
+    if kind in H2D_KINDS:
+        return "h2d"
+    if kind in D2H_KINDS:
+        return "d2h"
     return "network" if kind in COLLECTIVE_KINDS else "compute"
 
 
@@ -123,12 +132,15 @@ def lint_measured_trace(events: Iterable[TraceEvent], blocks: int) -> list[str]:
             problems.append(f"bad interval on {e.gpu_id} {e.kind} u{e.unit} j{e.microbatch}")
         by_gpu.setdefault(e.gpu_id, []).append(e)
     for g, evs in by_gpu.items():
-        comp = sorted((e for e in evs if e.kind in COMPUTE_KINDS), key=lambda e: e.start_ms)
-        for a, b in zip(comp, comp[1:]):
-            if b.start_ms < a.end_ms - EPS:
-                problems.append(f"compute overlap on {g}: {a.kind} u{a.unit} / {b.kind} u{b.unit}")
+        for kinds, label in ((COMPUTE_KINDS, "compute"), (H2D_KINDS, "h2d"), (D2H_KINDS, "d2h")):
+            ss = sorted((e for e in evs if e.kind in kinds), key=lambda e: e.start_ms)
+            for a, b in zip(ss, ss[1:]):
+                if b.start_ms < a.end_ms - EPS:
+                    problems.append(f"{label} overlap on {g}: {a.kind} u{a.unit} / "
+                                    f"{b.kind} u{b.unit}")
         ag = {(e.phase, e.unit): e for e in evs if e.kind == "allgather"}
-        idx = {(e.kind, e.unit, e.microbatch): e for e in evs if e.kind in COMPUTE_KINDS}
+        idx = {(e.kind, e.unit, e.microbatch): e for e in evs
+               if e.kind in COMPUTE_KINDS + H2D_KINDS + D2H_KINDS}
         last_bwd: dict[int, float] = {}
         for e in evs:
             if e.kind == "fwd_compute":
@@ -139,6 +151,15 @@ def lint_measured_trace(events: Iterable[TraceEvent], blocks: int) -> list[str]:
                 c = ag.get(("bwd", e.unit)) or ag.get(("fwd", e.unit))
                 if c and e.start_ms < c.end_ms - EPS:
                     problems.append(f"RA u{e.unit} j{e.microbatch} on {g} starts before its allgather")
+                pf = idx.get(("prefetch_act", e.unit, e.microbatch))
+                if pf and e.start_ms < pf.end_ms - EPS:
+                    problems.append(f"RA u{e.unit} j{e.microbatch} on {g} starts before its "
+                                    "input prefetch")
+            elif e.kind == "offload_act":
+                f = idx.get(("fwd_compute", e.unit, e.microbatch))
+                if f and e.start_ms < f.end_ms - EPS:
+                    problems.append(f"offload_act u{e.unit} j{e.microbatch} on {g} starts "
+                                    "before its consumer finished")
             elif e.kind == "bwd_compute":
                 ra = idx.get(("recompute", e.unit, e.microbatch))
                 if ra and e.start_ms < ra.end_ms - EPS:
