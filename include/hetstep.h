@@ -74,6 +74,21 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
               double lr, double beta1, double beta2, double eps, double weight_decay,
               int64_t step, void* stream);
 
+/* (4b) embedding backward fused with layered accumulation of the root unit:
+ *   acc[wte_off + t*d + c] += scale * sum_{i : token[i] == t} dy[i, c]
+ *   acc[wpe_off + s*d + c] += scale * sum_{i : i % seq == s} dy[i, c]   (wpe_off >= 0)
+ * dy: bf16 [rows, d] (rows = m*seq) upstream gradient of the embedding output.
+ * order/seg_start/seg_token: the rows sorted by token id (stable) and the
+ * run boundaries (nseg unique tokens), built on the device by the caller.
+ * One CTA owns each token row / position row and sums its contributions in
+ * fp32 in a fixed order: deterministic, no atomics, and no [vocab, d] bf16
+ * dense gradient is ever materialised (replaces embedding_dense_backward +
+ * het_accumulate of its output). */
+int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void* dy_bf16,
+                       int64_t rows, int64_t d, const int32_t* order, const int32_t* seg_start,
+                       const int32_t* seg_token, int64_t nseg, int64_t seq, float scale,
+                       void* stream);
+
 /* fill / zero helpers used by the step driver (idle ranks, pads) */
 int het_fill_f32(float* dst, float value, int64_t n, void* stream);
 

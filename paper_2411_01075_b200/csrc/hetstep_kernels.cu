@@ -316,6 +316,48 @@ __global__ void adamw_scalar_kernel(float* __restrict__ p, const float* __restri
   }
 }
 
+// ---------------------------------------------------------------- embedding grad
+
+// blockIdx.x < nseg: token run; otherwise position row (wpe). Each thread owns
+// kVecE columns of the row (d <= kThreads * kVecE).
+constexpr int kVecE = 8;
+
+__global__ void __launch_bounds__(kThreads) embedding_grad_kernel(
+    float* __restrict__ acc, int64_t wte_off, int64_t wpe_off,
+    const __nv_bfloat16* __restrict__ dy, int64_t rows, int64_t d,
+    const int32_t* __restrict__ order, const int32_t* __restrict__ seg_start,
+    const int32_t* __restrict__ seg_token, int64_t nseg, int64_t seq, float w) {
+  const int64_t b = blockIdx.x;
+  for (int64_t c0 = static_cast<int64_t>(threadIdx.x) * kVecE; c0 < d;
+       c0 += static_cast<int64_t>(blockDim.x) * kVecE) {
+    float sum[kVecE];
+#pragma unroll
+    for (int k = 0; k < kVecE; ++k) sum[k] = 0.f;
+    const bool vec = c0 + kVecE <= d && (d % kVecE) == 0;
+    auto add_row = [&](int64_t r) {
+      const __nv_bfloat16* row = dy + r * d + c0;
+      if (vec) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(row), f);
+#pragma unroll
+        for (int k = 0; k < kVecE; ++k) sum[k] += f[k];
+      } else {
+        for (int k = 0; k < kVecE && c0 + k < d; ++k) sum[k] += __bfloat162float(row[k]);
+      }
+    };
+    int64_t dst;
+    if (b < nseg) {
+      for (int32_t i = seg_start[b]; i < seg_start[b + 1]; ++i) add_row(order[i]);
+      dst = wte_off + static_cast<int64_t>(seg_token[b]) * d + c0;
+    } else {
+      const int64_t s = b - nseg;
+      for (int64_t r = s; r < rows; r += seq) add_row(r);
+      dst = wpe_off + s * d + c0;
+    }
+    for (int k = 0; k < kVecE && c0 + k < d; ++k) acc[dst + k] = fmaf(w, sum[k], acc[dst + k]);
+  }
+}
+
 __global__ void fill_kernel(float* __restrict__ dst, float value, int64_t n) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -423,6 +465,22 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
         p, g, m, v, static_cast<__nv_bfloat16*>(p_bf16_or_null), n, c);
   }
   return het::check_launch("het_adamw");
+}
+
+int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void* dy_bf16,
+                       int64_t rows, int64_t d, const int32_t* order, const int32_t* seg_start,
+                       const int32_t* seg_token, int64_t nseg, int64_t seq, float scale,
+                       void* stream) {
+  if (!acc || !dy_bf16 || rows < 0 || d <= 0 || nseg < 0 || seq <= 0 || wte_off < 0 ||
+      (nseg > 0 && (!order || !seg_start || !seg_token)))
+    return fail(HET_EARG, "het_embedding_grad: bad args");
+  const int64_t blocks = nseg + (wpe_off >= 0 ? seq : 0);
+  if (blocks == 0 || rows == 0) return HET_OK;
+  embedding_grad_kernel<<<static_cast<unsigned>(blocks), kThreads, 0,
+                          static_cast<cudaStream_t>(stream)>>>(
+      acc, wte_off, wpe_off, static_cast<const __nv_bfloat16*>(dy_bf16), rows, d, order,
+      seg_start, seg_token, nseg, seq, scale);
+  return het::check_launch("het_embedding_grad");
 }
 
 int het_fill_f32(float* dst, float value, int64_t n, void* stream) {

@@ -27,7 +27,7 @@ HET_SYMM_TIMEOUT = 17
 SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
-           "het_fill_f32", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_fill_f32", "het_embedding_grad", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
@@ -62,6 +62,7 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_accumulate": ([vp, ctypes.POINTER(HetSeg), i32, i32, f32, vp], i32),
         "het_adamw": ([vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, i64, vp], i32),
         "het_fill_f32": ([vp, f32, i64, vp], i32),
+        "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
         "het_comm_destroy": ([vp], i32),
@@ -157,6 +158,29 @@ def adamw(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,
                             _cuda(m, torch.float32, "m"), _cuda(v, torch.float32, "v"), sh, n,
                             lr, beta1, beta2, eps, weight_decay, int(step), _stream(stream)),
            "het_adamw")
+
+
+def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: torch.Tensor,
+                   tokens: torch.Tensor, seq: int, scale: float, stream=None) -> None:
+    """Fused embedding backward + layered accumulate into the fp32 root
+    accumulator (see include/hetstep.h het_embedding_grad). tokens: [rows]
+    (any int dtype), dy: bf16 [rows, d]."""
+    rows, d = dy.reshape(-1, dy.shape[-1]).shape
+    tok = tokens.reshape(-1)
+    if tok.numel() != rows:
+        raise InputError("embedding_grad: one token per gradient row")
+    srt, order = torch.sort(tok.to(torch.int64), stable=True)
+    uniq, counts = torch.unique_consecutive(srt, return_counts=True)
+    seg = torch.zeros(uniq.numel() + 1, dtype=torch.int32, device=dy.device)
+    torch.cumsum(counts, 0, out=seg[1:])
+    order32 = order.to(torch.int32)
+    uniq32 = uniq.to(torch.int32)
+    dyc = dy.reshape(rows, d).contiguous()
+    _check(load().het_embedding_grad(
+        _cuda(acc, torch.float32, "acc"), int(wte_off), -1 if wpe_off is None else int(wpe_off),
+        _cuda(dyc, torch.bfloat16, "dy"), rows, d, order32.data_ptr(), seg.data_ptr(),
+        uniq32.data_ptr(), uniq.numel(), int(seq), float(scale), _stream(stream)),
+        "het_embedding_grad")
 
 
 def fill(dst: torch.Tensor, value: float, stream=None) -> None:

@@ -433,14 +433,15 @@ class UnevenFSDPTrainer:
                 rs_ev[u] = self._rs(u, acc, done_ev[u])
 
         # ---- embedding backward + root RS -----------------------------------
-        emb_names = ["wte"] if arch.kind == "llama" else ["wte", "wpe"]
+        # fused embedding backward: token / position rows summed in fp32 straight into
+        # the root accumulator (no dense [vocab, d] bf16 gradient, deterministic order)
+        wpe_off = self.root_seg.get("wpe") if arch.kind != "llama" else None
         for k, (x_tok, _) in enumerate(mb):
             with self._span("embed_bwd", root, k + 1, "bwd", comp):
-                with torch.enable_grad():
-                    e = embed_forward(arch, leaves, x_tok)
-                grads = torch.autograd.grad(e, [leaves[nm] for nm in emb_names], dy[k])
+                K.embedding_grad(racc, self.root_seg["wte"], wpe_off, dy[k], x_tok, arch.seq,
+                                 self.w)
+                self.launches += 1
                 dy[k] = None
-                self._accumulate(racc, grads, emb_names, self.root_seg, first=False)
         if multi:
             rs_ev[root] = self._rs(root, racc, self._event(comp))
             comp.wait_event(rs_ev[root])            # RS stream is in order: all shards ready

@@ -65,6 +65,21 @@ def adamw(p, g, m, v, shadow, *, lr, beta1, beta2, eps, weight_decay, step, stre
         pack_bf16(p, shadow)
 
 
+def embedding_grad(acc, wte_off, wpe_off, dy, tokens, seq, scale, stream=None):
+    calls.append("embedding_grad")
+    d = dy.shape[-1]
+    g = dy.reshape(-1, d).float()
+    tok = tokens.reshape(-1).long()
+    wte = torch.zeros(int(tok.max()) + 1, d)
+    wte.index_add_(0, tok, g)
+    rows = torch.arange(wte.shape[0])
+    for r in rows.tolist():
+        acc[wte_off + r * d: wte_off + (r + 1) * d] += scale * wte[r]
+    if wpe_off is not None:
+        pos = g.view(-1, seq, d).sum(0)
+        acc[wpe_off: wpe_off + seq * d] += scale * pos.reshape(-1)
+
+
 def fill(dst, value, stream=None):
     calls.append("fill")
     dst.fill_(value)

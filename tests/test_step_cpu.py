@@ -53,6 +53,7 @@ def test_single_rank_step_gradients(fake, m, l):
         assert float((got - g.double()).norm() / g.double().norm()) <= 2e-2
     # one accumulate per (unit, microbatch) + head and embedding passes, one AdamW
     n_acc = fake.calls.count("accumulate")
-    assert n_acc == arch.layers * l + 2 * l
+    assert n_acc == arch.layers * l + l            # units + head; embedding is fused
+    assert fake.calls.count("embedding_grad") == l
     assert fake.calls.count("adamw") == 1
     assert "allgather" not in fake.calls and "reduce_scatter" not in fake.calls
