@@ -3,6 +3,10 @@
 import os
 import sys
 
+# deterministic cuBLAS workspaces, so tests may enable torch's deterministic
+# algorithms (must be set before the first cuBLAS handle is created)
+os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

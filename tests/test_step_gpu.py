@@ -108,11 +108,25 @@ def test_activation_offload_matches_and_saves_memory(cuda):
     """Checkpoint offload leaves the step's math
     unchanged, is lint-clean against the simulator's offload rules, and cuts
     the resident boundary activations."""
-    from paper_2411_01075_b200.trace import StepTracer, lint_measured_trace
     arch = ARCHS["gpt2_small"]
     plan = one_gpu_plan(arch, 4, 4)
     tok = torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=3, step=0)).to(cuda)
     res = {}
+    torch.use_deterministic_algorithms(True)   # deterministic cuDNN attention backward
+    try:
+        _offload_runs(arch, plan, tok, cuda, res)
+    finally:
+        torch.use_deterministic_algorithms(False)
+    assert {"offload_act", "prefetch_act"} <= res[True][3]
+    assert res[True][0] == res[False][0]
+    assert torch.equal(res[True][1], res[False][1])       # offload moves bytes, not math
+    # 12 units x 4 microbatches x [4, 512, 768] bf16 checkpoints = 151 MB resident without
+    # offload; with it at most ~2 units' worth stays on the GPU
+    assert res[True][2] < res[False][2] - 80e6, (res[True][2], res[False][2])
+
+
+def _offload_runs(arch, plan, tok, cuda, res):
+    from paper_2411_01075_b200.trace import StepTracer, lint_measured_trace
     for off in (False, True):
         tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda, offload_activations=off)
         tr.init_params(seed=1)
@@ -127,9 +141,3 @@ def test_activation_offload_matches_and_saves_memory(cuda):
         assert lint_measured_trace(ev, arch.layers) == [], off
         res[off] = (float(loss), tr.p32.clone(), peak, {e.kind for e in ev})
         del tr
-    assert {"offload_act", "prefetch_act"} <= res[True][3]
-    assert abs(res[True][0] - res[False][0]) <= 1e-6 * abs(res[False][0])
-    assert _nrel(res[True][1].cpu().numpy(), res[False][1].cpu().numpy()) <= 1e-5
-    # 12 units x 4 microbatches x [4, 512, 768] bf16 checkpoints = 151 MB resident without
-    # offload; with it at most ~2 units' worth stays on the GPU
-    assert res[True][2] < res[False][2] - 80e6, (res[True][2], res[False][2])
