@@ -89,6 +89,13 @@ int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void*
                        const int32_t* seg_token, int64_t nseg, int64_t seq, float scale,
                        void* stream);
 
+/* Launch-shape tuning knobs (process-wide; defaults are the measured best).
+ * HET_TUNE_ACC_VARIANT: het_accumulate CTA shape index 0..5
+  * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));
+ * default 4, measured fastest on B200 (tools/acc_bench.cu). */
+#define HET_TUNE_ACC_VARIANT 1
+int het_tune(int key, int value);
+
 /* fill / zero helpers used by the step driver (idle ranks, pads) */
 int het_fill_f32(float* dst, float value, int64_t n, void* stream);
 

@@ -147,18 +147,24 @@ struct SegTable {
 };
 
 constexpr int kAccVec = 8;                 // bf16 elements per 16-byte load
-constexpr int kAccIters = 4;               // 16-byte requests in flight per thread
-constexpr int64_t kAccChunk = static_cast<int64_t>(kThreads) * kAccVec * kAccIters;
+// (THREADS, ITERS) variants: ITERS 16-byte gradient loads in flight per thread;
+// a CTA covers THREADS * 8 * ITERS elements of one segment.
+struct AccShape {
+  int threads, iters;
+};
+constexpr AccShape kAccShapes[] = {{256, 4}, {256, 2}, {256, 1}, {512, 2}, {512, 1}, {128, 4}};
+int g_acc_variant = 4;   // het_tune(HET_TUNE_ACC_VARIANT, i); 4 = (512 threads, 1 load) measured best
 
 template <int MODE>
 __device__ __forceinline__ float acc_op(float a, float g, float w) {
   return MODE == HET_ACC_FIRST ? w * g : fmaf(w, g, a);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict__ acc,
-                                                              const __grid_constant__ SegTable t,
-                                                              float w) {
+template <int MODE, int THREADS, int ITERS>
+__global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__ acc,
+                                                             const __grid_constant__ SegTable t,
+                                                             float w) {
+  constexpr int64_t kAccChunk = static_cast<int64_t>(THREADS) * kAccVec * ITERS;
   // locate this block's segment (<= 64 entries; warp-uniform scan)
   const int64_t b = blockIdx.x;
   int s = 0;
@@ -170,12 +176,12 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict_
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
                       ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
   if (vec_ok && base + kAccChunk <= sg.n) {
-    uint4 raw[kAccIters];
-    F8 a[kAccIters];
+    uint4 raw[ITERS];
+    F8 a[ITERS];
     const bool wide = aligned32(dst);     // 256-bit accumulator accesses
 #pragma unroll
-    for (int it = 0; it < kAccIters; ++it) {
-      const int64_t e = base + (static_cast<int64_t>(it) * kThreads + threadIdx.x) * kAccVec;
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t e = base + (static_cast<int64_t>(it) * THREADS + threadIdx.x) * kAccVec;
       raw[it] = __ldcs(reinterpret_cast<const uint4*>(src + e));
       if (MODE == HET_ACC_FIRST) {
 #pragma unroll
@@ -189,8 +195,8 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict_
       }
     }
 #pragma unroll
-    for (int it = 0; it < kAccIters; ++it) {
-      const int64_t e = base + (static_cast<int64_t>(it) * kThreads + threadIdx.x) * kAccVec;
+    for (int it = 0; it < ITERS; ++it) {
+      const int64_t e = base + (static_cast<int64_t>(it) * THREADS + threadIdx.x) * kAccVec;
       float g[8];
       unpack8(raw[it], g);
       F8 o;
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(float* __restrict_
   }
   // ragged tail of a segment (or unaligned segment): scalar, coalesced
   const int64_t end = base + kAccChunk < sg.n ? base + kAccChunk : sg.n;
-  for (int64_t e = base + threadIdx.x; e < end; e += kThreads) {
+  for (int64_t e = base + threadIdx.x; e < end; e += THREADS) {
     const float g = __bfloat162float(src[e]);
     const float a = (MODE & HET_ACC_FIRST) ? 0.f : dst[e];
     dst[e] = acc_op<MODE>(a, g, w);
@@ -396,13 +402,15 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
     return fail(HET_EARG, "het_accumulate: bad args (nseg=%d mode=%d)", nseg, mode);
   SegTable t;
   t.nseg = nseg;
+  const AccShape shape = kAccShapes[g_acc_variant];
+  const int64_t chunk = static_cast<int64_t>(shape.threads) * kAccVec * shape.iters;
   int64_t blocks = 0;
   for (int s = 0; s < nseg; ++s) {
     if (segs[s].n < 0 || segs[s].dst_off < 0 || (segs[s].n > 0 && !segs[s].src))
       return fail(HET_EARG, "het_accumulate: bad segment %d", s);
     t.seg[s] = segs[s];
     t.first_block[s] = blocks;
-    blocks += (segs[s].n + kAccChunk - 1) / kAccChunk;
+    blocks += (segs[s].n + chunk - 1) / chunk;
   }
   t.first_block[nseg] = blocks;
   for (int s = nseg + 1; s <= HET_MAX_SEGS; ++s) t.first_block[s] = blocks;
@@ -410,10 +418,22 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
   if (blocks > 0x7fffffff) return fail(HET_EARG, "het_accumulate: too large");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const dim3 grid(static_cast<unsigned>(blocks));
-  if (mode == HET_ACC_FIRST)
-    accumulate_kernel<HET_ACC_FIRST><<<grid, kThreads, 0, st>>>(acc, t, scale);
-  else
-    accumulate_kernel<HET_ACC_ADD><<<grid, kThreads, 0, st>>>(acc, t, scale);
+#define HET_ACC_LAUNCH(T, I)                                                              \
+  do {                                                                                    \
+    if (mode == HET_ACC_FIRST)                                                            \
+      accumulate_kernel<HET_ACC_FIRST, T, I><<<grid, T, 0, st>>>(acc, t, scale);          \
+    else                                                                                  \
+      accumulate_kernel<HET_ACC_ADD, T, I><<<grid, T, 0, st>>>(acc, t, scale);            \
+  } while (0)
+  switch (g_acc_variant) {
+    case 1: HET_ACC_LAUNCH(256, 2); break;
+    case 2: HET_ACC_LAUNCH(256, 1); break;
+    case 3: HET_ACC_LAUNCH(512, 2); break;
+    case 4: HET_ACC_LAUNCH(512, 1); break;
+    case 5: HET_ACC_LAUNCH(128, 4); break;
+    default: HET_ACC_LAUNCH(256, 4);
+  }
+#undef HET_ACC_LAUNCH
   return het::check_launch("het_accumulate");
 }
 
@@ -481,6 +501,16 @@ int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void*
       acc, wte_off, wpe_off, static_cast<const __nv_bfloat16*>(dy_bf16), rows, d, order,
       seg_start, seg_token, nseg, seq, scale);
   return het::check_launch("het_embedding_grad");
+}
+
+int het_tune(int key, int value) {
+  if (key == HET_TUNE_ACC_VARIANT) {
+    if (value < 0 || value >= static_cast<int>(sizeof(kAccShapes) / sizeof(kAccShapes[0])))
+      return fail(HET_EARG, "het_tune: accumulate variant %d out of range", value);
+    g_acc_variant = value;
+    return HET_OK;
+  }
+  return fail(HET_EARG, "het_tune: unknown key %d", key);
 }
 
 int het_fill_f32(float* dst, float value, int64_t n, void* stream) {

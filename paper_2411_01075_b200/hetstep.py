@@ -27,7 +27,7 @@ HET_SYMM_TIMEOUT = 17
 SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
-           "het_fill_f32", "het_embedding_grad", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_fill_f32", "het_tune", "het_embedding_grad", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
@@ -62,6 +62,7 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_accumulate": ([vp, ctypes.POINTER(HetSeg), i32, i32, f32, vp], i32),
         "het_adamw": ([vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, i64, vp], i32),
         "het_fill_f32": ([vp, f32, i64, vp], i32),
+        "het_tune": ([i32, i32], i32),
         "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
@@ -181,6 +182,13 @@ def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: tor
         _cuda(dyc, torch.bfloat16, "dy"), rows, d, order32.data_ptr(), seg.data_ptr(),
         uniq32.data_ptr(), uniq.numel(), int(seq), float(scale), _stream(stream)),
         "het_embedding_grad")
+
+
+HET_TUNE_ACC_VARIANT = 1
+
+
+def tune(key: int, value: int) -> None:
+    _check(load().het_tune(int(key), int(value)), "het_tune")
 
 
 def fill(dst: torch.Tensor, value: float, stream=None) -> None:
