@@ -89,6 +89,17 @@ int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void*
                        const int32_t* seg_token, int64_t nseg, int64_t seq, float scale,
                        void* stream);
 
+/* Fused LayerNorm of the transformer units (bf16 activations, fp32 stats),
+ * d in {256, 768, 1024}. Forward writes y, per-row mean and rstd; backward
+ * writes dx and dgamma/dbeta (bf16) using `partial`, a caller-owned fp32
+ * scratch of het_layernorm_partial_floats(d) floats. Deterministic. */
+int64_t het_layernorm_partial_floats(int64_t d);
+int het_layernorm_fwd(const void* x, const void* w, const void* b, void* y, float* mean,
+                      float* rstd, int64_t rows, int64_t d, float eps, void* stream);
+int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float* mean,
+                      const float* rstd, void* dx, void* dgamma, void* dbeta, float* partial,
+                      int64_t rows, int64_t d, void* stream);
+
 /* Launch-shape tuning knobs (process-wide; defaults are the measured best).
  * HET_TUNE_ACC_VARIANT: het_accumulate CTA shape index 0..5
   * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));

@@ -1,0 +1,232 @@
+// Fused LayerNorm forward/backward for the transformer units (bf16 in/out,
+// fp32 statistics). Not on the owned hot path proper, but the model's single
+// largest non-GEMM cost: torch's LayerNorm backward runs a separate
+// gamma/beta kernel at ~4x HBM time on [m*seq, d] bf16 activations.
+//
+// One warp owns a row (d = 32 * 8 * CHUNKS elements, 16-byte vectors). The
+// backward is persistent: each warp walks rows with a grid stride and keeps
+// its columns' dgamma/dbeta partial sums in registers; CTAs reduce their warps
+// through shared memory and write one fp32 partial row each; a second pass
+// sums the partial rows (fixed order: deterministic).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hetstep.h"
+#include "hetstep_internal.cuh"
+
+using het::fail;
+
+namespace {
+
+constexpr int kWarps = 8;
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float((w[i] & 0xffffu) << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int CHUNKS>
+__global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
+    float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows, float eps) {
+  constexpr int D = CHUNKS * 256;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const __nv_bfloat16* xr = x + row * D;
+  float v[CHUNKS][8];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    load8(xr + c * 256 + lane * 8, v[c]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[c][i];
+  }
+  const float mean = warp_sum(s) * (1.f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float t = v[c][i] - mean;
+      q += t * t;
+    }
+  const float rstd = rsqrtf(warp_sum(q) * (1.f / D) + eps);
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    float g[8], bb[8], o[8];
+    load8(w + c * 256 + lane * 8, g);
+    load8(b + c * 256 + lane * 8, bb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = (v[c][i] - mean) * rstd * g[i] + bb[i];
+    store8(y + row * D + c * 256 + lane * 8, o);
+  }
+  if (lane == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+template <int CHUNKS>
+__global__ void __launch_bounds__(kWarps * 32, 2) ln_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean,
+    const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
+    float* __restrict__ partial /* [gridDim.x][2][D] */, int64_t rows) {
+  constexpr int D = CHUNKS * 256;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float dg[CHUNKS][8], db[CHUNKS][8];
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dg[c][i] = db[c][i] = 0.f;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + warp; row < rows;
+       row += nwarps) {
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) {       // pass 1: row sums + dgamma/dbeta partials
+      float xv[8], dv[8], gv[8];
+      load8(x + row * D + c * 256 + lane * 8, xv);
+      load8(dy + row * D + c * 256 + lane * 8, dv);
+      load8(w + c * 256 + lane * 8, gv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (xv[i] - mu) * rs, gy = dv[i] * gv[i];
+        dg[c][i] += dv[i] * xh;
+        db[c][i] += dv[i];
+        s1 += gy;
+        s2 += gy * xh;
+      }
+    }
+    s1 = warp_sum(s1) * (1.f / D);
+    s2 = warp_sum(s2) * (1.f / D);
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) {       // pass 2 (row re-read from L1): dx
+      float xv[8], dv[8], gv[8], o[8];
+      load8(x + row * D + c * 256 + lane * 8, xv);
+      load8(dy + row * D + c * 256 + lane * 8, dv);
+      load8(w + c * 256 + lane * 8, gv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = rs * (dv[i] * gv[i] - s1 - (xv[i] - mu) * rs * s2);
+      store8(dx + row * D + c * 256 + lane * 8, o);
+    }
+  }
+  // CTA reduction of the warps' dgamma/dbeta partials (fixed order)
+  __shared__ float red[kWarps][2][256];
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      red[warp][0][lane * 8 + i] = dg[c][i];
+      red[warp][1][lane * 8 + i] = db[c][i];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 2 * 256; k += blockDim.x) {
+      const int which = k / 256, col = k % 256;
+      float acc = 0.f;
+#pragma unroll
+      for (int wv = 0; wv < kWarps; ++wv) acc += red[wv][which][col];
+      partial[(static_cast<int64_t>(blockIdx.x) * 2 + which) * D + c * 256 + col] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// sum the per-CTA partial rows (fixed order) -> dgamma, dbeta (bf16)
+__global__ void ln_bwd_finalize_kernel(const float* __restrict__ partial, int nblk, int64_t d,
+                                       __nv_bfloat16* __restrict__ dgamma,
+                                       __nv_bfloat16* __restrict__ dbeta) {
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (col >= 2 * d) return;
+  const int which = static_cast<int>(col / d);
+  const int64_t c = col % d;
+  float acc = 0.f;
+  for (int b = 0; b < nblk; ++b) acc += partial[(static_cast<int64_t>(b) * 2 + which) * d + c];
+  (which == 0 ? dgamma : dbeta)[c] = __float2bfloat16_rn(acc);
+}
+
+int grid_bwd() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms * 2;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int64_t het_layernorm_partial_floats(int64_t d) { return static_cast<int64_t>(grid_bwd()) * 2 * d; }
+
+int het_layernorm_fwd(const void* x, const void* w, const void* b, void* y, float* mean,
+                      float* rstd, int64_t rows, int64_t d, float eps, void* stream) {
+  if (!x || !w || !b || !y || !mean || !rstd || rows < 0 || (d != 256 && d != 768 && d != 1024) ||
+      !aligned16(x) || !aligned16(y) || !aligned16(w) || !aligned16(b))
+    return fail(HET_EARG, "het_layernorm_fwd: unsupported shape/alignment (d=%lld)", (long long)d);
+  if (rows == 0) return HET_OK;
+  const unsigned grid = static_cast<unsigned>((rows + kWarps - 1) / kWarps);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto W = static_cast<const __nv_bfloat16*>(w);
+  auto B = static_cast<const __nv_bfloat16*>(b);
+  auto Y = static_cast<__nv_bfloat16*>(y);
+  if (d == 256) ln_fwd_kernel<1><<<grid, kWarps * 32, 0, st>>>(X, W, B, Y, mean, rstd, rows, eps);
+  else if (d == 768) ln_fwd_kernel<3><<<grid, kWarps * 32, 0, st>>>(X, W, B, Y, mean, rstd, rows, eps);
+  else ln_fwd_kernel<4><<<grid, kWarps * 32, 0, st>>>(X, W, B, Y, mean, rstd, rows, eps);
+  return het::check_launch("het_layernorm_fwd");
+}
+
+int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float* mean,
+                      const float* rstd, void* dx, void* dgamma, void* dbeta, float* partial,
+                      int64_t rows, int64_t d, void* stream) {
+  if (!dy || !x || !w || !mean || !rstd || !dx || !dgamma || !dbeta || !partial || rows < 0 ||
+      (d != 256 && d != 768 && d != 1024) || !aligned16(dy) || !aligned16(x) || !aligned16(dx) ||
+      !aligned16(w))
+    return fail(HET_EARG, "het_layernorm_bwd: unsupported shape/alignment (d=%lld)", (long long)d);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nblk = grid_bwd();
+  auto DY = static_cast<const __nv_bfloat16*>(dy);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto W = static_cast<const __nv_bfloat16*>(w);
+  auto DX = static_cast<__nv_bfloat16*>(dx);
+  if (d == 256) ln_bwd_kernel<1><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
+  else if (d == 768) ln_bwd_kernel<3><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
+  else ln_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
+  int rc = het::check_launch("het_layernorm_bwd");
+  if (rc != HET_OK) return rc;
+  ln_bwd_finalize_kernel<<<static_cast<unsigned>((2 * d + 255) / 256), 256, 0, st>>>(
+      partial, nblk, d, static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
+  return het::check_launch("het_layernorm_bwd(finalize)");
+}
+
+}  // extern "C"

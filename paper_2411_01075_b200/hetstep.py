@@ -27,7 +27,8 @@ HET_SYMM_TIMEOUT = 17
 SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
-           "het_fill_f32", "het_tune", "het_embedding_grad", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
+           "het_layernorm_fwd", "het_layernorm_bwd", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
@@ -63,6 +64,9 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_adamw": ([vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, i64, vp], i32),
         "het_fill_f32": ([vp, f32, i64, vp], i32),
         "het_tune": ([i32, i32], i32),
+        "het_layernorm_partial_floats": ([i64], i64),
+        "het_layernorm_fwd": ([vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
+        "het_layernorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
         "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
@@ -185,6 +189,49 @@ def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: tor
 
 
 HET_TUNE_ACC_VARIANT = 1
+LN_DIMS = (256, 768, 1024)
+
+
+class LayerNormFn(torch.autograd.Function):
+    """Fused LayerNorm (het_layernorm_fwd/bwd) as an autograd op; bf16 CUDA
+    tensors with d in LN_DIMS."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, eps):
+        d = x.shape[-1]
+        xc = x.contiguous()
+        rows = xc.numel() // d
+        y = torch.empty_like(xc)
+        mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        _check(load().het_layernorm_fwd(_cuda(xc, torch.bfloat16, "x"), _cuda(w, torch.bfloat16, "w"),
+                                        _cuda(b, torch.bfloat16, "b"), y.data_ptr(),
+                                        mean.data_ptr(), rstd.data_ptr(), rows, d, float(eps),
+                                        _stream(None)), "het_layernorm_fwd")
+        ctx.save_for_backward(xc, w, mean, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        xc, w, mean, rstd = ctx.saved_tensors
+        d = xc.shape[-1]
+        rows = xc.numel() // d
+        dyc = dy.contiguous()
+        dx = torch.empty_like(xc)
+        dw = torch.empty_like(w)
+        db = torch.empty_like(w)
+        part = torch.empty(int(load().het_layernorm_partial_floats(d)), dtype=torch.float32,
+                           device=xc.device)
+        _check(load().het_layernorm_bwd(_cuda(dyc, torch.bfloat16, "dy"), xc.data_ptr(),
+                                        w.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                                        dx.data_ptr(), dw.data_ptr(), db.data_ptr(),
+                                        part.data_ptr(), rows, d, _stream(None)),
+               "het_layernorm_bwd")
+        return dx, dw, db, None
+
+
+def layer_norm(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, eps: float = 1e-5):
+    return LayerNormFn.apply(x, w, b, eps)
 
 
 def tune(key: int, value: int) -> None:

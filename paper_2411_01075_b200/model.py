@@ -21,6 +21,7 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
+from . import hetstep as _K
 from .core import InputError, ModelSpec
 
 
@@ -173,9 +174,11 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
 
 
 def _ln(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """LayerNorm as normalize + separate affine: the affine's weight/bias
-    gradients become two row reductions instead of torch's GammaBeta backward
-    kernel (~4x slower on [m*seq, d] bf16 activations)."""
+    """LayerNorm. On CUDA the fused sm_100a kernel (hetstep.LayerNormFn: one
+    pass forward, one pass backward incl. deterministic gamma/beta partials);
+    elsewhere normalize + affine with torch ops (used by CPU tests only)."""
+    if x.is_cuda and x.dtype == torch.bfloat16 and x.shape[-1] in _K.LN_DIMS:
+        return _K.layer_norm(x, w, b)
     return torch.addcmul(b, F.layer_norm(x, (x.shape[-1],)), w)
 
 

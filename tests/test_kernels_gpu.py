@@ -147,3 +147,25 @@ def test_embedding_grad_matches_oracle(cuda, vocab, d, m, seq, wpe):
     K.embedding_grad(acc2, wte_off, wpe_off, dy.to(cuda), tok.to(cuda), seq, 0.25)
     torch.cuda.synchronize()
     assert torch.equal(acc, acc2)
+
+
+@pytest.mark.parametrize("d,rows", [(256, 1000), (768, 4 * 512 + 3), (1024, 2048)])
+def test_fused_layernorm_matches_torch_fp32(cuda, d, rows):
+    """Model-side fused LayerNorm: forward and backward against torch's fp32
+    LayerNorm on the same bf16 inputs (outputs are bf16: 1e-2 normwise)."""
+    from oracle.tolerances import norm_rel
+    g = torch.Generator().manual_seed(d)
+    x = (torch.randn(rows, d, generator=g) * 2 + 0.5).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(d, generator=g)).to(torch.bfloat16)
+    b = (0.1 * torch.randn(d, generator=g)).to(torch.bfloat16)
+    dy = torch.randn(rows, d, generator=g).to(torch.bfloat16)
+    xs, ws, bs = (t.to(cuda).requires_grad_(True) for t in (x, w, b))
+    y = K.layer_norm(xs, ws, bs)
+    y.backward(dy.to(cuda))
+    xr, wr, br = (t.float().requires_grad_(True) for t in (x, w, b))
+    yr = torch.nn.functional.layer_norm(xr, (d,), wr, br, 1e-5)
+    yr.backward(dy.float())
+    assert norm_rel(y.float().detach().cpu().numpy(), yr.detach().numpy()) <= 1e-2
+    assert norm_rel(xs.grad.float().cpu().numpy(), xr.grad.numpy()) <= 1e-2
+    assert norm_rel(ws.grad.float().cpu().numpy(), wr.grad.numpy()) <= 1e-2
+    assert norm_rel(bs.grad.float().cpu().numpy(), br.grad.numpy()) <= 1e-2
