@@ -149,10 +149,22 @@ class UnevenFSDPTrainer:
                        (i + 1 == len(order) or self.rs_route[order[i + 1]] != "symm")
                        for i, u in enumerate(order)}
         self.need_shadow = not sym or "nccl" in self.ag_route
+        # l_i == 1: the backward accumulates units in PAIRS (one launch over both units'
+        # gradients, then both reduce-scatters): half the launches, twice the bytes each
+        # (decided from the whole plan so every rank issues its collectives in the same order)
+        self.pair_units = self.L.blocks >= 2 and all(a.num_microbatches <= 1
+                                                     for a in plan.assignments)
+        if self.pair_units:
+            for u in range(self.L.blocks):
+                second = (self.L.blocks - 1 - u) % 2 == 1 or u == 0
+                if self.rs_route[u] == "symm" and second:
+                    self.rs_end[u] = True   # nothing later proves peers finished reading it
         if self.N > 1 and self.symm is None:
             self.ubuf = [torch.empty(U, dtype=torch.bfloat16, device=dev) for _ in range(2)]
             self.rbuf = torch.empty(E, dtype=torch.bfloat16, device=dev)
-            self.acc = [torch.zeros(U, dtype=torch.float32, device=dev) for _ in range(2)]
+            pad_u = (U + 63) // 64 * 64
+            self._acc_pair = torch.zeros(2 * pad_u, dtype=torch.float32, device=dev)
+            self.acc = [self._acc_pair[:U], self._acc_pair[pad_u:pad_u + U]]
             self.racc = torch.zeros(E, dtype=torch.float32, device=dev)
         self.ag_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
         self.rs_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
@@ -303,6 +315,34 @@ class UnevenFSDPTrainer:
             return self._local(self.g32, u)
         return self.racc if u == self.L.root else self.acc[u % 2]
 
+    def _acc_base(self, u: int) -> tuple[torch.Tensor, int]:
+        """(tensor, element offset) addressing unit u's accumulator, with one base
+        shared by both unit accumulators so a paired launch can cover two units."""
+        if self.N == 1:
+            return self.g32, self.L.local_off[u]
+        a0, a = self.acc[0], self.acc[u % 2]
+        off = (a.data_ptr() - a0.data_ptr()) // 4
+        span = (self.acc[1].data_ptr() - a0.data_ptr()) // 4 + self.acc[1].numel()
+        return a0.as_strided((span,), (1,), a0.storage_offset()), off
+
+    def _accumulate_units(self, items, names, seg):
+        """One het_accumulate (FIRST) over [(u, grads), ...] of several units."""
+        base = None
+        pairs = []
+        n = 0
+        for u, grads in items:
+            t, off = self._acc_base(u)
+            base = t if base is None else base
+            pairs += [(g, off + seg[nm]) for g, nm in zip(grads, names)]
+            n += sum(g.numel() for g in grads)
+        a, b = self.timers.pair("accumulate", n * 6.0)
+        if a is not None:
+            a.record()
+        K.accumulate(base, pairs, True, self.w)
+        if b is not None:
+            b.record()
+        self.launches += 1
+
     def _accumulate(self, acc, grads, names, seg, first):
         n = sum(g.numel() for g in grads)
         a, b = self.timers.pair("accumulate", n * (6.0 if first else 10.0))
@@ -391,6 +431,7 @@ class UnevenFSDPTrainer:
 
         # ---- backward --------------------------------------------------------
         rs_ev: dict[int, torch.cuda.Event] = {}
+        pending: list[tuple[int, list[torch.Tensor]]] = []     # paired-accumulate queue
         for u in reversed(range(nb)):
             if multi:
                 # prefetch u-1 unless it is still resident from the forward
@@ -399,12 +440,13 @@ class UnevenFSDPTrainer:
                     ag_ev[u - 1] = self._ag(u - 1, self.ubuf[(u - 1) % 2], "bwd")
                 if u < nb - 2:
                     comp.wait_event(ag_ev[u])
-                if u + 2 in rs_ev:                  # acc[u % 2] last read by RS(u+2)
-                    comp.wait_event(rs_ev[u + 2])
-                if self.symm is not None and u + 1 in rs_ev:
-                    # peers read acc[u % 2] remotely during RS(u+2): my RS(u+1) having
-                    # passed its start barrier proves every rank finished RS(u+2)
-                    comp.wait_event(rs_ev[u + 1])
+                if not self.pair_units:
+                    if u + 2 in rs_ev:              # acc[u % 2] last read by RS(u+2)
+                        comp.wait_event(rs_ev[u + 2])
+                    if self.symm is not None and u + 1 in rs_ev:
+                        # peers read acc[u % 2] remotely during RS(u+2): my RS(u+1) having
+                        # passed its start barrier proves every rank finished RS(u+2)
+                        comp.wait_event(rs_ev[u + 1])
             if self.offload and mb:
                 if u - 1 >= 0:                    # one unit of look-ahead
                     pref[u - 1] = self._prefetch(u - 1, len(mb))
@@ -426,11 +468,33 @@ class UnevenFSDPTrainer:
                     grads = torch.autograd.grad(y, plist + [x], dy[k])
                     dy[k] = grads[-1]
                     h[k][u] = None
-                    self._accumulate(acc, grads[:-1], unit_names, self.unit_seg,
-                                     first=(k == 0))
+                    if self.pair_units:
+                        unit_grads = list(grads[:-1])
+                    else:
+                        self._accumulate(acc, grads[:-1], unit_names, self.unit_seg,
+                                         first=(k == 0))
             done_ev[u] = self._event(comp)
-            if multi:                                # an idle rank's acc holds zeros
-                rs_ev[u] = self._rs(u, acc, done_ev[u])
+            if not self.pair_units:
+                if multi:                            # an idle rank's acc holds zeros
+                    rs_ev[u] = self._rs(u, acc, done_ev[u])
+                continue
+            pending.append((u, unit_grads if mb else []))   # idle ranks still reduce-scatter
+            if len(pending) < 2 and u > 0:
+                continue                             # wait for the pair's second unit
+            if multi:
+                # both accumulators are rewritten: their previous readers are the last
+                # pair's reduce-scatters (the second one ends with a cross-rank barrier
+                # when fused; its start barrier covers the first one)
+                for v, _ in pending:
+                    if v + 2 in rs_ev:
+                        comp.wait_event(rs_ev[v + 2])
+            if mb:
+                self._accumulate_units([p for p in pending if p[1]], unit_names, self.unit_seg)
+            ev = self._event(comp)
+            if multi:
+                for v, _ in pending:
+                    rs_ev[v] = self._rs(v, self._acc(v), ev)
+            pending = []
 
         # ---- embedding backward + root RS -----------------------------------
         # fused embedding backward: token / position rows summed in fp32 straight into
