@@ -157,17 +157,31 @@ __global__ void __launch_bounds__(kWarps * 32, 2) ln_bwd_kernel(
   }
 }
 
-// sum the per-CTA partial rows (fixed order) -> dgamma, dbeta (bf16)
-__global__ void ln_bwd_finalize_kernel(const float* __restrict__ partial, int nblk, int64_t d,
-                                       __nv_bfloat16* __restrict__ dgamma,
-                                       __nv_bfloat16* __restrict__ dbeta) {
-  const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (col >= 2 * d) return;
-  const int which = static_cast<int>(col / d);
-  const int64_t c = col % d;
+// sum the per-CTA partial rows (fixed order) -> dgamma, dbeta (bf16): a CTA owns
+// 32 columns (lane = column, coalesced), its 8 warps split the partial rows and
+// combine through shared memory in a fixed order.
+__global__ void __launch_bounds__(256) ln_bwd_finalize_kernel(const float* __restrict__ partial,
+                                                              int nblk, int64_t d,
+                                                              __nv_bfloat16* __restrict__ dgamma,
+                                                              __nv_bfloat16* __restrict__ dbeta) {
+  __shared__ float red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + lane;   // in [0, 2d)
   float acc = 0.f;
-  for (int b = 0; b < nblk; ++b) acc += partial[(static_cast<int64_t>(b) * 2 + which) * d + c];
-  (which == 0 ? dgamma : dbeta)[c] = __float2bfloat16_rn(acc);
+  if (col < 2 * d) {
+    const int which = static_cast<int>(col / d);
+    const int64_t c = col % d;
+    for (int b = warp; b < nblk; b += 8) acc += partial[(static_cast<int64_t>(b) * 2 + which) * d + c];
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && col < 2 * d) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    const int64_t c = col % d;
+    (col / d == 0 ? dgamma : dbeta)[c] = __float2bfloat16_rn(t);
+  }
 }
 
 int grid_bwd() {
@@ -224,7 +238,7 @@ int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float*
   else ln_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
   int rc = het::check_launch("het_layernorm_bwd");
   if (rc != HET_OK) return rc;
-  ln_bwd_finalize_kernel<<<static_cast<unsigned>((2 * d + 255) / 256), 256, 0, st>>>(
+  ln_bwd_finalize_kernel<<<static_cast<unsigned>((2 * d + 31) / 32), 256, 0, st>>>(
       partial, nblk, d, static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
   return het::check_launch("het_layernorm_bwd(finalize)");
 }
