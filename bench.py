@@ -129,7 +129,8 @@ def make_comms(world: int, rank: int):
     return K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
 
 
-def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None) -> dict:
+def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None,
+                       warmup: int = 1) -> dict:
     """The oracle step (torch CPU fp32, N simulated ranks in one process) on a
     bounded sample of the same workload: `sample` global samples per step."""
     from oracle import model_oracle as MO
@@ -149,6 +150,9 @@ def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None)
     # sample: the first `sample` global samples, split over two simulated ranks as m=1 each
     micro = [(1, sample // 2), (1, sample - sample // 2)]
     from paper_2411_01075_b200.data import tokens
+    for w in range(warmup):                 # untimed warm-up steps
+        toks = tokens(np.arange(sample), arch.seq, arch.vocab, SEED, 10_000 + w)
+        st.step([toks[:micro[0][1]], toks[micro[0][1]:]], micro)
     done, t_total, n = 0, 0.0, 0
     while True:
         toks = tokens(np.arange(sample), arch.seq, arch.vocab, SEED, n)
@@ -161,8 +165,9 @@ def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None)
         if (steps is not None and n >= steps) or (steps is None and t_total >= max_seconds):
             break
     return {"value": done / t_total, "unit": "samples/s", "cores": cores, "kind": "port",
-            "sample": f"{n} CPU steps x {sample} samples of {job.config.name} (seq {arch.seq}) "
-                      f"over 2 simulated ranks, torch CPU fp32 oracle (oracle/model_oracle.py)",
+            "sample": f"{n} timed CPU steps (after {warmup} warm-up) x {sample} samples of "
+                      f"{job.config.name} (seq {arch.seq}) over 2 simulated ranks, torch CPU "
+                      f"fp32 oracle (oracle/model_oracle.py)",
             "seconds": t_total}
 
 
@@ -172,7 +177,7 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     job = build_job(args.config, max(args.gpus, world))
-    ref = cpu_reference_rate(job, steps=args.warmup + args.steps)
+    ref = cpu_reference_rate(job, steps=args.steps, warmup=args.warmup)
     line = {"metric": "train samples/s", "value": ref["value"], "unit": "samples/s",
             "impl": "reference", "n_gpus": max(args.gpus, world), "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "dtype": "f32",

@@ -171,7 +171,17 @@ __global__ void __launch_bounds__(256) ln_bwd_finalize_kernel(const float* __res
   if (col < 2 * d) {
     const int which = static_cast<int>(col / d);
     const int64_t c = col % d;
-    for (int b = warp; b < nblk; b += 8) acc += partial[(static_cast<int64_t>(b) * 2 + which) * d + c];
+    // 8 independent partial sums per thread keep 8 loads in flight (order fixed)
+    float part8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int b = warp;
+    for (; b + 56 < nblk; b += 64) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        part8[k] += partial[(static_cast<int64_t>(b + 8 * k) * 2 + which) * d + c];
+    }
+    for (; b < nblk; b += 8) part8[0] += partial[(static_cast<int64_t>(b) * 2 + which) * d + c];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += part8[k];
   }
   red[warp][lane] = acc;
   __syncthreads();
