@@ -100,6 +100,16 @@ int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float*
                       const float* rstd, void* dx, void* dgamma, void* dbeta, float* partial,
                       int64_t rows, int64_t d, void* stream);
 
+/* Fused next-token cross-entropy over bf16 logits [rows, vocab] (vocab % 8 == 0):
+ * forward writes per-row log-sum-exp and loss; backward writes
+ * dlogits = (*grad_loss / rows) * (softmax - onehot(target)), grad_loss being
+ * the device-resident upstream gradient of the mean loss (no host sync);
+ * dlogits may alias logits. */
+int het_xent_fwd(const void* logits, const int64_t* target, int64_t rows, int64_t vocab,
+                 float* lse, float* loss, void* stream);
+int het_xent_bwd(const void* logits, const int64_t* target, int64_t rows, int64_t vocab,
+                 const float* lse, const float* grad_loss, void* dlogits, void* stream);
+
 /* Launch-shape tuning knobs (process-wide; defaults are the measured best).
  * HET_TUNE_ACC_VARIANT: het_accumulate CTA shape index 0..5
   * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));

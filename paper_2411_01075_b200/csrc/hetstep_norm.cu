@@ -254,3 +254,135 @@ int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- cross-entropy
+//
+// Fused next-token cross-entropy over bf16 logits [T, V]: the forward writes
+// each row's log-sum-exp and loss (one read of the logits); the backward
+// writes dlogits = scale * (softmax - onehot) in one read + one write (may
+// alias the logits buffer). Replaces log_softmax + nll_loss and their
+// backward (three passes over the [T, V] matrix plus the log-prob tensor).
+namespace {
+
+constexpr int kXentThreads = 512;
+
+__device__ __forceinline__ float block_reduce(float v, bool is_max, float* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, t) : v + t;
+  }
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < kXentThreads / 32 ? smem[lane] : (is_max ? -INFINITY : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float t = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmaxf(v, t) : v + t;
+    }
+    if (lane == 0) smem[32] = v;
+  }
+  __syncthreads();
+  const float r = smem[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kXentThreads) xent_fwd_kernel(
+    const __nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ target, int64_t V,
+    float* __restrict__ lse_out, float* __restrict__ loss_out) {
+  __shared__ float smem[33];
+  const int64_t row = blockIdx.x;
+  const __nv_bfloat16* x = logits + row * V;
+  const int64_t nv = V / 8;
+  float mx = -INFINITY, sum = 0.f;             // online max / sum of exp per thread
+  for (int64_t i = threadIdx.x; i < nv; i += kXentThreads) {
+    float f[8];
+    load8(x + i * 8, f);
+    float m8 = f[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) m8 = fmaxf(m8, f[k]);
+    if (m8 > mx) {
+      sum *= __expf(mx - m8);
+      mx = m8;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += __expf(f[k] - mx);
+  }
+  for (int64_t j = nv * 8 + threadIdx.x; j < V; j += kXentThreads) {
+    const float v = __bfloat162float(x[j]);
+    if (v > mx) {
+      sum *= __expf(mx - v);
+      mx = v;
+    }
+    sum += __expf(v - mx);
+  }
+  const float gmax = block_reduce(mx, true, smem);
+  const float gsum = block_reduce(sum * __expf(mx - gmax), false, smem);
+  if (threadIdx.x == 0) {
+    const float lse = gmax + __logf(gsum);
+    lse_out[row] = lse;
+    loss_out[row] = lse - __bfloat162float(x[target[row]]);
+  }
+}
+
+__global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(
+    const __nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ target, int64_t V,
+    const float* __restrict__ lse, const float* __restrict__ gout, float inv_rows,
+    __nv_bfloat16* __restrict__ dlogits) {
+  const int64_t row = blockIdx.x;
+  const float scale = *gout * inv_rows;     // upstream gradient of the mean loss
+  const __nv_bfloat16* x = logits + row * V;
+  __nv_bfloat16* g = dlogits + row * V;
+  const float l = lse[row];
+  const int64_t tgt = target[row];
+  const int64_t nv = V / 8;
+  for (int64_t i = threadIdx.x; i < nv; i += kXentThreads) {
+    float f[8];
+    load8(x + i * 8, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float p = __expf(f[k] - l);
+      f[k] = scale * (p - (i * 8 + k == tgt ? 1.f : 0.f));
+    }
+    store8(g + i * 8, f);
+  }
+  for (int64_t j = nv * 8 + threadIdx.x; j < V; j += kXentThreads) {
+    const float p = __expf(__bfloat162float(x[j]) - l);
+    g[j] = __float2bfloat16_rn(scale * (p - (j == tgt ? 1.f : 0.f)));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int het_xent_fwd(const void* logits, const int64_t* target, int64_t rows, int64_t vocab,
+                 float* lse, float* loss, void* stream) {
+  if (!logits || !target || !lse || !loss || rows < 0 || vocab <= 0 ||
+      (reinterpret_cast<uintptr_t>(logits) & 15) || (vocab % 8))
+    return fail(HET_EARG, "het_xent_fwd: bad args (vocab %% 8 and 16-byte alignment required)");
+  if (rows == 0) return HET_OK;
+  xent_fwd_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0,
+                    static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(logits), target, vocab, lse, loss);
+  return het::check_launch("het_xent_fwd");
+}
+
+int het_xent_bwd(const void* logits, const int64_t* target, int64_t rows, int64_t vocab,
+                 const float* lse, const float* grad_loss, void* dlogits, void* stream) {
+  if (!logits || !target || !lse || !grad_loss || !dlogits || rows < 0 || vocab <= 0 ||
+      (reinterpret_cast<uintptr_t>(logits) & 15) || (reinterpret_cast<uintptr_t>(dlogits) & 15) ||
+      (vocab % 8))
+    return fail(HET_EARG, "het_xent_bwd: bad args");
+  if (rows == 0) return HET_OK;
+  xent_bwd_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0,
+                    static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(logits), target, vocab, lse, grad_loss,
+      1.f / static_cast<float>(rows), static_cast<__nv_bfloat16*>(dlogits));
+  return het::check_launch("het_xent_bwd");
+}
+
+}  // extern "C"

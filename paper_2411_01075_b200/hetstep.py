@@ -28,7 +28,7 @@ SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
-           "het_layernorm_fwd", "het_layernorm_bwd", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
@@ -67,6 +67,8 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_layernorm_partial_floats": ([i64], i64),
         "het_layernorm_fwd": ([vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_layernorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
+        "het_xent_fwd": ([vp, vp, i64, i64, vp, vp, vp], i32),
+        "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
         "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
@@ -228,6 +230,38 @@ class LayerNormFn(torch.autograd.Function):
                                         part.data_ptr(), rows, d, _stream(None)),
                "het_layernorm_bwd")
         return dx, dw, db, None
+
+
+class CrossEntropyFn(torch.autograd.Function):
+    """Mean next-token cross-entropy over bf16 logits with the fused kernels
+    (het_xent_fwd/bwd); the backward overwrites the logits buffer in place
+    with dlogits (the logits are dead after it)."""
+
+    @staticmethod
+    def forward(ctx, logits, target):
+        rows, vocab = logits.shape
+        lg = logits.contiguous()
+        tgt = target.reshape(-1).to(torch.int64).contiguous()
+        lse = torch.empty(rows, dtype=torch.float32, device=lg.device)
+        loss = torch.empty(rows, dtype=torch.float32, device=lg.device)
+        _check(load().het_xent_fwd(_cuda(lg, torch.bfloat16, "logits"), tgt.data_ptr(), rows,
+                                   vocab, lse.data_ptr(), loss.data_ptr(), _stream(None)),
+               "het_xent_fwd")
+        ctx.save_for_backward(lg, tgt, lse)
+        return loss.mean()
+
+    @staticmethod
+    def backward(ctx, gout):
+        lg, tgt, lse = ctx.saved_tensors
+        rows, vocab = lg.shape
+        g = gout.reshape(1).to(torch.float32).contiguous()   # stays on the device
+        _check(load().het_xent_bwd(lg.data_ptr(), tgt.data_ptr(), rows, vocab, lse.data_ptr(),
+                                   g.data_ptr(), lg.data_ptr(), _stream(None)), "het_xent_bwd")
+        return lg, None
+
+
+def cross_entropy(logits: torch.Tensor, target: torch.Tensor) -> torch.Tensor:
+    return CrossEntropyFn.apply(logits, target)
 
 
 def layer_norm(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, eps: float = 1e-5):

@@ -197,6 +197,8 @@ def head_loss(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor,
     else:
         h = _ln(x, p["lnf_w"], p["lnf_b"])
     logits = h @ p["wte"].t()
-    # bf16 logits straight into the fused log-softmax/NLL (fp32 accumulation
-    # inside); no fp32 copy of the [tokens, vocab] matrix
-    return F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1).long())
+    flat = logits.view(-1, logits.shape[-1])
+    if flat.is_cuda and flat.dtype == torch.bfloat16 and flat.shape[-1] % 8 == 0:
+        # fused sm_100a cross-entropy: one pass forward, one in-place pass backward
+        return _K.cross_entropy(flat, targets.reshape(-1))
+    return F.cross_entropy(flat, targets.reshape(-1).long())

@@ -169,3 +169,21 @@ def test_fused_layernorm_matches_torch_fp32(cuda, d, rows):
     assert norm_rel(xs.grad.float().cpu().numpy(), xr.grad.numpy()) <= 1e-2
     assert norm_rel(ws.grad.float().cpu().numpy(), wr.grad.numpy()) <= 1e-2
     assert norm_rel(bs.grad.float().cpu().numpy(), br.grad.numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("rows,vocab", [(3000, 50304), (517, 4096), (64, 32000)])
+def test_fused_cross_entropy_matches_torch_fp32(cuda, rows, vocab):
+    """Model-side fused cross-entropy against torch's fp32 cross-entropy on the
+    same bf16 logits: loss 1e-5 relative, dlogits (bf16 output) 1e-2 normwise."""
+    from oracle.tolerances import norm_rel
+    g = torch.Generator().manual_seed(vocab)
+    logits = (torch.randn(rows, vocab, generator=g) * 3).to(torch.bfloat16)
+    tgt = torch.randint(0, vocab, (rows,), generator=g)
+    x = logits.to(cuda).requires_grad_(True)
+    loss = K.cross_entropy(x * 1, tgt.to(cuda))
+    (loss * 0.5).backward()
+    xr = logits.float().requires_grad_(True)
+    lr = torch.nn.functional.cross_entropy(xr, tgt)
+    (lr * 0.5).backward()
+    assert abs(float(loss) - float(lr)) <= 1e-5 * abs(float(lr))
+    assert norm_rel(x.grad.float().cpu().numpy(), xr.grad.numpy()) <= 1e-2
