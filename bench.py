@@ -252,7 +252,7 @@ def main() -> None:
     barrier()
     tr.timers.enabled = True
     tr.timers.reset()
-    launches0 = tr.launches
+    launches0 = K.LAUNCHES
     comp = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -262,7 +262,7 @@ def main() -> None:
             tr.step(resident[s])
         t1.record(comp)
         barrier()
-    launches = tr.launches - launches0
+    launches = K.LAUNCHES - launches0
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
     kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate")}
     tr.timers.enabled = False

@@ -98,8 +98,16 @@ def version() -> str:
     return load().het_version().decode()
 
 
+LAUNCHES = 0      # owned kernel launches issued by this process (incl. model-side kernels)
+_NOT_LAUNCHES = ("het_comm_unique_id", "het_comm_init", "het_comm_destroy", "het_tune",
+                 "het_symm_status")
+
+
 def _check(rc: int, what: str) -> None:
+    global LAUNCHES
     if rc == HET_OK:
+        if what not in _NOT_LAUNCHES:
+            LAUNCHES += 1
         return
     msg = load().het_last_error().decode()
     if rc == HET_EARG:
