@@ -100,7 +100,7 @@ def version() -> str:
 
 LAUNCHES = 0      # owned kernel launches issued by this process (incl. model-side kernels)
 _NOT_LAUNCHES = ("het_comm_unique_id", "het_comm_init", "het_comm_destroy", "het_tune",
-                 "het_symm_status")
+                 "het_symm_status", "het_allgather_uneven", "het_reduce_scatter_uneven")  # NCCL
 
 
 def _check(rc: int, what: str) -> None:
