@@ -7,16 +7,22 @@ Schedule (the reference's executable spec, sim.py:342-368):
        for u in 0..L-1:  prefetch AG(u+1) into the other buffer once unit
                          u-1 has released it                  [ag stream]
                          all l_i microbatches through unit u, keeping only
-                         the unit-boundary activations (checkpoints)
+                         the unit-boundary activations (checkpoints; with
+                         offload_activations they go to pinned host memory)
        head: loss_k and dL/dh_L for every microbatch; root grads accumulate
   BWD  for u in L-1..0:  prefetch AG(u-1) (units L-1 and L-2 are still
                          resident from the forward: no re-gather)
                          for each microbatch: recompute unit u, backward,
-                         het_accumulate(acc_u, grads, w = m_i/B)  (kernel 4)
+                         het_accumulate(acc_u, grads, w = m_i/B)  (kernel 4;
+                         plans with l_i == 1 accumulate units in pairs)
                          then RS(acc_u -> rank's fp32 grad shard)  [rs stream]
-       embedding backward into the root accumulator, RS(root)
-  OPT  one het_adamw over the rank's whole flat shard, writing the bf16
-       shadow that the next step all-gathers                 (kernel 5 + 1)
+       het_embedding_grad straight into the root accumulator, RS(root)
+  OPT  one het_adamw over the rank's whole flat shard (kernel 5), writing the
+       bf16 shadow only when some unit's all-gather goes through NCCL
+
+Collectives are routed per unit (hetstep.route_collective): the fused
+symmetric-memory kernels (pack + all-gather from the fp32 master; switch or
+peer reduction straight into the fp32 shard) or NCCL rings.
 
 Eq. 1 weighting (gradcheck.py:30-46) is the w = m_i/B pre-scale inside
 het_accumulate, so RS is a plain SUM. Idle ranks (m_i = 0, core.py:224-226)
