@@ -110,6 +110,19 @@ int het_xent_fwd(const void* logits, const int64_t* target, int64_t rows, int64_
 int het_xent_bwd(const void* logits, const int64_t* target, int64_t rows, int64_t vocab,
                  const float* lse, const float* grad_loss, void* dlogits, void* stream);
 
+/* Fused RMSNorm (Llama units), d in {256, 768, 1024, 2048}; same conventions
+ * as the LayerNorm pair (partial scratch of het_rmsnorm_partial_floats(d)). */
+int64_t het_rmsnorm_partial_floats(int64_t d);
+int het_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int64_t d,
+                    float eps, void* stream);
+int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, void* dx,
+                    void* dgamma, float* partial, int64_t rows, int64_t d, void* stream);
+/* Rotary position embedding in place on bf16 [rows, heads, dh] (row r at
+ * position r % seq, rotate-half pairs); inverse=1 applies the backward
+ * (inverse) rotation. */
+int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int inverse,
+                     void* stream);
+
 /* Launch-shape tuning knobs (process-wide; defaults are the measured best).
  * HET_TUNE_ACC_VARIANT: het_accumulate CTA shape index 0..5
   * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));

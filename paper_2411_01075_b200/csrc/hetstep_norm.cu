@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(
 }
 
 template <int CHUNKS>
-__global__ void __launch_bounds__(kWarps * 32, 2) ln_bwd_kernel(
+__global__ void __launch_bounds__(kWarps * 32, CHUNKS > 3 ? 1 : 2) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean,
     const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
@@ -383,6 +383,217 @@ int het_xent_bwd(const void* logits, const int64_t* target, int64_t rows, int64_
       static_cast<const __nv_bfloat16*>(logits), target, vocab, lse, grad_loss,
       1.f / static_cast<float>(rows), static_cast<__nv_bfloat16*>(dlogits));
   return het::check_launch("het_xent_bwd");
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- RMSNorm + RoPE
+// Llama units: y = x * rsqrt(mean(x^2) + eps) * w (fp32 math, bf16 io), and
+// rotary position embedding applied in place on [rows = b*s, heads, dh]
+// (rotate-half convention; backward is the inverse rotation).
+namespace {
+
+template <int CHUNKS>
+__global__ void __launch_bounds__(kWarps * 32) rms_fwd_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd_out, int64_t rows, float eps) {
+  constexpr int D = CHUNKS * 256;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float v[CHUNKS][8];
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    load8(x + row * D + c * 256 + lane * 8, v[c]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q += v[c][i] * v[c][i];
+  }
+  const float rs = rsqrtf(warp_sum(q) * (1.f / D) + eps);
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    float g[8], o[8];
+    load8(w + c * 256 + lane * 8, g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = v[c][i] * rs * g[i];
+    store8(y + row * D + c * 256 + lane * 8, o);
+  }
+  if (lane == 0) rstd_out[row] = rs;
+}
+
+template <int CHUNKS>
+__global__ void __launch_bounds__(kWarps * 32, CHUNKS > 4 ? 1 : 2) rms_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ partial /* [gridDim.x][D] */,
+    int64_t rows) {
+  constexpr int D = CHUNKS * 256;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float dg[CHUNKS][8];
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dg[c][i] = 0.f;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * kWarps + warp; row < rows;
+       row += nwarps) {
+    const float rs = rstd[row];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) {
+      float xv[8], dv[8], gv[8];
+      load8(x + row * D + c * 256 + lane * 8, xv);
+      load8(dy + row * D + c * 256 + lane * 8, dv);
+      load8(w + c * 256 + lane * 8, gv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = xv[i] * rs;
+        dg[c][i] += dv[i] * xh;
+        s += dv[i] * gv[i] * xh;
+      }
+    }
+    s = warp_sum(s) * (1.f / D);
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) {
+      float xv[8], dv[8], gv[8], o[8];
+      load8(x + row * D + c * 256 + lane * 8, xv);
+      load8(dy + row * D + c * 256 + lane * 8, dv);
+      load8(w + c * 256 + lane * 8, gv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = rs * (dv[i] * gv[i] - xv[i] * rs * s);
+      store8(dx + row * D + c * 256 + lane * 8, o);
+    }
+  }
+  __shared__ float red[kWarps][256];
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[warp][lane * 8 + i] = dg[c][i];
+    __syncthreads();
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+      float acc = 0.f;
+#pragma unroll
+      for (int wv = 0; wv < kWarps; ++wv) acc += red[wv][k];
+      partial[static_cast<int64_t>(blockIdx.x) * D + c * 256 + k] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) rms_bwd_finalize_kernel(const float* __restrict__ partial,
+                                                               int nblk, int64_t d,
+                                                               __nv_bfloat16* __restrict__ dgamma) {
+  __shared__ float red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  float part8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (col < d) {
+    int b = warp;
+    for (; b + 56 < nblk; b += 64) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) part8[k] += partial[static_cast<int64_t>(b + 8 * k) * d + col];
+    }
+    for (; b < nblk; b += 8) part8[0] += partial[static_cast<int64_t>(b) * d + col];
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc += part8[k];
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && col < d) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    dgamma[col] = __float2bfloat16_rn(t);
+  }
+}
+
+// x: [rows, heads, dh] bf16 contiguous, position of row r = r % seq; rotate
+// pairs (i, i + dh/2) by angle pos * 10000^(-2i/dh) (sign = -1 for backward)
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ x, int64_t rows, int heads, int dh,
+                            int64_t seq, float sign) {
+  const int half = dh / 2;
+  const int64_t total = rows * heads * half;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += stride) {
+    const int i = static_cast<int>(t % half);
+    const int64_t rh = t / half;                      // row * heads + head
+    const int64_t pos = (rh / heads) % seq;
+    const float inv = exp2f(-static_cast<float>(2 * i) / dh * 13.287712379549449f);  // log2(1e4)
+    float sn, cs;
+    __sincosf(static_cast<float>(pos) * inv, &sn, &cs);
+    sn *= sign;
+    __nv_bfloat16* p = x + rh * dh;
+    const float a = __bfloat162float(p[i]), b = __bfloat162float(p[i + half]);
+    p[i] = __float2bfloat16_rn(a * cs - b * sn);
+    p[i + half] = __float2bfloat16_rn(a * sn + b * cs);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t het_rmsnorm_partial_floats(int64_t d) { return static_cast<int64_t>(grid_bwd()) * d; }
+
+int het_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int64_t d,
+                    float eps, void* stream) {
+  if (!x || !w || !y || !rstd || rows < 0 || (d != 2048 && d != 1024 && d != 768 && d != 256) ||
+      !aligned16(x) || !aligned16(y) || !aligned16(w))
+    return fail(HET_EARG, "het_rmsnorm_fwd: unsupported shape/alignment (d=%lld)", (long long)d);
+  if (rows == 0) return HET_OK;
+  const unsigned grid = static_cast<unsigned>((rows + kWarps - 1) / kWarps);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto W = static_cast<const __nv_bfloat16*>(w);
+  auto Y = static_cast<__nv_bfloat16*>(y);
+  switch (d) {
+    case 256: rms_fwd_kernel<1><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps); break;
+    case 768: rms_fwd_kernel<3><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps); break;
+    case 1024: rms_fwd_kernel<4><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps); break;
+    default: rms_fwd_kernel<8><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps);
+  }
+  return het::check_launch("het_rmsnorm_fwd");
+}
+
+int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, void* dx,
+                    void* dgamma, float* partial, int64_t rows, int64_t d, void* stream) {
+  if (!dy || !x || !w || !rstd || !dx || !dgamma || !partial || rows < 0 ||
+      (d != 2048 && d != 1024 && d != 768 && d != 256) || !aligned16(dy) || !aligned16(x) ||
+      !aligned16(dx) || !aligned16(w))
+    return fail(HET_EARG, "het_rmsnorm_bwd: unsupported shape/alignment (d=%lld)", (long long)d);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nblk = grid_bwd();
+  auto DY = static_cast<const __nv_bfloat16*>(dy);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto W = static_cast<const __nv_bfloat16*>(w);
+  auto DX = static_cast<__nv_bfloat16*>(dx);
+  switch (d) {
+    case 256: rms_bwd_kernel<1><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows); break;
+    case 768: rms_bwd_kernel<3><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows); break;
+    case 1024: rms_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows); break;
+    default: rms_bwd_kernel<8><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows);
+  }
+  int rc = het::check_launch("het_rmsnorm_bwd");
+  if (rc != HET_OK) return rc;
+  rms_bwd_finalize_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(
+      partial, nblk, d, static_cast<__nv_bfloat16*>(dgamma));
+  return het::check_launch("het_rmsnorm_bwd(finalize)");
+}
+
+int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int inverse,
+                     void* stream) {
+  if (!x || rows < 0 || heads <= 0 || dh <= 0 || (dh % 2) || seq <= 0)
+    return fail(HET_EARG, "het_rope_inplace: bad args");
+  const int64_t total = rows * heads * (dh / 2);
+  if (total == 0) return HET_OK;
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  rope_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<__nv_bfloat16*>(x), rows, heads, dh, seq, inverse ? -1.f : 1.f);
+  return het::check_launch("het_rope_inplace");
 }
 
 }  // extern "C"

@@ -28,7 +28,8 @@ SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
-           "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
+           "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
@@ -68,6 +69,10 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_layernorm_fwd": ([vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_layernorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
         "het_xent_fwd": ([vp, vp, i64, i64, vp, vp, vp], i32),
+        "het_rmsnorm_partial_floats": ([i64], i64),
+        "het_rmsnorm_fwd": ([vp, vp, vp, vp, i64, i64, f32, vp], i32),
+        "het_rmsnorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
+        "het_rope_inplace": ([vp, i64, i32, i32, i64, i32, vp], i32),
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
         "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
@@ -266,6 +271,70 @@ class CrossEntropyFn(torch.autograd.Function):
         _check(load().het_xent_bwd(lg.data_ptr(), tgt.data_ptr(), rows, vocab, lse.data_ptr(),
                                    g.data_ptr(), lg.data_ptr(), _stream(None)), "het_xent_bwd")
         return lg, None
+
+
+RMS_DIMS = (256, 768, 1024, 2048)
+
+
+class RMSNormFn(torch.autograd.Function):
+    """Fused RMSNorm (het_rmsnorm_fwd/bwd) for bf16 CUDA tensors, d in RMS_DIMS."""
+
+    @staticmethod
+    def forward(ctx, x, w, eps):
+        d = x.shape[-1]
+        xc = x.contiguous()
+        rows = xc.numel() // d
+        y = torch.empty_like(xc)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        _check(load().het_rmsnorm_fwd(_cuda(xc, torch.bfloat16, "x"), _cuda(w, torch.bfloat16, "w"),
+                                      y.data_ptr(), rstd.data_ptr(), rows, d, float(eps),
+                                      _stream(None)), "het_rmsnorm_fwd")
+        ctx.save_for_backward(xc, w, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        xc, w, rstd = ctx.saved_tensors
+        d = xc.shape[-1]
+        rows = xc.numel() // d
+        dyc = dy.contiguous()
+        dx = torch.empty_like(xc)
+        dw = torch.empty_like(w)
+        part = torch.empty(int(load().het_rmsnorm_partial_floats(d)), dtype=torch.float32,
+                           device=xc.device)
+        _check(load().het_rmsnorm_bwd(_cuda(dyc, torch.bfloat16, "dy"), xc.data_ptr(),
+                                      w.data_ptr(), rstd.data_ptr(), dx.data_ptr(), dw.data_ptr(),
+                                      part.data_ptr(), rows, d, _stream(None)), "het_rmsnorm_bwd")
+        return dx, dw, None
+
+
+def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
+    return RMSNormFn.apply(x, w, eps)
+
+
+class RopeFn(torch.autograd.Function):
+    """In-place rotary embedding on a contiguous bf16 [b, s, heads, dh] tensor."""
+
+    @staticmethod
+    def forward(ctx, t, seq):
+        b, s, h, dh = t.shape
+        _check(load().het_rope_inplace(_cuda(t, torch.bfloat16, "x"), b * s, h, dh, int(seq), 0,
+                                       _stream(None)), "het_rope_inplace")
+        ctx.mark_dirty(t)
+        ctx.seq = seq
+        return t
+
+    @staticmethod
+    def backward(ctx, g):
+        g = g.contiguous()
+        b, s, h, dh = g.shape
+        _check(load().het_rope_inplace(g.data_ptr(), b * s, h, dh, int(ctx.seq), 1,
+                                       _stream(None)), "het_rope_inplace")
+        return g, None
+
+
+def rope_(t: torch.Tensor) -> torch.Tensor:
+    return RopeFn.apply(t, t.shape[1])
 
 
 def cross_entropy(logits: torch.Tensor, target: torch.Tensor) -> torch.Tensor:

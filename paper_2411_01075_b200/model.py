@@ -152,6 +152,16 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     b, s, d = x.shape
     H, dh = arch.heads, d // arch.heads
     if arch.kind == "llama":
+        if x.is_cuda and x.dtype == torch.bfloat16 and d in _K.RMS_DIMS:
+            # fused sm_100a RMSNorm and in-place rotary embedding (no cos/sin/cat temporaries)
+            h = _K.rms_norm(x, p["rms1"])
+            q = _K.rope_((h @ p["wq"].t()).view(b, s, H, dh)).transpose(1, 2)
+            k = _K.rope_((h @ p["wk"].t()).view(b, s, H, dh)).transpose(1, 2)
+            v = (h @ p["wv"].t()).view(b, s, H, dh).transpose(1, 2)
+            a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+            x = x + a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
+            h = _K.rms_norm(x, p["rms2"])
+            return x + (F.silu(h @ p["w1"].t()) * (h @ p["w3"].t())) @ p["w2"].t()
         h = _rms(x, p["rms1"])
         q = (h @ p["wq"].t()).view(b, s, H, dh).transpose(1, 2)
         k = (h @ p["wk"].t()).view(b, s, H, dh).transpose(1, 2)
@@ -193,7 +203,8 @@ def head_loss(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor,
               targets: torch.Tensor) -> torch.Tensor:
     """Mean next-token cross-entropy of one microbatch (tied LM head)."""
     if arch.kind == "llama":
-        h = _rms(x, p["normf"])
+        h = (_K.rms_norm(x, p["normf"]) if x.is_cuda and x.dtype == torch.bfloat16 and
+             x.shape[-1] in _K.RMS_DIMS else _rms(x, p["normf"]))
     else:
         h = _ln(x, p["lnf_w"], p["lnf_b"])
     logits = h @ p["wte"].t()

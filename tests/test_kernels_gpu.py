@@ -187,3 +187,40 @@ def test_fused_cross_entropy_matches_torch_fp32(cuda, rows, vocab):
     (lr * 0.5).backward()
     assert abs(float(loss) - float(lr)) <= 1e-5 * abs(float(lr))
     assert norm_rel(x.grad.float().cpu().numpy(), xr.grad.numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("d,rows", [(2048, 1500), (256, 777)])
+def test_fused_rmsnorm_matches_torch_fp32(cuda, d, rows):
+    from oracle.tolerances import norm_rel
+    g = torch.Generator().manual_seed(d)
+    x = (torch.randn(rows, d, generator=g) * 2).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(d, generator=g)).to(torch.bfloat16)
+    dy = torch.randn(rows, d, generator=g).to(torch.bfloat16)
+    xs, ws = (t.to(cuda).requires_grad_(True) for t in (x, w))
+    y = K.rms_norm(xs, ws)
+    y.backward(dy.to(cuda))
+    xr, wr = (t.float().requires_grad_(True) for t in (x, w))
+    yr = xr * torch.rsqrt((xr * xr).mean(-1, keepdim=True) + 1e-6) * wr
+    yr.backward(dy.float())
+    assert norm_rel(y.float().detach().cpu().numpy(), yr.detach().numpy()) <= 1e-2
+    assert norm_rel(xs.grad.float().cpu().numpy(), xr.grad.numpy()) <= 1e-2
+    assert norm_rel(ws.grad.float().cpu().numpy(), wr.grad.numpy()) <= 1e-2
+
+
+def test_fused_rope_matches_oracle_and_inverts(cuda):
+    from oracle import model_oracle as MO
+    from oracle.tolerances import norm_rel
+    b, s, h, dh = 2, 64, 4, 128
+    t = torch.randn(b, s, h, dh, generator=torch.Generator().manual_seed(0)).to(torch.bfloat16)
+    x = t.to(cuda).clone().requires_grad_(False)
+    y = K.rope_(x.clone())
+    ref = MO._rotary(t.float().transpose(1, 2)).transpose(1, 2)     # [b, h, s, dh] convention
+    assert norm_rel(y.float().cpu().numpy(), ref.numpy()) <= 1e-2
+    # backward = inverse rotation: d(rope(x))/dx applied to dy rotates it back
+    xs = t.to(cuda).clone().requires_grad_(True)
+    yy = K.rope_(xs * 1)
+    dy = torch.randn_like(yy)
+    yy.backward(dy)
+    xr = t.float().transpose(1, 2).clone().requires_grad_(True)
+    MO._rotary(xr).backward(dy.float().cpu().transpose(1, 2))
+    assert norm_rel(xs.grad.float().cpu().numpy(), xr.grad.transpose(1, 2).numpy()) <= 1e-2

@@ -141,3 +141,22 @@ def _offload_runs(arch, plan, tok, cuda, res):
         assert lint_measured_trace(ev, arch.layers) == [], off
         res[off] = (float(loss), tr.p32.clone(), peak, {e.kind for e in ev})
         del tr
+
+
+def test_llama_unit_step_matches_cpu_oracle(cuda):
+    """Llama-style units (fused RMSNorm, in-place RoPE, SwiGLU) against the
+    independent fp32 CPU model oracle."""
+    from paper_2411_01075_b200.model import ArchSpec
+    arch = ArchSpec("tiny_llama", "llama", d=256, layers=2, heads=2, ffn=512, vocab=4096, seq=128)
+    plan = one_gpu_plan(arch, 2, 2)
+    units = cpu_units(arch, seed=4)
+    tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda)
+    tr.load_full_units(units)
+    tok = rank_tokens(plan, 0, arch.seq, arch.vocab, seed=9, step=0)
+    loss = tr.step(torch.from_numpy(tok).to(cuda))
+    torch.cuda.synchronize()
+    gu, gr, ref_loss = MO.weighted_gradient(arch, units[:-1], units[-1], [tok], [(2, 2)])
+    assert abs(float(loss) - ref_loss) / abs(ref_loss) <= 2e-2
+    for u, ref in enumerate(gu + [gr]):
+        off, cnt = tr.L.local_range(u)
+        assert _nrel(tr.g32[off:off + cnt].cpu().numpy(), ref.numpy()) <= 2e-2, f"unit {u}"
