@@ -326,7 +326,7 @@ class RopeFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g):
-        g = g.contiguous()
+        g = g.clone(memory_format=torch.contiguous_format)   # never rotate autograd's buffer
         b, s, h, dh = g.shape
         _check(load().het_rope_inplace(g.data_ptr(), b * s, h, dh, int(ctx.seq), 1,
                                        _stream(None)), "het_rope_inplace")
