@@ -189,6 +189,16 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+
+def route_summary(tr) -> dict | str:
+    """Which collective route each unit took and the fused kernels' startup
+    known-answer check (step._check_symm_routes)."""
+    if tr.N == 1:
+        return "none"
+    return {"ag": {r: tr.ag_route.count(r) for r in sorted(set(tr.ag_route))},
+            "rs": {r: tr.rs_route.count(r) for r in sorted(set(tr.rs_route))},
+            "symm_self_check": tr.route_check}
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -325,8 +335,7 @@ def main() -> None:
                        "planner_predicted_iteration_ms": plan.predicted_iteration_ms,
                        "parallelism": f"uneven-fsdp{world}",
                        "emulation_rank0": emu.describe(),
-                       "collectives": ("fused-symm" if tr.symm is not None else
-                                       "nccl" if world > 1 else "none"),
+                       "collectives": route_summary(tr),
                        "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": tok_bytes, "d2h_bytes_per_step": 4 * world},

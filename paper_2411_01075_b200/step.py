@@ -105,7 +105,7 @@ class UnevenFSDPTrainer:
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
                  algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64,
-                 offload_activations: bool = False):
+                 offload_activations: bool = False, check_routes: bool = True):
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
         self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo
@@ -143,28 +143,17 @@ class UnevenFSDPTrainer:
             self.rbuf = self.symm["rbuf"]
             self.acc = [self.symm["acc0"], self.symm["acc1"]]
             self.racc = self.symm["racc"]
-        # per-unit collective routes (fused symmetric kernels vs NCCL ring), fixed by shape
-        units = range(self.L.blocks + 1)
-        sym = self.symm is not None
-        self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
-        self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
-        # a fused RS whose successor (RS order: L-1..0, root) is not fused must end with a
-        # cross-rank barrier: nothing later proves that peers finished reading its acc
-        order = list(range(self.L.blocks - 1, -1, -1)) + [self.L.root]
-        self.rs_end = {u: self.rs_route[u] == "symm" and
-                       (i + 1 == len(order) or self.rs_route[order[i + 1]] != "symm")
-                       for i, u in enumerate(order)}
-        self.need_shadow = not sym or "nccl" in self.ag_route
         # l_i == 1: the backward accumulates units in PAIRS (one launch over both units'
         # gradients, then both reduce-scatters): half the launches, twice the bytes each
         # (decided from the whole plan so every rank issues its collectives in the same order)
         self.pair_units = self.L.blocks >= 2 and all(a.num_microbatches <= 1
                                                      for a in plan.assignments)
-        if self.pair_units:
-            for u in range(self.L.blocks):
-                second = (self.L.blocks - 1 - u) % 2 == 1 or u == 0
-                if self.rs_route[u] == "symm" and second:
-                    self.rs_end[u] = True   # nothing later proves peers finished reading it
+        self._set_routes(self.symm is not None)
+        self.route_check = None
+        if self.symm is not None and check_routes:
+            self.route_check = self._check_symm_routes()
+            if not self.route_check["ok"]:       # every rank agrees: all-NCCL routes
+                self._set_routes(False)
         if self.N > 1 and self.symm is None:
             self.ubuf = [torch.empty(U, dtype=torch.bfloat16, device=dev) for _ in range(2)]
             self.rbuf = torch.empty(E, dtype=torch.bfloat16, device=dev)
@@ -189,6 +178,82 @@ class UnevenFSDPTrainer:
             self.h2d_stream = torch.cuda.Stream(device=dev)
             self._host: dict[tuple[int, int], torch.Tensor] = {}
             self._off_ev: dict[tuple[int, int], torch.cuda.Event] = {}
+
+    # ------------------------------------------------------------------ routes
+    def _set_routes(self, sym: bool) -> None:
+        """Per-unit collective routes (fused symmetric kernels vs NCCL ring), fixed by shape."""
+        units = range(self.L.blocks + 1)
+        self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
+        self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
+        # a fused RS whose successor (RS order: L-1..0, root) is not fused must end with a
+        # cross-rank barrier: nothing later proves that peers finished reading its acc
+        order = list(range(self.L.blocks - 1, -1, -1)) + [self.L.root]
+        self.rs_end = {u: self.rs_route[u] == "symm" and
+                       (i + 1 == len(order) or self.rs_route[order[i + 1]] != "symm")
+                       for i, u in enumerate(order)}
+        self.need_shadow = not sym or "nccl" in self.ag_route
+        if self.pair_units:
+            for u in range(self.L.blocks):
+                second = (self.L.blocks - 1 - u) % 2 == 1 or u == 0
+                if self.rs_route[u] == "symm" and second:
+                    self.rs_end[u] = True   # nothing later proves peers finished reading it
+
+    def _check_symm_routes(self) -> dict:
+        """Known-answer check of every fused collective shape this plan uses,
+        run once at construction on the real symmetric workspace (the fused
+        kernels are specialised per rank count; this proves the specialisation
+        for THIS world size before a step trusts it). Exactly representable
+        integer patterns make the expected bf16 gather and fp32 sum
+        order-independent. Any mismatch or barrier timeout on any rank turns
+        every route to NCCL on every rank."""
+        import torch.distributed as dist
+        dev = self.device
+        shapes = {}
+        for u in range(self.L.blocks + 1):
+            key = (tuple(self.L.counts[u]), tuple(self.L.offsets[u]))
+            shapes.setdefault(key, (u, self.ag_route[u] == "symm", self.rs_route[u] == "symm"))
+        K.SymmWorkspace.status(reset=True)
+        bad = 0
+        checked = 0
+
+        def pattern(idx: torch.Tensor, r: int) -> torch.Tensor:
+            return (((idx * 7 + r * 13) % 251) - 125).to(torch.float32)
+
+        for (counts, offsets), (u, ag, rs) in shapes.items():
+            size = sum(counts)
+            root = u == self.L.root
+            ub, acc = ("rbuf", "racc") if root else ("ub0", "acc0")
+            lo, cnt = offsets[self.rank], counts[self.rank]
+            if ag:
+                src = pattern(torch.arange(lo, lo + cnt, device=dev), 0)
+                self.symm.allgather_pack(src, ub, 0, counts, offsets, stream=self._current())
+                want = pattern(torch.arange(size, device=dev), 0).to(torch.bfloat16)
+                bad += int(not torch.equal(self.symm[ub][:size], want))
+                checked += 1
+            if rs:
+                self.symm[acc][:size].copy_(pattern(torch.arange(size, device=dev), self.rank))
+                out = torch.full((cnt,), float("nan"), device=dev)
+                torch.cuda.synchronize(dev)
+                self.symm.handle.barrier()
+                self.symm.reduce_scatter(acc, 0, out, counts, offsets, end_barrier=True,
+                                         stream=self._current())
+                idx = torch.arange(lo, lo + cnt, device=dev)
+                want = sum(pattern(idx, r) for r in range(self.N))
+                bad += int(not torch.equal(out, want))
+                checked += 1
+        torch.cuda.synchronize(dev)
+        status = K.SymmWorkspace.status(reset=True)
+        on_cpu = dist.get_backend() == "gloo"
+        flag = torch.tensor([bad + (1 if status else 0)], dtype=torch.int32,
+                            device="cpu" if on_cpu else dev)
+        dist.all_reduce(flag)
+        self.symm.handle.barrier()
+        for name in ("ub0", "acc0", "rbuf", "racc"):
+            self.symm[name].zero_()
+        torch.cuda.synchronize(dev)
+        self.symm.handle.barrier()
+        return {"ok": int(flag.item()) == 0, "checked": checked, "failures": int(flag.item()),
+                "status": status}
 
     # ------------------------------------------------------------------ params
     def _local(self, buf: torch.Tensor, u: int) -> torch.Tensor:

@@ -141,6 +141,8 @@ def main(out_dir: str) -> None:
         # the same step through the fused symmetric-memory (NVLS) collectives
         trs = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev,
                                 algo=K.ALGO_SYMM)
+        report["symm_route_check_ok"] = float(trs.route_check["ok"] and
+                                              trs.route_check["checked"] > 0)
         trs.load_full_units(units)
         from paper_2411_01075_b200.trace import StepTracer, lint_measured_trace
         trs.tracer = StepTracer(f"g{rank}")

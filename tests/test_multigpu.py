@@ -47,6 +47,8 @@ def test_multigpu_collectives_and_step(tmp_path):
                 assert v <= FP32_RTOL, f"reduce-scatter {k}: {v}"
             elif k.startswith("symm_status"):
                 assert v == 0.0, f"symmetric barrier timed out ({k})"
+            elif k == "symm_route_check_ok":
+                assert v == 1.0, "fused collectives failed their startup known-answer check"
             elif k == "trace_lint_problems":
                 assert v == 0.0, "measured multi-rank trace violates the schedule's causality"
     arch = ARCHS["tiny_gpt"]

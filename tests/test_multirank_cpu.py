@@ -44,13 +44,13 @@ def _plan(arch, micro, ratios):
     return TrainPlan(rows, 1.0, 1.0, 2.0 * arch.layers, True, assign_unit_shards(ratios, model))
 
 
-def _run(plan, arch, units, steps=1):
+def _run(plan, arch, units, steps=1, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     procs = [ctx.Process(target=mr_worker.run_rank,
-                         args=(r, 2, port, plan_to_dict(plan), arch.name, units, steps, q))
-             for r in range(2)]
+                         args=(r, world, port, plan_to_dict(plan), arch.name, units, steps, q))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
@@ -112,3 +112,25 @@ def test_planner_job_two_ranks_two_steps():
         toks = [rank_tokens(plan, i, arch.seq, arch.vocab, seed=11, step=s) for i in range(2)]
         ref = cpu.step(toks, micro)
         assert abs(res[0]["loss"][s] - ref) <= BF16_GRAD_RTOL * abs(ref)
+
+
+def test_planner_job_eight_ranks():
+    """The 8-rank plan the bench's N=8 run uses (4 state owners, 4 zero-shard
+    ranks, 2:1 micro-batches): the host logic of the widest world size, which
+    the GPU pool here cannot host, against the oracle."""
+    job = build_job("tiny_gpt", 8)
+    arch, plan = job.arch, job.plan
+    assert len(plan.assignments) == 8
+    units = _units(arch)
+    res = _run(plan, arch, units, steps=1, world=8)
+    for r in range(1, 8):
+        for a, b in zip(res[0]["g"] + res[0]["p"], res[r]["g"] + res[r]["p"]):
+            assert np.array_equal(a, b)
+    assert sum(res[r]["owned"] for r in range(8)) == \
+        arch.layers * arch.unit_params + arch.root_params
+    micro = [(a.microbatch, a.num_microbatches) for a in plan.assignments]
+    toks = [rank_tokens(plan, i, arch.seq, arch.vocab, seed=11, step=0) for i in range(8)]
+    gu, gr, loss = MO.weighted_gradient(arch, units[:-1], units[-1], toks, micro)
+    assert abs(res[0]["loss"][0] - loss) <= BF16_GRAD_RTOL * abs(loss)
+    for u, ref in enumerate(gu + [gr]):
+        assert norm_rel(res[0]["g"][u], ref.numpy()) <= BF16_GRAD_RTOL, f"unit {u}"
