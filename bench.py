@@ -52,27 +52,46 @@ def peaks() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    """SM clocks + clock-event (throttle) reasons sampled while the timed
+    region runs: NVML every 20 ms (nvidia-smi every 200 ms if NVML is absent)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits, in the order of the query above
+    BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, index: int):
         self.index, self.rows, self._stop = index, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _nvml(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return None, None
+
     def _run(self):
+        nv, h = self._nvml()
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if nv is not None:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append([str(sm), str(mx)] +
+                                     ["Active" if rs & b else "Not Active" for b in self.BITS])
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if nv is not None else 0.2)
 
     def __enter__(self):
         self._t.start()
