@@ -31,18 +31,9 @@ from paper_2411_01075_b200 import hetstep as K  # noqa: E402
 from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
-         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer",
-         "symm_hybrid": "symm_hybrid", "route": "route"}
+         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route"}
 SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
-        "symm_peer": (False, K.SYMM_PEER), "symm_hybrid": (True, K.SYMM_HYBRID)}
-
-
-def algo_of(name: str):
-    """ALGOS entry, or ("symm_hybrid", k) for "symm_splitK": the hybrid kernel
-    with this rank's multicast share forced to K/32 (sweeps of the link model)."""
-    if name.startswith("symm_split"):
-        return "symm_hybrid", int(name[len("symm_split"):])
-    return ALGOS[name], -1
+        "symm_peer": (False, K.SYMM_PEER)}
 
 
 def skew_counts(skew: str, total: int, n: int) -> list[int]:
@@ -118,8 +109,7 @@ def main() -> None:
     maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
     ws = {}
     for an, (mc, policy) in SYMM.items():
-        if an in args.algos or (an == "symm" and "route" in args.algos) or \
-                (an == "symm_hybrid" and any(a.startswith("symm_split") for a in args.algos)):
+        if an in args.algos or (an == "symm" and "route" in args.algos):
             ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
                                                                          torch.float32)],
                                      dist.group.WORLD.group_name, dev, rank, world,
@@ -139,8 +129,7 @@ def main() -> None:
                         c = skew_counts(skew, total, world)
                     o = offsets(c)
                     for an in args.algos:
-                        algo, split = algo_of(an)
-                        K.tune(K.HET_TUNE_SYMM_SPLIT, split)
+                        algo = ALGOS[an]
                         if op == "reduce_scatter" and algo == K.ALGO_P2P:
                             continue
                         if algo == "route":   # the train step's per-unit choice

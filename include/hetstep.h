@@ -128,10 +128,6 @@ int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int 
   * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));
  * default 4, measured fastest on B200 (tools/acc_bench.cu). */
 #define HET_TUNE_ACC_VARIANT 1
-/* HET_TUNE_SYMM_SPLIT: force this process's multicast share of its own range
- * in the fused collectives to value/32 (0..32) under HET_SYMM_HYBRID; -1
- * (default) = the per-rank link model below. For measurement sweeps. */
-#define HET_TUNE_SYMM_SPLIT 2
 int het_tune(int key, int value);
 
 /* fill / zero helpers used by the step driver (idle ranks, pads) */
@@ -177,22 +173,12 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
 #define HET_SYMM_CHANNELS 2   /* independent barrier channels: 0 = AG stream, 1 = RS stream */
 #define HET_SYMM_TIMEOUT 17   /* het_symm_status(): a cross-rank barrier timed out */
 
-/* Route policy of the fused collectives.
- * MULTICAST / PEER: every rank moves its whole range through the NVLS
- *   multicast address / through peer pointers.
- * AUTO: one of the two per call from the shard vector: multicast moves S
- *   bytes over every GPU's link (the switch loops a rank's own range back),
- *   peer push/pull moves max((N-1) max_j s_j, S - min_i s_i).
- * HYBRID: each rank splits its OWN range: a share a_i through multicast (link
- *   cost a_i s_i out, a_i s_i extra in), the rest through peers ((N-1) s_i out).
- *   a_i = clamp((N s_i - S) / ((N-1) s_i), 0, 1) balances rank i's egress and
- *   ingress, so the slowest link carries max_i (S(N-2) + s_i)/(N-1) or
- *   S - min s, instead of AUTO's max(S - min s, min(S, (N-1) max s)). The
- *   split is interleaved every 32 vectors so both kinds of traffic overlap. */
+/* Route policy of the fused collectives. AUTO picks per call from the shard
+ * vector: NVLS multicast moves S bytes over every GPU's link, peer push/pull
+ * moves max((N-1) max_j s_j, S - min_i s_i); the cheaper one runs. */
 #define HET_SYMM_AUTO 0
 #define HET_SYMM_MULTICAST 1
 #define HET_SYMM_PEER 2
-#define HET_SYMM_HYBRID 3
 
 /* A buffer allocated at the same byte layout on every rank (torch symmetric
  * memory is the plumbing): peer_base[j] = its address on rank j mapped into

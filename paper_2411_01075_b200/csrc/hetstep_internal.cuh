@@ -10,8 +10,6 @@ extern thread_local std::string g_last_error;
 int fail(int code, const char* fmt, ...);
 // HET_ECUDA with the launch error text if the last launch failed.
 int check_launch(const char* what);
-// HET_TUNE_SYMM_SPLIT (hetstep_symm.cu): -1 = link model, 0..32 = forced share
-void set_symm_split(int value);
 // Grid size for a grid-stride loop over `work_items` (x threads per CTA),
 // capped at 8 resident 256-thread CTAs per SM.
 int grid_for(int64_t work_items, int threads);

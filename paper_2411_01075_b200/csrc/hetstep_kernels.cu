@@ -510,11 +510,6 @@ int het_tune(int key, int value) {
     g_acc_variant = value;
     return HET_OK;
   }
-  if (key == HET_TUNE_SYMM_SPLIT) {
-    if (value < -1 || value > 32) return fail(HET_EARG, "het_tune: symm split %d out of range", value);
-    het::set_symm_split(value);
-    return HET_OK;
-  }
   return fail(HET_EARG, "het_tune: unknown key %d", key);
 }
 

@@ -41,12 +41,6 @@ constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
 constexpr uint64_t kSpinTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s wall clock
 
 __device__ int g_symm_status = 0;
-int g_split_override = -1;   // het_tune(HET_TUNE_SYMM_SPLIT, ·)
-
-// warp-uniform interleave of the multicast / peer share of a rank's range
-__device__ __forceinline__ bool via_mc(int64_t v, int mc32) {
-  return static_cast<int>((v >> 5) & 31) < mc32;
-}
 
 struct Args {
   het_symm_t s;
@@ -56,7 +50,6 @@ struct Args {
   uint32_t epoch;
   int channel;
   int end_barrier;
-  int mc32;                // body vector v goes through multicast iff ((v >> 5) & 31) < mc32
 };
 
 __device__ __forceinline__ uint32_t* slot(uint64_t owner_base, uint64_t signal_off, int channel,
@@ -200,7 +193,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
       const int64_t v = v0 + u * gsz;
       if (v < nvec) {
         const uint64_t off = dst0 + static_cast<uint64_t>(h2 + v * 8) * 2;
-        if (MC && via_mc(v, a.mc32)) {
+        if (MC) {
           mc_st_v4(s.mc_base + off, w[u]);
         } else {
 #pragma unroll
@@ -264,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  if (MC && a.mc32 >= 32) {
+  if (MC) {
     for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
       float4 r[kUnroll];
 #pragma unroll
@@ -279,25 +272,18 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
       }
     }
   } else {
-    // peer pull: all (vector, rank) loads of a batch issued before any add; under
-    // HYBRID the multicast share of the vectors is one switch reduction instead
+    // peer pull: all (vector, rank) loads of a batch issued before any add
     constexpr int kB = NR > 0 ? (16 / NR > 1 ? 16 / NR : 2) : 2;
     for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kB) {
       float4 x[kB][NR > 0 ? NR : HET_MAX_RANKS];
-      bool m[kB];
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
         const int64_t v = v0 + u * gsz;
-        m[u] = MC && via_mc(v, a.mc32);
         if (v < nvec) {
           const uint64_t off = src0 + static_cast<uint64_t>(head + v * 4) * 4;
-          if (m[u]) {
-            x[u][0] = mc_ldr_v4(s.mc_base + off);
-          } else {
 #pragma unroll
-            for (int p = 0; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p)
-              if (p < nr) x[u][p] = __ldcg(reinterpret_cast<const float4*>(peer[p] + off));
-          }
+          for (int p = 0; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p)
+            if (p < nr) x[u][p] = __ldcg(reinterpret_cast<const float4*>(peer[p] + off));
         }
       }
 #pragma unroll
@@ -307,7 +293,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
           float4 r = x[u][0];
 #pragma unroll
           for (int p = 1; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p) {
-            if (p < nr && !m[u]) {
+            if (p < nr) {
               r.x += x[u][p].x;
               r.y += x[u][p].y;
               r.z += x[u][p].z;
@@ -336,19 +322,11 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading my acc
 }
 
-// pure multicast kernels do not loop over ranks; peer and hybrid kernels get
-// the rank count as a template constant for 2/4/8 ranks so their loops unroll
-#define HET_DISPATCH_NR(mc, mc32, n, LAUNCH) \
+// multicast kernels do not loop over ranks; peer kernels get the rank count
+// as a template constant for 2/4/8 ranks so their per-rank loops unroll
+#define HET_DISPATCH_NR(mc, n, LAUNCH) \
   do {                                 \
-    if (mc && (mc32) >= 32) {          \
-      LAUNCH(true, 0);                 \
-    } else if (mc && (n) == 2) {       \
-      LAUNCH(true, 2);                 \
-    } else if (mc && (n) == 4) {       \
-      LAUNCH(true, 4);                 \
-    } else if (mc && (n) == 8) {       \
-      LAUNCH(true, 8);                 \
-    } else if (mc) {                   \
+    if (mc) {                          \
       LAUNCH(true, 0);                 \
     } else if ((n) == 2) {             \
       LAUNCH(false, 2);                \
@@ -366,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
 // max((N-1) * max_j s_j, S - min_i s_i). Pick the cheaper one.
 bool pick_multicast(const het_symm_t* s, const int64_t* counts, int policy) {
   if (!s->mc_base || policy == HET_SYMM_PEER) return false;
-  if (policy == HET_SYMM_MULTICAST || policy == HET_SYMM_HYBRID) return true;
+  if (policy == HET_SYMM_MULTICAST) return true;
   int64_t total = 0, mx = 0, mn = INT64_MAX;
   for (int j = 0; j < s->nranks; ++j) {
     total += counts[j];
@@ -375,23 +353,6 @@ bool pick_multicast(const het_symm_t* s, const int64_t* counts, int policy) {
   }
   const int64_t push = (s->nranks - 1) * mx > total - mn ? (s->nranks - 1) * mx : total - mn;
   return total < push;
-}
-
-// Multicast share (in 1/32) of THIS rank's range: 32 for the multicast route,
-// 0 for peer, and under HYBRID the share that equalises the rank's link
-// egress (N-1) s - a s (N-2) with its ingress S - s + a s (header comment).
-int split32(const het_symm_t* s, const int64_t* counts, int policy, bool mc) {
-  if (!mc) return 0;
-  if (policy != HET_SYMM_HYBRID) return 32;
-  if (g_split_override >= 0) return g_split_override;
-  const int n = s->nranks;
-  const double si = static_cast<double>(counts[s->rank]);
-  double total = 0;
-  for (int j = 0; j < n; ++j) total += static_cast<double>(counts[j]);
-  if (si <= 0 || n < 2) return 0;
-  double a = (n * si - total) / ((n - 1) * si);
-  a = a < 0 ? 0 : (a > 1 ? 1 : a);
-  return static_cast<int>(a * 32 + 0.5);
 }
 
 int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offsets, int ctas) {
@@ -411,8 +372,6 @@ int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offset
 }
 
 }  // namespace
-
-void het::set_symm_split(int value) { g_split_override = value; }
 
 extern "C" {
 
@@ -439,12 +398,11 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
   if (counts[s->rank] > 0 && !src) return fail(HET_EARG, "het_symm_allgather_pack: null src");
   if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
-  const bool mc = pick_multicast(s, counts, policy);
-  const int mc32 = split32(s, counts, policy, mc);
-  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1, mc32};
+  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool mc = pick_multicast(s, counts, policy);
 #define HET_AG(MCV, NRV) symm_ag_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(src, a)
-  HET_DISPATCH_NR(mc, mc32, s->nranks, HET_AG);
+  HET_DISPATCH_NR(mc, s->nranks, HET_AG);
 #undef HET_AG
   return het::check_launch("het_symm_allgather_pack");
 }
@@ -457,12 +415,11 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
   if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter: null out");
   if (acc_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter: acc offset not 16B aligned");
-  const bool mc = pick_multicast(s, counts, policy);
-  const int mc32 = split32(s, counts, policy, mc);
-  Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier, mc32};
+  Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool mc = pick_multicast(s, counts, policy);
 #define HET_RS(MCV, NRV) symm_rs_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(out, a)
-  HET_DISPATCH_NR(mc, mc32, s->nranks, HET_RS);
+  HET_DISPATCH_NR(mc, s->nranks, HET_RS);
 #undef HET_RS
   return het::check_launch("het_symm_reduce_scatter");
 }

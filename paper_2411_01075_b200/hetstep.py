@@ -24,7 +24,7 @@ ALGO_SYMM = 4            # fused kernels on a symmetric buffer (NVLS multicast /
 HET_MAX_RANKS = 8
 HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
-SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_HYBRID = 0, 1, 2, 3
+SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
@@ -204,7 +204,6 @@ def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: tor
 
 
 HET_TUNE_ACC_VARIANT = 1
-HET_TUNE_SYMM_SPLIT = 2
 LN_DIMS = (256, 768, 1024)
 
 
