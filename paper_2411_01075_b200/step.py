@@ -176,8 +176,10 @@ class UnevenFSDPTrainer:
         if self.offload:
             self.d2h_stream = torch.cuda.Stream(device=dev)
             self.h2d_stream = torch.cuda.Stream(device=dev)
-            self._host: dict[tuple[int, int], torch.Tensor] = {}
-            self._off_ev: dict[tuple[int, int], torch.cuda.Event] = {}
+            # pinned host copies keyed (microbatch k, consumer unit u): "act" = the input
+            # checkpoint of unit u, "grad" = the upstream gradient of unit u
+            self._host: dict[tuple[str, int, int], torch.Tensor] = {}
+            self._off_ev: dict[tuple[str, int, int], torch.cuda.Event] = {}
 
     # ------------------------------------------------------------------ routes
     def _set_routes(self, sym: bool) -> None:
@@ -294,30 +296,50 @@ class UnevenFSDPTrainer:
         self.load_full_units(units)
 
     # ------------------------------------------------------------------ offload
-    def _offload(self, k: int, u: int, t: torch.Tensor, comp) -> None:
-        host = self._host.get((k, u))
+    def _offload(self, what: str, k: int, u: int, t: torch.Tensor, comp, span_u: int,
+                 phase: str) -> None:
+        """D2H of `t` (key what/k/u) on the D2H stream once `comp` produced it; the
+        GPU copy is released when the copy lands."""
+        key = (what, k, u)
+        host = self._host.get(key)
         if host is None or host.shape != t.shape:
             host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            self._host[(k, u)] = host
+            self._host[key] = host
         self.d2h_stream.wait_stream(comp)
-        with self._span("offload_act", u, k + 1, "fwd", self.d2h_stream):
+        kind = "offload_act" if what == "act" else "offload_grad"
+        with self._span(kind, span_u, k + 1, phase, self.d2h_stream):
             with torch.cuda.stream(self.d2h_stream):
                 host.copy_(t, non_blocking=True)
         t.record_stream(self.d2h_stream)       # GPU copy released once the D2H lands
         ev = torch.cuda.Event()
         ev.record(self.d2h_stream)
-        self._off_ev[(k, u)] = ev
+        self._off_ev[key] = ev
 
-    def _prefetch(self, u: int, nmb: int) -> tuple[list[torch.Tensor], torch.cuda.Event]:
-        out = []
-        for k in range(nmb):
-            self.h2d_stream.wait_event(self._off_ev[(k, u)])
-            with self._span("prefetch_act", u, k + 1, "bwd", self.h2d_stream):
-                with torch.cuda.stream(self.h2d_stream):
-                    out.append(self._host[(k, u)].to(self.device, non_blocking=True))
+    def _fetch(self, what: str, k: int, u: int, phase: str):
+        """H2D of the host copy what/k/u on the H2D stream (after its D2H landed);
+        returns (device tensor, event the consumer waits on)."""
+        key = (what, k, u)
+        self.h2d_stream.wait_event(self._off_ev[key])
+        kind = "prefetch_act" if what == "act" else "prefetch_grad"
+        with self._span(kind, u, k + 1, phase, self.h2d_stream):
+            with torch.cuda.stream(self.h2d_stream):
+                t = self._host[key].to(self.device, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self.h2d_stream)
+        return t, ev
+
+    def _prefetch_unit(self, u: int, nmb: int) -> tuple[list[torch.Tensor], torch.cuda.Event]:
+        """All microbatch inputs of unit u back to the GPU (one unit of look-ahead)."""
+        out = [self._fetch("act", k, u, "bwd")[0] for k in range(nmb)]
         ev = torch.cuda.Event()
         ev.record(self.h2d_stream)
         return out, ev
+
+    def _take(self, fetched, comp) -> torch.Tensor:
+        t, ev = fetched
+        comp.wait_event(ev)
+        t.record_stream(comp)
+        return t
 
     # ------------------------------------------------------------------ comm
     def _event(self, stream):
@@ -440,7 +462,14 @@ class UnevenFSDPTrainer:
         if self.tracer is not None and self.cuda:
             self.tracer.begin(comp)
 
-        # ---- forward -------------------------------------------------------
+        # ---- forward (+ head) ----------------------------------------------
+        # Offload (sim.py:226-338): every unit input checkpoint goes to pinned host memory
+        # once its forward consumed it and comes back for its recompute. With l_i >= 2
+        # ("deep") the reference schedule is followed in full: unit outputs go to host as
+        # soon as they are produced and the next forward microbatch's input is prefetched,
+        # upstream gradients likewise in the backward, so O(1) boundary tensors stay on
+        # the GPU instead of O(l_i). With l_i = 1 the one in-flight tensor is consumed
+        # next, so a round trip would only sit on the critical path.
         ag_ev: dict[int, torch.cuda.Event] = {}
         done_ev: dict[int, torch.cuda.Event] = {}
         if multi:
@@ -456,14 +485,19 @@ class UnevenFSDPTrainer:
         active = self.m > 0
         mb = [(tok[k * self.m:(k + 1) * self.m, :-1], tok[k * self.m:(k + 1) * self.m, 1:])
               for k in range(self.l)] if active else []
+        nmb = len(mb)
+        off = self.offload and nmb > 0
+        deep = off and nmb >= 2
         h: list[list[torch.Tensor | None]] = [[None] * (nb + 1) for _ in mb]
+        dy: list[torch.Tensor | None] = [None] * nmb
+        fetched: dict[tuple[str, int, int], tuple] = {}
         if multi:
             comp.wait_event(ag_ev[root])
         rp = views(self._unit_flat(root), arch.root_layout())
+        leaves = {nm: t.requires_grad_(True) for nm, t in
+                  views(self._unit_flat(root), arch.root_layout()).items()}
+        head_names = [nm for nm in root_names if nm != "wpe"]
         with torch.no_grad():
-            for k, (x_tok, _) in enumerate(mb):
-                with self._span("fwd_compute", root, k + 1, "fwd", comp):
-                    h[k][0] = embed_forward(arch, rp, x_tok)
             for u in range(nb):
                 if multi:
                     if u + 1 < nb:
@@ -472,37 +506,54 @@ class UnevenFSDPTrainer:
                         ag_ev[u + 1] = self._ag(u + 1, self.ubuf[(u + 1) % 2])
                     comp.wait_event(ag_ev[u])
                 p = views(self._unit_flat(u), arch.unit_layout())
-                for k in range(len(mb)):
+                for k in range(nmb):
+                    if u == 0:
+                        with self._span("fwd_compute", root, k + 1, "fwd", comp):
+                            x = embed_forward(arch, rp, mb[k][0])
+                    elif deep:
+                        x = self._take(fetched.pop(("act", k, u)), comp)
+                    else:
+                        x = h[k][u]
+                    if deep:                      # next forward microbatch's input
+                        nk, nu = (k + 1, u) if k + 1 < nmb else (0, u + 1)
+                        if 1 <= nu < nb:
+                            fetched[("act", nk, nu)] = self._fetch("act", nk, nu, "fwd")
                     with self._span("fwd_compute", u, k + 1, "fwd", comp):
-                        h[k][u + 1] = block_forward(arch, p, h[k][u])
+                        y = block_forward(arch, p, x)
+                    if off and (u == 0 or not deep):
+                        self._offload("act", k, u, x, comp, u, "fwd")   # recompute input
+                    h[k][u] = None if off else x
+                    if deep and u + 1 < nb:
+                        self._offload("act", k, u + 1, y, comp, u, "fwd")
+                        y = None
+                    if u + 1 < nb:
+                        h[k][u + 1] = y
+                        continue
+                    # head + loss of microbatch k right behind the last unit's forward
+                    with self._span("head", root, k + 1, "fwd", comp):
+                        y.requires_grad_(True)
+                        with torch.enable_grad():
+                            lk = head_loss(arch, leaves, y, mb[k][1])
+                            grads = torch.autograd.grad(lk, [leaves[nm] for nm in head_names] + [y])
+                        self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
+                        loss += lk.detach() * self.w
+                    if deep:
+                        self._offload("grad", k, nb - 1, grads[-1], comp, nb, "bwd")
+                    else:
+                        dy[k] = grads[-1]
+                    del grads, y
                 done_ev[u] = self._event(comp)
-                if self.offload:                  # unit u's inputs are now only recompute inputs
-                    for k in range(len(mb)):
-                        self._offload(k, u, h[k][u], comp)
-                        h[k][u] = None
         pref: dict[int, tuple[list[torch.Tensor], torch.cuda.Event]] = {}
-        if self.offload and mb:
-            pref[nb - 1] = self._prefetch(nb - 1, len(mb))
-
-        # ---- head + loss ---------------------------------------------------
-        dy: list[torch.Tensor | None] = [None] * len(mb)
-        leaves = {nm: t.requires_grad_(True) for nm, t in
-                  views(self._unit_flat(root), arch.root_layout()).items()}
-        head_names = [nm for nm in root_names if nm != "wpe"]
-        for k, (_, tgt) in enumerate(mb):
-            with self._span("head", root, k + 1, "fwd", comp):
-                x = h[k][nb].requires_grad_(True)
-                with torch.enable_grad():
-                    lk = head_loss(arch, leaves, x, tgt)
-                grads = torch.autograd.grad(lk, [leaves[nm] for nm in head_names] + [x])
-                dy[k] = grads[-1]
-                h[k][nb] = None
-                self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
-                loss += lk.detach() * self.w
+        if deep:                                  # turnaround (sim.py:270-274)
+            fetched[("act", 0, nb - 1)] = self._fetch("act", 0, nb - 1, "bwd")
+            fetched[("grad", 0, nb - 1)] = self._fetch("grad", 0, nb - 1, "bwd")
+        elif off:
+            pref[nb - 1] = self._prefetch_unit(nb - 1, nmb)
 
         # ---- backward --------------------------------------------------------
         rs_ev: dict[int, torch.cuda.Event] = {}
         pending: list[tuple[int, list[torch.Tensor]]] = []     # paired-accumulate queue
+        wpe_off = self.root_seg.get("wpe") if arch.kind != "llama" else None
         for u in reversed(range(nb)):
             if multi:
                 # prefetch u-1 unless it is still resident from the forward
@@ -518,9 +569,9 @@ class UnevenFSDPTrainer:
                         # peers read acc[u % 2] remotely during RS(u+2): my RS(u+1) having
                         # passed its start barrier proves every rank finished RS(u+2)
                         comp.wait_event(rs_ev[u + 1])
-            if self.offload and mb:
+            if off and not deep:
                 if u - 1 >= 0:                    # one unit of look-ahead
-                    pref[u - 1] = self._prefetch(u - 1, len(mb))
+                    pref[u - 1] = self._prefetch_unit(u - 1, nmb)
                 tensors, ev = pref.pop(u)
                 comp.wait_event(ev)
                 for k, t in enumerate(tensors):
@@ -530,20 +581,45 @@ class UnevenFSDPTrainer:
             flat = self._unit_flat(u)
             pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}
             plist = [pl[nm] for nm in unit_names]
-            for k in range(len(mb)):
+            for k in range(nmb):
+                nk, nu = (k + 1, u) if k + 1 < nmb else (0, u - 1)
+                if deep:
+                    x = self._take(fetched.pop(("act", k, u)), comp)
+                    if nu >= 0:                   # next recompute input (at RA start)
+                        fetched[("act", nk, nu)] = self._fetch("act", nk, nu, "bwd")
+                else:
+                    x = h[k][u]
                 with self._span("recompute", u, k + 1, "bwd", comp):
-                    x = h[k][u].requires_grad_(True)
+                    x = x.requires_grad_(True)
                     with torch.enable_grad():
                         y = block_forward(arch, pl, x)
+                if deep:
+                    g_in = self._take(fetched.pop(("grad", k, u)), comp)
+                    if nu >= 0:                   # next upstream gradient (at B start)
+                        fetched[("grad", nk, nu)] = self._fetch("grad", nk, nu, "bwd")
+                else:
+                    g_in = dy[k]
                 with self._span("bwd_compute", u, k + 1, "bwd", comp):
-                    grads = torch.autograd.grad(y, plist + [x], dy[k])
-                    dy[k] = grads[-1]
-                    h[k][u] = None
+                    grads = torch.autograd.grad(y, plist + [x], g_in)
+                    h[k][u] = dy[k] = None
                     if self.pair_units:
                         unit_grads = list(grads[:-1])
                     else:
                         self._accumulate(acc, grads[:-1], unit_names, self.unit_seg,
                                          first=(k == 0))
+                if u == 0:
+                    # fused embedding backward: token / position rows summed in fp32 straight
+                    # into the root accumulator (no dense [vocab, d] bf16 gradient,
+                    # deterministic order)
+                    with self._span("embed_bwd", root, k + 1, "bwd", comp):
+                        K.embedding_grad(racc, self.root_seg["wte"], wpe_off, grads[-1],
+                                         mb[k][0], arch.seq, self.w)
+                        self.launches += 1
+                elif deep:
+                    self._offload("grad", k, u - 1, grads[-1], comp, u, "bwd")
+                else:
+                    dy[k] = grads[-1]
+                del grads, y, x, g_in
             done_ev[u] = self._event(comp)
             if not self.pair_units:
                 if multi:                            # an idle rank's acc holds zeros
@@ -567,16 +643,7 @@ class UnevenFSDPTrainer:
                     rs_ev[v] = self._rs(v, self._acc(v), ev)
             pending = []
 
-        # ---- embedding backward + root RS -----------------------------------
-        # fused embedding backward: token / position rows summed in fp32 straight into
-        # the root accumulator (no dense [vocab, d] bf16 gradient, deterministic order)
-        wpe_off = self.root_seg.get("wpe") if arch.kind != "llama" else None
-        for k, (x_tok, _) in enumerate(mb):
-            with self._span("embed_bwd", root, k + 1, "bwd", comp):
-                K.embedding_grad(racc, self.root_seg["wte"], wpe_off, dy[k], x_tok, arch.seq,
-                                 self.w)
-                self.launches += 1
-                dy[k] = None
+        # ---- root RS -----------------------------------------------------------
         if multi:
             rs_ev[root] = self._rs(root, racc, self._event(comp))
             comp.wait_event(rs_ev[root])            # RS stream is in order: all shards ready

@@ -15,9 +15,13 @@ rules:
     backward all-gather, or the forward one for the two units this step keeps
     resident — DESIGN.md §3);
   * bwd_compute(u, j) starts after recompute(u, j);
-  * with activation offload: the H2D and D2H copy streams are each exclusive,
-    offload_act(u, j) starts after the forward that consumed the checkpoint,
-    and recompute(u, j) starts after prefetch_act(u, j) landed;
+  * with activation offload: the H2D and D2H copy streams are each exclusive;
+    offload_act(u, j) starts after fwd_compute(u, j) (the forward that consumed
+    or produced the checkpoint); fwd_compute(u, j) / recompute(u, j) start
+    after their forward- / backward-phase prefetch_act(u, j) landed;
+    offload_grad(u, j) starts after the bwd_compute(u, j) that produced it
+    (the head's, for unit 0); bwd_compute(u, j) starts after prefetch_grad(u, j)
+    landed (sim.py:226-338);
   * reducescatter(u) starts after the rank's last bwd_compute(u, .).
 Units are 1-indexed like the simulator; the root unit (embeddings/head) is
 unit 0. Cross-rank rules of the simulator (identical collective windows on
@@ -139,31 +143,41 @@ def lint_measured_trace(events: Iterable[TraceEvent], blocks: int) -> list[str]:
                     problems.append(f"{label} overlap on {g}: {a.kind} u{a.unit} / "
                                     f"{b.kind} u{b.unit}")
         ag = {(e.phase, e.unit): e for e in evs if e.kind == "allgather"}
-        idx = {(e.kind, e.unit, e.microbatch): e for e in evs
-               if e.kind in COMPUTE_KINDS + H2D_KINDS + D2H_KINDS}
+        idx = {(e.kind, e.unit, e.microbatch): e for e in evs if e.kind in COMPUTE_KINDS}
+        pf = {(e.kind, e.unit, e.microbatch, e.phase): e for e in evs if e.kind in H2D_KINDS}
+
+        def landed(kind, e, phase, label):
+            c = pf.get((kind, e.unit, e.microbatch, phase))
+            if c and e.start_ms < c.end_ms - EPS:
+                problems.append(f"{label} u{e.unit} j{e.microbatch} on {g} starts before its "
+                                f"{kind}")
         last_bwd: dict[int, float] = {}
         for e in evs:
             if e.kind == "fwd_compute":
                 c = ag.get(("fwd", e.unit))
                 if c and e.start_ms < c.end_ms - EPS:
                     problems.append(f"F u{e.unit} j{e.microbatch} on {g} starts before its allgather")
+                landed("prefetch_act", e, "fwd", "F")
             elif e.kind == "recompute":
                 c = ag.get(("bwd", e.unit)) or ag.get(("fwd", e.unit))
                 if c and e.start_ms < c.end_ms - EPS:
                     problems.append(f"RA u{e.unit} j{e.microbatch} on {g} starts before its allgather")
-                pf = idx.get(("prefetch_act", e.unit, e.microbatch))
-                if pf and e.start_ms < pf.end_ms - EPS:
-                    problems.append(f"RA u{e.unit} j{e.microbatch} on {g} starts before its "
-                                    "input prefetch")
+                landed("prefetch_act", e, "bwd", "RA")
             elif e.kind == "offload_act":
                 f = idx.get(("fwd_compute", e.unit, e.microbatch))
                 if f and e.start_ms < f.end_ms - EPS:
                     problems.append(f"offload_act u{e.unit} j{e.microbatch} on {g} starts "
-                                    "before its consumer finished")
+                                    "before its forward finished")
+            elif e.kind == "offload_grad":
+                b = idx.get(("head" if e.unit == 0 else "bwd_compute", e.unit, e.microbatch))
+                if b and e.start_ms < b.end_ms - EPS:
+                    problems.append(f"offload_grad u{e.unit} j{e.microbatch} on {g} starts "
+                                    "before the backward that produced it")
             elif e.kind == "bwd_compute":
                 ra = idx.get(("recompute", e.unit, e.microbatch))
                 if ra and e.start_ms < ra.end_ms - EPS:
                     problems.append(f"B u{e.unit} j{e.microbatch} on {g} starts before its recompute")
+                landed("prefetch_grad", e, "bwd", "B")
                 last_bwd[e.unit] = max(last_bwd.get(e.unit, 0.0), e.end_ms)
         for e in evs:
             if e.kind == "reducescatter" and e.unit in last_bwd and \

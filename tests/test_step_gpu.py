@@ -117,12 +117,13 @@ def test_activation_offload_matches_and_saves_memory(cuda):
         _offload_runs(arch, plan, tok, cuda, res)
     finally:
         torch.use_deterministic_algorithms(False)
-    assert {"offload_act", "prefetch_act"} <= res[True][3]
+    # l_i = 4: the full reference schedule, activation gradients included
+    assert {"offload_act", "prefetch_act", "offload_grad", "prefetch_grad"} <= res[True][3]
     assert res[True][0] == res[False][0]
     assert torch.equal(res[True][1], res[False][1])       # offload moves bytes, not math
     # 12 units x 4 microbatches x [4, 512, 768] bf16 checkpoints = 151 MB resident without
-    # offload; with it at most ~2 units' worth stays on the GPU
-    assert res[True][2] < res[False][2] - 80e6, (res[True][2], res[False][2])
+    # offload; with it a few boundary tensors stay on the GPU
+    assert res[True][2] < res[False][2] - 120e6, (res[True][2], res[False][2])
 
 
 def _offload_runs(arch, plan, tok, cuda, res):

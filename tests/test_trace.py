@@ -64,6 +64,32 @@ def test_tampered_traces_are_flagged(tamper):
     assert lint_measured_trace(ev, 3), tamper
 
 
+def _at(ev, kind, unit, mb):
+    return next(e for e in ev if (e.kind, e.unit, e.microbatch) == (kind, unit, mb))
+
+
+@pytest.mark.parametrize("case", ["clean", "late_fwd_prefetch", "late_grad_prefetch",
+                                  "early_grad_offload"])
+def test_offload_rules(case):
+    """The simulator's offload residency rules (sim.py:226-338) on the measured
+    trace: forward-phase input prefetches, activation-gradient offload and
+    prefetch."""
+    ev = _good_trace()
+    f = _at(ev, "fwd_compute", 2, 1)
+    b2 = _at(ev, "bwd_compute", 2, 1)
+    b3 = _at(ev, "bwd_compute", 3, 1)
+    shift = {"late_fwd_prefetch": 0.3, "late_grad_prefetch": 0.3,
+             "early_grad_offload": -0.3}.get(case, 0.0)
+    ev.append(TraceEvent("g0", "prefetch_act", 2, 1, "fwd", f.start_ms - 0.5,
+                         f.start_ms + (shift if case == "late_fwd_prefetch" else 0.0)))
+    ev.append(TraceEvent("g0", "prefetch_grad", 2, 1, "bwd", b2.start_ms - 0.5,
+                         b2.start_ms + (shift if case == "late_grad_prefetch" else 0.0)))
+    t0 = b3.end_ms + (shift if case == "early_grad_offload" else 0.0)
+    ev.append(TraceEvent("g0", "offload_grad", 3, 1, "bwd", t0, t0 + 0.2))
+    problems = lint_measured_trace(ev, 3)
+    assert (problems == []) == (case == "clean"), problems
+
+
 @pytest.mark.gpu
 def test_real_step_trace_is_causal(cuda, tmp_path):
     from paper_2411_01075_b200.step import UnevenFSDPTrainer
