@@ -216,7 +216,7 @@ def route_summary(tr) -> dict | str:
         return "none"
     return {"ag": {r: tr.ag_route.count(r) for r in sorted(set(tr.ag_route))},
             "rs": {r: tr.rs_route.count(r) for r in sorted(set(tr.rs_route))},
-            "symm_self_check": tr.route_check}
+            "symm_self_check": tr.route_check, "symm_error": tr.symm_error}
 
 def main() -> None:
     ap = argparse.ArgumentParser()

@@ -98,6 +98,19 @@ class _NoStream:
         pass
 
 
+def _sum_ranks(value: int, dev: torch.device) -> int:
+    """Sum of an integer over the default process group (CPU tensor under gloo)."""
+    import torch.distributed as dist
+    on_cpu = dist.get_backend() == "gloo"
+    t = torch.tensor([int(value)], dtype=torch.int32, device="cpu" if on_cpu else dev)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def _any_rank(flag: bool, dev: torch.device) -> bool:
+    return _sum_ranks(int(flag), dev) > 0
+
+
 class UnevenFSDPTrainer:
     """Per-rank state (uneven flat shards in HBM) plus the step driver."""
 
@@ -130,15 +143,26 @@ class UnevenFSDPTrainer:
         self.p16 = torch.zeros(n, dtype=torch.bfloat16, device=dev)
         U, E = arch.unit_params, arch.root_params
         self.symm = None
+        self.symm_error = None
         if self.N > 1 and algo == K.ALGO_SYMM:
             # fused NVLS collectives: unit buffers and accumulators live in one
             # symmetric allocation; the AG reads the fp32 master directly
             import torch.distributed as dist
             gname = group_name or dist.group.WORLD.group_name
-            self.symm = K.SymmWorkspace(
-                [("ub0", U, torch.bfloat16), ("ub1", U, torch.bfloat16), ("rbuf", E, torch.bfloat16),
-                 ("acc0", U, torch.float32), ("acc1", U, torch.float32), ("racc", E, torch.float32)],
-                gname, dev, rank, self.N, ctas=symm_ctas)
+            err = None
+            try:
+                self.symm = K.SymmWorkspace(
+                    [("ub0", U, torch.bfloat16), ("ub1", U, torch.bfloat16),
+                     ("rbuf", E, torch.bfloat16), ("acc0", U, torch.float32),
+                     ("acc1", U, torch.float32), ("racc", E, torch.float32)],
+                    gname, dev, rank, self.N, ctas=symm_ctas)
+            except Exception as e:            # e.g. no peer mapping on this fabric
+                err = f"{type(e).__name__}: {e}"
+            # every rank drops the fused route if any rank could not build the workspace
+            if _any_rank(err is not None, dev):
+                self.symm = None
+                self.symm_error = err or "another rank failed to build the symmetric workspace"
+        if self.symm is not None:
             self.ubuf = [self.symm["ub0"], self.symm["ub1"]]
             self.rbuf = self.symm["rbuf"]
             self.acc = [self.symm["acc0"], self.symm["acc1"]]
@@ -245,17 +269,13 @@ class UnevenFSDPTrainer:
                 checked += 1
         torch.cuda.synchronize(dev)
         status = K.SymmWorkspace.status(reset=True)
-        on_cpu = dist.get_backend() == "gloo"
-        flag = torch.tensor([bad + (1 if status else 0)], dtype=torch.int32,
-                            device="cpu" if on_cpu else dev)
-        dist.all_reduce(flag)
+        failures = _sum_ranks(bad + (1 if status else 0), dev)
         self.symm.handle.barrier()
         for name in ("ub0", "acc0", "rbuf", "racc"):
             self.symm[name].zero_()
         torch.cuda.synchronize(dev)
         self.symm.handle.barrier()
-        return {"ok": int(flag.item()) == 0, "checked": checked, "failures": int(flag.item()),
-                "status": status}
+        return {"ok": failures == 0, "checked": checked, "failures": failures, "status": status}
 
     # ------------------------------------------------------------------ params
     def _local(self, buf: torch.Tensor, u: int) -> torch.Tensor:
