@@ -123,6 +123,30 @@ int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* r
 int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int inverse,
                      void* stream);
 
+/* SwiGLU on bf16: out[r, j] = silu(a[r, j]) * b[r, j] for r < rows, j < f,
+ * a and b with row stride ld (separate tensors, or the two halves of one
+ * [rows, 2f] projection), out contiguous [rows, f]. Rounds like torch's
+ * F.silu(a) * b (silu to bf16, then the product). Backward: da, db (row
+ * stride ldg) from dout [rows, f]. */
+int het_swiglu_fwd(const void* a, const void* b, int64_t ld, void* out, int64_t rows, int64_t f,
+                   void* stream);
+int het_swiglu_bwd(const void* dout, const void* a, const void* b, int64_t ld, void* da, void* db,
+                   int64_t ldg, int64_t rows, int64_t f, void* stream);
+
+/* Linear-layer epilogues (GPT/BERT units), bf16 in/out with fp32 sums:
+ * het_bias_grad:     db[c] = sum_r g[r, c] over a row-major [rows, n] gradient
+ *                    (deterministic two-pass column sum; `partial` holds
+ *                    het_colsum_partial_floats(rows, n) floats of scratch);
+ * het_gelu_fwd:      y = tanh-approximate GELU(x) over n elements;
+ * het_gelu_bwd_bias: dpre = GELU'(pre) * dy and db = column sums of dpre
+ *                    in one pass (the bias gradient of the projection that
+ *                    produced `pre`). */
+int64_t het_colsum_partial_floats(int64_t rows, int64_t n);
+int het_bias_grad(const void* g, int64_t rows, int64_t n, void* db, float* partial, void* stream);
+int het_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
+int het_gelu_bwd_bias(const void* dy, const void* pre, void* dpre, int64_t rows, int64_t n,
+                      void* db, float* partial, void* stream);
+
 /* Launch-shape tuning knobs (process-wide; defaults are the measured best).
  * HET_TUNE_ACC_VARIANT: het_accumulate CTA shape index 0..5
   * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));

@@ -531,6 +531,90 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ x, int64_t rows, int hea
   }
 }
 
+// ---------------------------------------------------------------- SwiGLU
+// out = silu(a) * b on bf16 [rows, f] (a, b with row stride ld); the rounding
+// sequence of torch's two-kernel form (silu rounded to bf16, then the product)
+// so the fused pass reproduces F.silu(a) * b. 8 elements per thread per step
+// (16-byte accesses) when f and the strides allow it.
+__device__ __forceinline__ float silu_f(float a) { return a / (1.0f + expf(-a)); }
+__device__ __forceinline__ float rbf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+template <int V>
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ a,
+                                  const __nv_bfloat16* __restrict__ b, int64_t ld,
+                                  __nv_bfloat16* __restrict__ out, int64_t rows, int64_t f) {
+  const int64_t per_row = f / V;
+  const int64_t total = rows * per_row;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += stride) {
+    const int64_t r = t / per_row, c = (t - r * per_row) * V;
+    __nv_bfloat16 av[V], bv[V], ov[V];
+    if (V == 8) {
+      *reinterpret_cast<uint4*>(av) = __ldcs(reinterpret_cast<const uint4*>(a + r * ld + c));
+      *reinterpret_cast<uint4*>(bv) = __ldcs(reinterpret_cast<const uint4*>(b + r * ld + c));
+    } else {
+      av[0] = a[r * ld + c];
+      bv[0] = b[r * ld + c];
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      ov[i] = __float2bfloat16_rn(rbf(silu_f(__bfloat162float(av[i]))) * __bfloat162float(bv[i]));
+    if (V == 8)
+      *reinterpret_cast<uint4*>(out + r * f + c) = *reinterpret_cast<uint4*>(ov);
+    else
+      out[r * f + c] = ov[0];
+  }
+}
+
+// da = (g*b) * s * (1 + a (1 - s)), db = g * silu(a), s = sigmoid(a) (torch's
+// mul / silu backward, g*b rounded to bf16 in between as torch does)
+template <int V>
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ g,
+                                  const __nv_bfloat16* __restrict__ a,
+                                  const __nv_bfloat16* __restrict__ b, int64_t ld,
+                                  __nv_bfloat16* __restrict__ da, __nv_bfloat16* __restrict__ db,
+                                  int64_t ldg, int64_t rows, int64_t f) {
+  const int64_t per_row = f / V;
+  const int64_t total = rows * per_row;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += stride) {
+    const int64_t r = t / per_row, c = (t - r * per_row) * V;
+    __nv_bfloat16 gv[V], av[V], bv[V], dav[V], dbv[V];
+    if (V == 8) {
+      *reinterpret_cast<uint4*>(gv) = __ldcs(reinterpret_cast<const uint4*>(g + r * f + c));
+      *reinterpret_cast<uint4*>(av) = __ldcs(reinterpret_cast<const uint4*>(a + r * ld + c));
+      *reinterpret_cast<uint4*>(bv) = __ldcs(reinterpret_cast<const uint4*>(b + r * ld + c));
+    } else {
+      gv[0] = g[r * f + c];
+      av[0] = a[r * ld + c];
+      bv[0] = b[r * ld + c];
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float x = __bfloat162float(av[i]), gg = __bfloat162float(gv[i]);
+      const float s = 1.0f / (1.0f + expf(-x));
+      const float dsilu = rbf(gg * __bfloat162float(bv[i]));
+      dav[i] = __float2bfloat16_rn(dsilu * s * (1.0f + x * (1.0f - s)));
+      dbv[i] = __float2bfloat16_rn(gg * rbf(silu_f(x)));
+    }
+    if (V == 8) {
+      *reinterpret_cast<uint4*>(da + r * ldg + c) = *reinterpret_cast<uint4*>(dav);
+      *reinterpret_cast<uint4*>(db + r * ldg + c) = *reinterpret_cast<uint4*>(dbv);
+    } else {
+      da[r * ldg + c] = dav[0];
+      db[r * ldg + c] = dbv[0];
+    }
+  }
+}
+
+unsigned elementwise_grid(int64_t items, int threads) {
+  int64_t blocks = (items + threads - 1) / threads;
+  const int64_t cap = 148 * 8;                  // grid-stride: 8 CTAs of 256 per SM
+  return static_cast<unsigned>(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
 }  // namespace
 
 extern "C" {
@@ -594,6 +678,43 @@ int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int 
   rope_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<__nv_bfloat16*>(x), rows, heads, dh, seq, inverse ? -1.f : 1.f);
   return het::check_launch("het_rope_inplace");
+}
+
+int het_swiglu_fwd(const void* a, const void* b, int64_t ld, void* out, int64_t rows, int64_t f,
+                   void* stream) {
+  if (!a || !b || !out || rows < 0 || f <= 0 || ld < f)
+    return fail(HET_EARG, "het_swiglu_fwd: bad args");
+  if (rows == 0) return HET_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto A = static_cast<const __nv_bfloat16*>(a);
+  auto B = static_cast<const __nv_bfloat16*>(b);
+  auto O = static_cast<__nv_bfloat16*>(out);
+  if (f % 8 == 0 && ld % 8 == 0 && aligned16(a) && aligned16(b) && aligned16(out))
+    swiglu_fwd_kernel<8><<<elementwise_grid(rows * f / 8, 256), 256, 0, st>>>(A, B, ld, O, rows, f);
+  else
+    swiglu_fwd_kernel<1><<<elementwise_grid(rows * f, 256), 256, 0, st>>>(A, B, ld, O, rows, f);
+  return het::check_launch("het_swiglu_fwd");
+}
+
+int het_swiglu_bwd(const void* dout, const void* a, const void* b, int64_t ld, void* da, void* db,
+                   int64_t ldg, int64_t rows, int64_t f, void* stream) {
+  if (!dout || !a || !b || !da || !db || rows < 0 || f <= 0 || ld < f || ldg < f)
+    return fail(HET_EARG, "het_swiglu_bwd: bad args");
+  if (rows == 0) return HET_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto G = static_cast<const __nv_bfloat16*>(dout);
+  auto A = static_cast<const __nv_bfloat16*>(a);
+  auto B = static_cast<const __nv_bfloat16*>(b);
+  auto DA = static_cast<__nv_bfloat16*>(da);
+  auto DB = static_cast<__nv_bfloat16*>(db);
+  if (f % 8 == 0 && ld % 8 == 0 && ldg % 8 == 0 && aligned16(dout) && aligned16(a) &&
+      aligned16(b) && aligned16(da) && aligned16(db))
+    swiglu_bwd_kernel<8><<<elementwise_grid(rows * f / 8, 256), 256, 0, st>>>(G, A, B, ld, DA, DB,
+                                                                             ldg, rows, f);
+  else
+    swiglu_bwd_kernel<1><<<elementwise_grid(rows * f, 256), 256, 0, st>>>(G, A, B, ld, DA, DB, ldg,
+                                                                         rows, f);
+  return het::check_launch("het_swiglu_bwd");
 }
 
 }  // extern "C"

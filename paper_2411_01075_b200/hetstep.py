@@ -29,7 +29,9 @@ SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
            "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
-           "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
+           "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace",
+           "het_swiglu_fwd", "het_swiglu_bwd", "het_colsum_partial_floats", "het_bias_grad",
+           "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
 
@@ -74,6 +76,12 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_rmsnorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
         "het_rope_inplace": ([vp, i64, i32, i32, i64, i32, vp], i32),
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
+        "het_swiglu_fwd": ([vp, vp, i64, vp, i64, i64, vp], i32),
+        "het_colsum_partial_floats": ([i64, i64], i64),
+        "het_bias_grad": ([vp, i64, i64, vp, vp, vp], i32),
+        "het_gelu_fwd": ([vp, vp, i64, vp], i32),
+        "het_gelu_bwd_bias": ([vp, vp, vp, i64, i64, vp, vp, vp], i32),
+        "het_swiglu_bwd": ([vp, vp, vp, i64, vp, vp, i64, i64, i64, vp], i32),
         "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
@@ -331,6 +339,121 @@ class RopeFn(torch.autograd.Function):
         _check(load().het_rope_inplace(g.data_ptr(), b * s, h, dh, int(ctx.seq), 1,
                                        _stream(None)), "het_rope_inplace")
         return g, None
+
+
+class SwiGLUFn(torch.autograd.Function):
+    """silu(a) * b for bf16 [..., f] a, b (same shape, last dim contiguous, any
+    common row stride): one fused pass forward, one backward (da, db)."""
+
+    @staticmethod
+    def forward(ctx, a, b):
+        f = a.shape[-1]
+        a2, b2 = a.reshape(-1, f), b.reshape(-1, f)
+        if a2.stride() != b2.stride() or a2.stride(1) != 1:
+            a2, b2 = a2.contiguous(), b2.contiguous()
+        out = torch.empty(a.shape, dtype=torch.bfloat16, device=a.device)
+        for t, name in ((a2, "a"), (b2, "b")):
+            if not t.is_cuda or t.dtype != torch.bfloat16:
+                raise InputError(f"swiglu: {name} must be a bf16 CUDA tensor")
+        _check(load().het_swiglu_fwd(a2.data_ptr(), b2.data_ptr(), a2.stride(0), out.data_ptr(),
+                                     a2.shape[0], f, _stream(None)),
+               "het_swiglu_fwd")
+        ctx.save_for_backward(a2, b2)
+        ctx.shape = a.shape
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        a2, b2 = ctx.saved_tensors
+        rows, f = a2.shape[0], a2.shape[1]
+        g = g.reshape(rows, f).contiguous()
+        da = torch.empty((rows, f), dtype=torch.bfloat16, device=g.device)
+        db = torch.empty_like(da)
+        _check(load().het_swiglu_bwd(g.data_ptr(), a2.data_ptr(), b2.data_ptr(), a2.stride(0),
+                                     da.data_ptr(), db.data_ptr(), f, rows, f, _stream(None)),
+               "het_swiglu_bwd")
+        return da.view(ctx.shape), db.view(ctx.shape)
+
+
+def _colsum_scratch(rows: int, n: int, device) -> torch.Tensor:
+    return torch.empty(int(load().het_colsum_partial_floats(rows, n)), dtype=torch.float32,
+                       device=device)
+
+
+def bias_grad(g2: torch.Tensor) -> torch.Tensor:
+    """Column sums of a contiguous bf16 [rows, n] gradient (fp32 sums, bf16 out)."""
+    rows, n = g2.shape
+    db = torch.empty(n, dtype=torch.bfloat16, device=g2.device)
+    part = _colsum_scratch(rows, n, g2.device)
+    _check(load().het_bias_grad(_cuda(g2, torch.bfloat16, "g"), rows, n, db.data_ptr(),
+                                part.data_ptr(), _stream(None)), "het_bias_grad")
+    return db
+
+
+class LinearFn(torch.autograd.Function):
+    """y = x W^T + b with torch's GEMMs both ways and the bias gradient from the
+    fused deterministic column sum (het_bias_grad) instead of torch's reduction."""
+
+    @staticmethod
+    def forward(ctx, x, w, b):
+        ctx.save_for_backward(x, w)
+        return torch.nn.functional.linear(x, w, b)
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        g2 = g.reshape(-1, g.shape[-1]).contiguous()
+        dx = (g2 @ w).view(x.shape) if ctx.needs_input_grad[0] else None
+        dw = g2.t() @ x.reshape(-1, x.shape[-1])
+        return dx, dw, bias_grad(g2)
+
+
+class LinearGeluFn(torch.autograd.Function):
+    """gelu_tanh(x W^T + b): torch's bias-epilogue GEMM, the fused GELU pass
+    forward, and one pass backward for GELU' and the bias gradient together."""
+
+    @staticmethod
+    def forward(ctx, x, w, b):
+        pre = torch.nn.functional.linear(x, w, b)
+        y = torch.empty_like(pre)
+        _check(load().het_gelu_fwd(pre.data_ptr(), y.data_ptr(), pre.numel(), _stream(None)),
+               "het_gelu_fwd")
+        ctx.save_for_backward(x, w, pre)
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w, pre = ctx.saved_tensors
+        n = pre.shape[-1]
+        rows = pre.numel() // n
+        g2 = g.reshape(rows, n).contiguous()
+        dpre = torch.empty((rows, n), dtype=torch.bfloat16, device=g.device)
+        db = torch.empty(n, dtype=torch.bfloat16, device=g.device)
+        part = _colsum_scratch(rows, n, g.device)
+        _check(load().het_gelu_bwd_bias(g2.data_ptr(), pre.data_ptr(), dpre.data_ptr(), rows, n,
+                                        db.data_ptr(), part.data_ptr(), _stream(None)),
+               "het_gelu_bwd_bias")
+        dx = (dpre @ w).view(x.shape) if ctx.needs_input_grad[0] else None
+        dw = dpre.t() @ x.reshape(-1, x.shape[-1])
+        return dx, dw, db
+
+
+def linear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    if not torch.is_grad_enabled():
+        return torch.nn.functional.linear(x, w, b)
+    return LinearFn.apply(x, w, b)
+
+
+def linear_gelu(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    if not torch.is_grad_enabled():
+        # no-grad forward: cuBLASLt's GELU+bias epilogue, one kernel
+        y = torch._addmm_activation(b, x.reshape(-1, x.shape[-1]), w.t(), use_gelu=True)
+        return y.view(*x.shape[:-1], w.shape[0])
+    return LinearGeluFn.apply(x, w, b)
+
+
+def swiglu(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    return SwiGLUFn.apply(a, b)
 
 
 def rope_(t: torch.Tensor) -> torch.Tensor:

@@ -161,7 +161,7 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
             x = x + a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
             h = _K.rms_norm(x, p["rms2"])
-            return x + (F.silu(h @ p["w1"].t()) * (h @ p["w3"].t())) @ p["w2"].t()
+            return x + _K.swiglu(h @ p["w1"].t(), h @ p["w3"].t()) @ p["w2"].t()
         h = _rms(x, p["rms1"])
         q = (h @ p["wq"].t()).view(b, s, H, dh).transpose(1, 2)
         k = (h @ p["wk"].t()).view(b, s, H, dh).transpose(1, 2)
@@ -170,17 +170,24 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
         x = x + a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
         h = _rms(x, p["rms2"])
         return x + (F.silu(h @ p["w1"].t()) * (h @ p["w3"].t())) @ p["w2"].t()
+    # CUDA: linears with the fused bias-gradient column sum, and the MLP
+    # up-projection + GELU as one epilogue GEMM (no-grad) / fused GELU passes
+    fused = x.is_cuda and x.dtype == torch.bfloat16
+    lin = _K.linear if fused else F.linear
     h = _ln(x, p["ln1_w"], p["ln1_b"])
     # q/k/v as views of the fused projection in (b, s, H, dh) memory order: SDPA
     # (cuDNN) keeps that layout for its output, so neither the head split nor
     # the merge below copies, forward or backward
-    q, k, v = F.linear(h, p["qkv_w"], p["qkv_b"]).split(d, dim=-1)
+    q, k, v = lin(h, p["qkv_w"], p["qkv_b"]).split(d, dim=-1)
     q, k, v = (t.view(b, s, H, dh).transpose(1, 2) for t in (q, k, v))
     a = F.scaled_dot_product_attention(q, k, v, is_causal=arch.kind == "gpt")
-    x = x + F.linear(a.transpose(1, 2).reshape(b, s, d), p["proj_w"], p["proj_b"])
+    x = x + lin(a.transpose(1, 2).reshape(b, s, d), p["proj_w"], p["proj_b"])
     h = _ln(x, p["ln2_w"], p["ln2_b"])
-    h = F.gelu(F.linear(h, p["fc_w"], p["fc_b"]), approximate="tanh")
-    return x + F.linear(h, p["fc2_w"], p["fc2_b"])
+    if fused:
+        h = _K.linear_gelu(h, p["fc_w"], p["fc_b"])
+    else:
+        h = F.gelu(F.linear(h, p["fc_w"], p["fc_b"]), approximate="tanh")
+    return x + lin(h, p["fc2_w"], p["fc2_b"])
 
 
 def _ln(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:

@@ -224,3 +224,81 @@ def test_fused_rope_matches_oracle_and_inverts(cuda):
     xr = t.float().transpose(1, 2).clone().requires_grad_(True)
     MO._rotary(xr).backward(dy.float().cpu().transpose(1, 2))
     assert norm_rel(xs.grad.float().cpu().numpy(), xr.grad.transpose(1, 2).numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("rows,f,fused_proj", [(512, 5504, False), (300, 1376, True), (7, 13, False)])
+def test_fused_swiglu_matches_torch(cuda, rows, f, fused_proj):
+    """silu(a) * b fused (forward + backward) against torch's two-kernel bf16
+    form and an fp32 reference; a/b either separate or the halves of one
+    [rows, 2f] projection (row stride 2f)."""
+    g = torch.Generator().manual_seed(rows + f)
+    if fused_proj:
+        ab = (torch.randn(rows, 2 * f, generator=g) * 2).to(torch.bfloat16).to(cuda)
+        a, b = ab[:, :f], ab[:, f:]
+    else:
+        a = (torch.randn(rows, f, generator=g) * 2).to(torch.bfloat16).to(cuda)
+        b = (torch.randn(rows, f, generator=g) * 2).to(torch.bfloat16).to(cuda)
+    dout = torch.randn(rows, f, generator=g).to(torch.bfloat16).to(cuda)
+    a1, b1 = a.detach().clone().requires_grad_(True), b.detach().clone().requires_grad_(True)
+    y = K.swiglu(a1, b1)
+    y.backward(dout)
+    a2, b2 = a.detach().clone().requires_grad_(True), b.detach().clone().requires_grad_(True)
+    yt = torch.nn.functional.silu(a2) * b2
+    yt.backward(dout)
+    # same rounding sequence as torch's bf16 ops: at most 1 bf16 ulp apart
+    for got, want in ((y, yt), (a1.grad, a2.grad), (b1.grad, b2.grad)):
+        d = (got.float() - want.float()).abs()
+        assert float((d > want.float().abs() * 2 ** -7 + 1e-30).float().mean()) < 1e-3
+    a3, b3 = a.float().requires_grad_(True), b.float().requires_grad_(True)
+    y3 = torch.nn.functional.silu(a3) * b3
+    y3.backward(dout.float())
+    for got, want in ((y, y3), (a1.grad, a3.grad), (b1.grad, b3.grad)):
+        rel = float((got.float() - want).norm() / want.norm())
+        assert rel <= 1e-2, rel
+
+
+@pytest.mark.parametrize("rows,n", [(4096, 768), (1000, 3072), (77, 2304), (33, 13)])
+def test_bias_grad_and_gelu_epilogues_match_torch(cuda, rows, n):
+    """Linear-layer epilogues: the deterministic bias-gradient column sum, the
+    GELU forward and the fused GELU-backward + bias-gradient pass, against
+    torch's bf16 ops and an fp32 reference; LinearFn / LinearGeluFn gradients
+    against torch autograd."""
+    g = torch.Generator().manual_seed(rows * n)
+    dy = torch.randn(rows, n, generator=g).to(torch.bfloat16).to(cuda)
+    db = K.bias_grad(dy)
+    ref = dy.float().sum(0)
+    assert float((db.float() - ref).norm() / ref.norm()) <= 4e-3
+    assert torch.equal(db, K.bias_grad(dy))                    # deterministic
+    # GELU forward + fused backward vs torch (same fp32 formula, bf16 rounding)
+    pre = (torch.randn(rows, n, generator=g) * 3).to(torch.bfloat16).to(cuda)
+    x = pre.clone().requires_grad_(True)
+    yt = torch.nn.functional.gelu(x, approximate="tanh")
+    yt.backward(dy)
+    y = torch.empty_like(pre)
+    K.load().het_gelu_fwd(pre.data_ptr(), y.data_ptr(), pre.numel(), 0)
+    dpre = torch.empty_like(pre)
+    dbg = torch.empty(n, dtype=torch.bfloat16, device=cuda)
+    part = K._colsum_scratch(rows, n, cuda)
+    assert K.load().het_gelu_bwd_bias(dy.data_ptr(), pre.data_ptr(), dpre.data_ptr(), rows, n,
+                                      dbg.data_ptr(), part.data_ptr(), 0) == 0
+    torch.cuda.synchronize()
+    for got, want in ((y, yt), (dpre, x.grad)):
+        d = (got.float() - want.float()).abs()
+        assert float((d > want.float().abs() * 2 ** -7 + 1e-6).float().mean()) < 1e-3
+    refb = x.grad.float().sum(0)
+    assert float((dbg.float() - refb).norm() / refb.norm()) <= 4e-3
+    # the autograd functions against torch's F.linear (+ GELU)
+    k = 64
+    xin = torch.randn(rows, k, generator=g).to(torch.bfloat16).to(cuda)
+    w = (torch.randn(n, k, generator=g) * 0.1).to(torch.bfloat16).to(cuda)
+    b = (torch.randn(n, generator=g) * 0.1).to(torch.bfloat16).to(cuda)
+    for fused, ref_fn in ((K.LinearFn.apply, lambda a, c, e: torch.nn.functional.linear(a, c, e)),
+                          (K.LinearGeluFn.apply, lambda a, c, e: torch.nn.functional.gelu(
+                              torch.nn.functional.linear(a, c, e), approximate="tanh"))):
+        ins1 = [t.clone().requires_grad_(True) for t in (xin, w, b)]
+        ins2 = [t.float().clone().requires_grad_(True) for t in (xin, w, b)]
+        fused(*ins1).backward(dy)
+        ref_fn(*ins2).backward(dy.float())
+        for a1, a2 in zip(ins1, ins2):
+            rel = float((a1.grad.float() - a2.grad).norm() / a2.grad.norm())
+            assert rel <= 1.5e-2, rel
