@@ -26,7 +26,7 @@ extern "C" {
 #define HET_ECUDA 2
 #define HET_ENCCL 3
 
-#define HET_MAX_SEGS 64
+#define HET_MAX_SEGS 256   /* segments per het_accumulate launch (kernel parameter table) */
 
 /* One gradient tensor landing in a unit-sized fp32 accumulator. */
 typedef struct {
@@ -122,6 +122,15 @@ int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* r
  * (inverse) rotation. */
 int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int inverse,
                      void* stream);
+
+/* Fused q/k/v projection output [rows, 3*heads*dh] (q | k | v per row) ->
+ * rotary-embedded q and k and a copy of v, each contiguous [rows, heads, dh]
+ * (row r at position r % seq); merge = the backward: dq, dk (inverse
+ * rotation) and dv into one [rows, 3*heads*dh] gradient. dh % 16 == 0. */
+int het_rope_qkv_split(const void* qkv, void* q, void* k, void* v, int64_t rows, int heads, int dh,
+                       int64_t seq, void* stream);
+int het_rope_qkv_merge(const void* dq, const void* dk, const void* dv, void* dqkv, int64_t rows,
+                       int heads, int dh, int64_t seq, void* stream);
 
 /* SwiGLU on bf16: out[r, j] = silu(a[r, j]) * b[r, j] for r < rows, j < f,
  * a and b with row stride ld (separate tensors, or the two halves of one

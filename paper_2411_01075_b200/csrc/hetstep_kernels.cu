@@ -165,10 +165,15 @@ __global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__
                                                              const __grid_constant__ SegTable t,
                                                              float w) {
   constexpr int64_t kAccChunk = static_cast<int64_t>(THREADS) * kAccVec * ITERS;
-  // locate this block's segment (<= 64 entries; warp-uniform scan)
+  // locate this block's segment: binary search of the block prefix sums
+  // (uniform per CTA; the table sits in the kernel parameter bank)
   const int64_t b = blockIdx.x;
-  int s = 0;
-  while (s + 1 < t.nseg && t.first_block[s + 1] <= b) ++s;
+  int lo = 0, hi = t.nseg - 1;            // invariant: first_block[lo] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.first_block[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const int s = lo;
   const het_seg_t sg = t.seg[s];
   const int64_t base = (b - t.first_block[s]) * kAccChunk;
   const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(sg.src);

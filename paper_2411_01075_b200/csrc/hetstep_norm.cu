@@ -615,6 +615,61 @@ unsigned elementwise_grid(int64_t items, int threads) {
   return static_cast<unsigned>(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
 }
 
+
+// Fused q/k/v projection output [rows, 3 * heads * dh] -> rotary-embedded q, k and a
+// copy of v, each contiguous [rows, heads, dh] (MERGE = false), or the backward:
+// dq, dk (inverse rotation) and dv back into one [rows, 3 * heads * dh] gradient
+// (MERGE = true). One thread per (row, head, 8-pair group): 16-byte accesses.
+template <bool MERGE>
+__global__ void rope_qkv_kernel(const __nv_bfloat16* __restrict__ in0,
+                                const __nv_bfloat16* __restrict__ in1,
+                                const __nv_bfloat16* __restrict__ in2,
+                                __nv_bfloat16* __restrict__ out0, __nv_bfloat16* __restrict__ out1,
+                                __nv_bfloat16* __restrict__ out2, int64_t rows, int heads, int dh,
+                                int64_t seq) {
+  const int half = dh / 2, groups = half / 8;
+  const int64_t d = static_cast<int64_t>(heads) * dh;
+  const int64_t total = rows * heads * groups;
+  const float sign = MERGE ? -1.f : 1.f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += stride) {
+    const int gi = static_cast<int>(t % groups);
+    const int64_t rh = t / groups;                 // row * heads + head
+    const int64_t row = rh / heads;
+    const int head = static_cast<int>(rh - row * heads);
+    const int64_t pos = row % seq;
+    const int64_t packed = row * 3 * d + static_cast<int64_t>(head) * dh;   // q slot in [rows, 3d]
+    const int64_t split = row * d + static_cast<int64_t>(head) * dh;        // in [rows, d]
+    const int i0 = gi * 8;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {      // q, k
+      const __nv_bfloat16* src = MERGE ? (which ? in1 : in0) + split : in0 + packed + which * d;
+      __nv_bfloat16* dst = MERGE ? out0 + packed + which * d : (which ? out1 : out0) + split;
+      __nv_bfloat16 lo[8], hi[8], ol[8], oh[8];
+      *reinterpret_cast<uint4*>(lo) = *reinterpret_cast<const uint4*>(src + i0);
+      *reinterpret_cast<uint4*>(hi) = *reinterpret_cast<const uint4*>(src + i0 + half);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + j;
+        const float inv = exp2f(-static_cast<float>(2 * i) / dh * 13.287712379549449f);
+        float sn, cs;
+        __sincosf(static_cast<float>(pos) * inv, &sn, &cs);
+        sn *= sign;
+        const float a = __bfloat162float(lo[j]), b = __bfloat162float(hi[j]);
+        ol[j] = __float2bfloat16_rn(a * cs - b * sn);
+        oh[j] = __float2bfloat16_rn(a * sn + b * cs);
+      }
+      *reinterpret_cast<uint4*>(dst + i0) = *reinterpret_cast<const uint4*>(ol);
+      *reinterpret_cast<uint4*>(dst + i0 + half) = *reinterpret_cast<const uint4*>(oh);
+    }
+    // v: plain copy of this thread's 2 x 8 elements
+    const __nv_bfloat16* vs = MERGE ? in2 + split : in0 + packed + 2 * d;
+    __nv_bfloat16* vd = MERGE ? out0 + packed + 2 * d : out2 + split;
+    *reinterpret_cast<uint4*>(vd + i0) = *reinterpret_cast<const uint4*>(vs + i0);
+    *reinterpret_cast<uint4*>(vd + i0 + half) = *reinterpret_cast<const uint4*>(vs + i0 + half);
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -715,6 +770,33 @@ int het_swiglu_bwd(const void* dout, const void* a, const void* b, int64_t ld, v
     swiglu_bwd_kernel<1><<<elementwise_grid(rows * f, 256), 256, 0, st>>>(G, A, B, ld, DA, DB, ldg,
                                                                          rows, f);
   return het::check_launch("het_swiglu_bwd");
+}
+
+int het_rope_qkv_split(const void* qkv, void* q, void* k, void* v, int64_t rows, int heads, int dh,
+                       int64_t seq, void* stream) {
+  if (!qkv || !q || !k || !v || rows < 0 || heads <= 0 || dh <= 0 || dh % 16 || seq <= 0 ||
+      !aligned16(qkv) || !aligned16(q) || !aligned16(k) || !aligned16(v))
+    return fail(HET_EARG, "het_rope_qkv_split: bad args (dh %% 16, 16-byte alignment)");
+  const int64_t total = rows * heads * (dh / 16);
+  if (total == 0) return HET_OK;
+  rope_qkv_kernel<false><<<elementwise_grid(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(qkv), nullptr, nullptr, static_cast<__nv_bfloat16*>(q),
+      static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v), rows, heads, dh, seq);
+  return het::check_launch("het_rope_qkv_split");
+}
+
+int het_rope_qkv_merge(const void* dq, const void* dk, const void* dv, void* dqkv, int64_t rows,
+                       int heads, int dh, int64_t seq, void* stream) {
+  if (!dq || !dk || !dv || !dqkv || rows < 0 || heads <= 0 || dh <= 0 || dh % 16 || seq <= 0 ||
+      !aligned16(dq) || !aligned16(dk) || !aligned16(dv) || !aligned16(dqkv))
+    return fail(HET_EARG, "het_rope_qkv_merge: bad args (dh %% 16, 16-byte alignment)");
+  const int64_t total = rows * heads * (dh / 16);
+  if (total == 0) return HET_OK;
+  rope_qkv_kernel<true><<<elementwise_grid(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(dq), static_cast<const __nv_bfloat16*>(dk),
+      static_cast<const __nv_bfloat16*>(dv), static_cast<__nv_bfloat16*>(dqkv), nullptr, nullptr,
+      rows, heads, dh, seq);
+  return het::check_launch("het_rope_qkv_merge");
 }
 
 }  // extern "C"

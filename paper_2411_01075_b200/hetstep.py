@@ -16,7 +16,7 @@ from ._build import STEP_LIB, build_step
 from .core import InputError
 
 HET_OK, HET_EARG, HET_ECUDA, HET_ENCCL = 0, 1, 2, 3
-HET_MAX_SEGS = 64
+HET_MAX_SEGS = 256
 ACC_ADD, ACC_FIRST = 0, 1
 DT_BF16, DT_F32 = 0, 1
 ALGO_AUTO, ALGO_P2P, ALGO_OWNER, ALGO_EVEN = 0, 1, 2, 3
@@ -30,7 +30,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
            "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
            "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace",
-           "het_swiglu_fwd", "het_swiglu_bwd", "het_colsum_partial_floats", "het_bias_grad",
+           "het_swiglu_fwd", "het_swiglu_bwd", "het_rope_qkv_split", "het_rope_qkv_merge", "het_colsum_partial_floats", "het_bias_grad",
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
@@ -77,6 +77,8 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_rope_inplace": ([vp, i64, i32, i32, i64, i32, vp], i32),
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
         "het_swiglu_fwd": ([vp, vp, i64, vp, i64, i64, vp], i32),
+        "het_rope_qkv_split": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
+        "het_rope_qkv_merge": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
         "het_colsum_partial_floats": ([i64, i64], i64),
         "het_bias_grad": ([vp, i64, i64, vp, vp, vp], i32),
         "het_gelu_fwd": ([vp, vp, i64, vp], i32),
@@ -162,14 +164,19 @@ def accumulate(acc: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]], fir
             accumulate(acc, grads[i:i + HET_MAX_SEGS], first, scale, stream)
         return
     cap = acc.numel()
-    segs = (HetSeg * len(grads))()
+    rows: list[list[int]] = []      # [src, dst_off, n]; back-to-back segments coalesce
     for i, (g, off) in enumerate(grads):
         if off < 0 or off + g.numel() > cap:
             raise InputError(f"accumulate: segment {i} [{off}, {off + g.numel()}) outside {cap}")
-        segs[i].src = _cuda(g, torch.bfloat16, f"grad[{i}]")
-        segs[i].dst_off = off
-        segs[i].n = g.numel()
-    _check(load().het_accumulate(_cuda(acc, torch.float32, "acc"), segs, len(grads),
+        src, n = _cuda(g, torch.bfloat16, f"grad[{i}]"), g.numel()
+        if rows and rows[-1][0] + 2 * rows[-1][2] == src and rows[-1][1] + rows[-1][2] == off:
+            rows[-1][2] += n
+        else:
+            rows.append([src, off, n])
+    segs = (HetSeg * len(rows))()
+    for i, (src, off, n) in enumerate(rows):
+        segs[i].src, segs[i].dst_off, segs[i].n = src, off, n
+    _check(load().het_accumulate(_cuda(acc, torch.float32, "acc"), segs, len(rows),
                                  ACC_FIRST if first else ACC_ADD, float(scale), _stream(stream)),
            "het_accumulate")
 
@@ -454,6 +461,100 @@ def linear_gelu(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tens
 
 def swiglu(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return SwiGLUFn.apply(a, b)
+
+
+class SwiGLUPackedFn(torch.autograd.Function):
+    """silu(y[..., :f]) * y[..., f:] of one contiguous [..., 2f] projection; the
+    backward writes both halves of dy in one pass (no slice/cat copies)."""
+
+    @staticmethod
+    def forward(ctx, y):
+        f = y.shape[-1] // 2
+        y2 = y.reshape(-1, 2 * f)
+        if not y2.is_contiguous():
+            y2 = y2.contiguous()
+        out = torch.empty(*y.shape[:-1], f, dtype=torch.bfloat16, device=y.device)
+        p = _cuda(y2, torch.bfloat16, "y")
+        _check(load().het_swiglu_fwd(p, p + 2 * f, 2 * f, out.data_ptr(), y2.shape[0], f,
+                                     _stream(None)), "het_swiglu_fwd")
+        ctx.save_for_backward(y2)
+        ctx.shape = y.shape
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        (y2,) = ctx.saved_tensors
+        rows, f = y2.shape[0], y2.shape[1] // 2
+        g = g.reshape(rows, f).contiguous()
+        dy = torch.empty_like(y2)
+        p, q = y2.data_ptr(), dy.data_ptr()
+        _check(load().het_swiglu_bwd(g.data_ptr(), p, p + 2 * f, 2 * f, q, q + 2 * f, 2 * f, rows,
+                                     f, _stream(None)), "het_swiglu_bwd")
+        return dy.view(ctx.shape)
+
+
+def swiglu_packed(y: torch.Tensor) -> torch.Tensor:
+    return SwiGLUPackedFn.apply(y)
+
+
+class AdjacentRowsFn(torch.autograd.Function):
+    """Row-major matrices that sit back to back in one buffer (a unit's flat
+    layout), seen as their row concatenation without a copy; the gradient
+    splits back into views."""
+
+    @staticmethod
+    def forward(ctx, *ts):
+        a = ts[0]
+        pos = a.data_ptr()
+        for t in ts:
+            if t.data_ptr() != pos or not t.is_contiguous() or t.shape[1:] != a.shape[1:] or \
+                    t.dtype != a.dtype:
+                raise InputError("adjacent_rows: matrices are not adjacent in memory")
+            pos += t.numel() * t.element_size()
+        ctx.rows = [t.shape[0] for t in ts]
+        return a.as_strided((sum(ctx.rows),) + tuple(a.shape[1:]), a.stride())
+
+    @staticmethod
+    def backward(ctx, g):
+        return tuple(g.split(ctx.rows, dim=0))
+
+
+def adjacent_rows(*ts: torch.Tensor) -> torch.Tensor:
+    return AdjacentRowsFn.apply(*ts)
+
+
+class RopeQKVFn(torch.autograd.Function):
+    """[b, s, 3d] fused q/k/v projection -> rotary q, k and v as contiguous
+    [b, s, heads, dh] tensors (one pass), and the backward back into one
+    [b, s, 3d] gradient (one pass: no cat, no adds of three dgrad GEMMs)."""
+
+    @staticmethod
+    def forward(ctx, y, heads):
+        b, s, d3 = y.shape
+        d = d3 // 3
+        dh = d // heads
+        y = y.contiguous()
+        q, k, v = (torch.empty(b, s, heads, dh, dtype=torch.bfloat16, device=y.device)
+                   for _ in range(3))
+        _check(load().het_rope_qkv_split(_cuda(y, torch.bfloat16, "qkv"), q.data_ptr(),
+                                         k.data_ptr(), v.data_ptr(), b * s, heads, dh, s,
+                                         _stream(None)), "het_rope_qkv_split")
+        ctx.dims = (b, s, heads, dh)
+        return q, k, v
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        b, s, heads, dh = ctx.dims
+        dq, dk, dv = (t.contiguous() for t in (dq, dk, dv))
+        dy = torch.empty(b, s, 3 * heads * dh, dtype=torch.bfloat16, device=dq.device)
+        _check(load().het_rope_qkv_merge(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                         dy.data_ptr(), b * s, heads, dh, s, _stream(None)),
+               "het_rope_qkv_merge")
+        return dy, None
+
+
+def rope_qkv(y: torch.Tensor, heads: int):
+    return RopeQKVFn.apply(y, heads)
 
 
 def rope_(t: torch.Tensor) -> torch.Tensor:

@@ -154,14 +154,17 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     if arch.kind == "llama":
         if x.is_cuda and x.dtype == torch.bfloat16 and d in _K.RMS_DIMS:
             # fused sm_100a RMSNorm and in-place rotary embedding (no cos/sin/cat temporaries)
+            # wq|wk|wv and w1|w3 sit back to back in the unit's flat layout: one GEMM
+            # each (no weight copies), RoPE and the head split in one pass, SwiGLU over
+            # the packed projection
             h = _K.rms_norm(x, p["rms1"])
-            q = _K.rope_((h @ p["wq"].t()).view(b, s, H, dh)).transpose(1, 2)
-            k = _K.rope_((h @ p["wk"].t()).view(b, s, H, dh)).transpose(1, 2)
-            v = (h @ p["wv"].t()).view(b, s, H, dh).transpose(1, 2)
+            qkv = h @ _K.adjacent_rows(p["wq"], p["wk"], p["wv"]).t()
+            q, k, v = (t.transpose(1, 2) for t in _K.rope_qkv(qkv, H))
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
             x = x + a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
             h = _K.rms_norm(x, p["rms2"])
-            return x + _K.swiglu(h @ p["w1"].t(), h @ p["w3"].t()) @ p["w2"].t()
+            w13 = _K.adjacent_rows(p["w1"], p["w3"])
+            return x + _K.swiglu_packed(h @ w13.t()) @ p["w2"].t()
         h = _rms(x, p["rms1"])
         q = (h @ p["wq"].t()).view(b, s, H, dh).transpose(1, 2)
         k = (h @ p["wk"].t()).view(b, s, H, dh).transpose(1, 2)

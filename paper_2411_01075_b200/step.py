@@ -172,6 +172,10 @@ class UnevenFSDPTrainer:
         # (decided from the whole plan so every rank issues its collectives in the same order)
         self.pair_units = self.L.blocks >= 2 and all(a.num_microbatches <= 1
                                                      for a in plan.assignments)
+        # units per grouped launch: pairs under collectives (each pair's reduce-scatters
+        # overlap the next pair's backward); with one rank nothing overlaps, so the whole
+        # backward's bf16 -> fp32 scale-cast is one launch (holds 2 B/param of bf16 grads)
+        self.acc_group = self.L.blocks if self.N == 1 else 2
         self._set_routes(self.symm is not None)
         self.route_check = None
         if self.symm is not None and check_routes:
@@ -646,8 +650,8 @@ class UnevenFSDPTrainer:
                     rs_ev[u] = self._rs(u, acc, done_ev[u])
                 continue
             pending.append((u, unit_grads if mb else []))   # idle ranks still reduce-scatter
-            if len(pending) < 2 and u > 0:
-                continue                             # wait for the pair's second unit
+            if len(pending) < self.acc_group and u > 0:
+                continue                             # wait for the group's last unit
             if multi:
                 # both accumulators are rewritten: their previous readers are the last
                 # pair's reduce-scatters (the second one ends with a cross-rank barrier

@@ -302,3 +302,52 @@ def test_bias_grad_and_gelu_epilogues_match_torch(cuda, rows, n):
         for a1, a2 in zip(ins1, ins2):
             rel = float((a1.grad.float() - a2.grad).norm() / a2.grad.norm())
             assert rel <= 1.5e-2, rel
+
+
+def test_rope_qkv_split_merge_and_packed_swiglu(cuda):
+    """Llama unit passes over fused projections: q/k/v split with RoPE (vs the
+    CPU oracle's rotary; the backward is its transpose), SwiGLU over one packed
+    [.., 2f] projection (vs torch), and the copy-free adjacent-rows view."""
+    from oracle import model_oracle as MO
+    from oracle.tolerances import norm_rel
+    b, s, H, dh = 2, 64, 4, 64
+    d = H * dh
+    g = torch.Generator().manual_seed(5)
+    y = torch.randn(b, s, 3 * d, generator=g).to(torch.bfloat16)
+    yc = y.to(cuda).requires_grad_(True)
+    q, k, v = K.rope_qkv(yc, H)
+    yf = y.float().requires_grad_(True)
+    heads = lambda t: t.view(b, s, H, dh).transpose(1, 2)       # noqa: E731
+    rq = MO._rotary(heads(yf[..., :d])).transpose(1, 2)
+    rk = MO._rotary(heads(yf[..., d:2 * d])).transpose(1, 2)
+    rv = yf[..., 2 * d:].view(b, s, H, dh)
+    for got, want in ((q, rq), (k, rk), (v, rv)):
+        assert norm_rel(got.float().detach().cpu().numpy(), want.detach().numpy()) <= 1e-2
+    assert torch.equal(v.detach().cpu(), y[..., 2 * d:].view(b, s, H, dh))
+    dq, dk, dv = (torch.randn(b, s, H, dh, generator=g).to(torch.bfloat16) for _ in range(3))
+    torch.autograd.backward([q, k, v], [t.to(cuda) for t in (dq, dk, dv)])
+    torch.autograd.backward([rq, rk, rv], [t.float() for t in (dq, dk, dv)])
+    assert norm_rel(yc.grad.float().cpu().numpy(), yf.grad.numpy()) <= 1e-2
+    # packed SwiGLU
+    f = 96
+    yp = (torch.randn(b * s, 2 * f, generator=g) * 2).to(torch.bfloat16).to(cuda)
+    y1 = yp.clone().requires_grad_(True)
+    y2 = yp.clone().requires_grad_(True)
+    out1 = K.swiglu_packed(y1)
+    out2 = torch.nn.functional.silu(y2[:, :f]) * y2[:, f:]
+    go = torch.randn(b * s, f, generator=g).to(torch.bfloat16).to(cuda)
+    out1.backward(go)
+    out2.backward(go)
+    for got, want in ((out1, out2), (y1.grad, y2.grad)):
+        dd = (got.float() - want.float()).abs()
+        assert float((dd > want.float().abs() * 2 ** -7 + 1e-30).float().mean()) < 1e-3
+    # adjacent rows: a view, gradients split back
+    buf = torch.randn(10 * 8, device=cuda, dtype=torch.bfloat16)
+    a, c = buf[:24].view(3, 8).requires_grad_(True), buf[24:80].view(7, 8).requires_grad_(True)
+    w = K.adjacent_rows(a, c)
+    assert w.data_ptr() == buf.data_ptr() and w.shape == (10, 8)
+    (w.float() * torch.arange(10, device=cuda)[:, None]).sum().backward()
+    assert torch.equal(a.grad, torch.arange(3, device=cuda)[:, None].expand(3, 8).to(a.dtype))
+    assert torch.equal(c.grad, torch.arange(3, 10, device=cuda)[:, None].expand(7, 8).to(a.dtype))
+    with pytest.raises(Exception):
+        K.adjacent_rows(c, a)

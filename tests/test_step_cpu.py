@@ -53,7 +53,7 @@ def test_single_rank_step_gradients(fake, m, l):
         assert float((got - g.double()).norm() / g.double().norm()) <= 2e-2
     # one accumulate per (unit, microbatch) + head and embedding passes, one AdamW
     n_acc = fake.calls.count("accumulate")
-    unit_launches = (arch.layers + 1) // 2 if l == 1 else arch.layers * l   # l=1: unit pairs
+    unit_launches = 1 if l == 1 else arch.layers * l     # l=1, one rank: one grouped launch
     assert n_acc == unit_launches + l            # units + head; embedding is fused
     assert fake.calls.count("embedding_grad") == l
     assert fake.calls.count("adamw") == 1
