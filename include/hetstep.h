@@ -120,6 +120,21 @@ int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* r
 /* Rotary position embedding in place on bf16 [rows, heads, dh] (row r at
  * position r % seq, rotate-half pairs); inverse=1 applies the backward
  * (inverse) rotation. */
+/* Residual add fused into the norms: xsum = bf16(x + r) is written and
+ * normalised (forward); the backward adds the residual path's gradient dres
+ * to the norm's input gradient in the same pass (dres may be NULL). */
+int het_layernorm_add_fwd(const void* x, const void* r, const void* w, const void* b, void* xsum,
+                          void* y, float* mean, float* rstd, int64_t rows, int64_t d, float eps,
+                          void* stream);
+int het_layernorm_bwd_add(const void* dy, const void* dres, const void* x, const void* w,
+                          const float* mean, const float* rstd, void* dx, void* dgamma, void* dbeta,
+                          float* partial, int64_t rows, int64_t d, void* stream);
+int het_rmsnorm_add_fwd(const void* x, const void* r, const void* w, void* xsum, void* y,
+                        float* rstd, int64_t rows, int64_t d, float eps, void* stream);
+int het_rmsnorm_bwd_add(const void* dy, const void* dres, const void* x, const void* w,
+                        const float* rstd, void* dx, void* dgamma, float* partial, int64_t rows,
+                        int64_t d, void* stream);
+
 int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int inverse,
                      void* stream);
 

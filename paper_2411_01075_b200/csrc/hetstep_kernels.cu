@@ -160,22 +160,11 @@ __device__ __forceinline__ float acc_op(float a, float g, float w) {
   return MODE == HET_ACC_FIRST ? w * g : fmaf(w, g, a);
 }
 
+// One chunk (THREADS * 8 * ITERS elements) of one segment.
 template <int MODE, int THREADS, int ITERS>
-__global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__ acc,
-                                                             const __grid_constant__ SegTable t,
-                                                             float w) {
+__device__ __forceinline__ void acc_chunk(float* __restrict__ acc, const het_seg_t& sg,
+                                          int64_t base, float w) {
   constexpr int64_t kAccChunk = static_cast<int64_t>(THREADS) * kAccVec * ITERS;
-  // locate this block's segment: binary search of the block prefix sums
-  // (uniform per CTA; the table sits in the kernel parameter bank)
-  const int64_t b = blockIdx.x;
-  int lo = 0, hi = t.nseg - 1;            // invariant: first_block[lo] <= b
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (t.first_block[mid] <= b) lo = mid; else hi = mid - 1;
-  }
-  const int s = lo;
-  const het_seg_t sg = t.seg[s];
-  const int64_t base = (b - t.first_block[s]) * kAccChunk;
   const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(sg.src);
   float* dst = acc + sg.dst_off;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
@@ -222,6 +211,30 @@ __global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__
     const float g = __bfloat162float(src[e]);
     const float a = (MODE & HET_ACC_FIRST) ? 0.f : dst[e];
     dst[e] = acc_op<MODE>(a, g, w);
+  }
+}
+
+// Persistent grid over the launch's chunks (prefix sums in the parameter
+// table): a CTA binary-searches its first chunk's segment once, then walks
+// forward with the grid stride, so the table lookup is amortised over the
+// CTA's chunks instead of paid per chunk.
+template <int MODE, int THREADS, int ITERS>
+__global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__ acc,
+                                                             const __grid_constant__ SegTable t,
+                                                             float w) {
+  constexpr int64_t kAccChunk = static_cast<int64_t>(THREADS) * kAccVec * ITERS;
+  const int64_t total = t.first_block[t.nseg];
+  int64_t b = blockIdx.x;
+  if (b >= total) return;
+  int lo = 0, hi = t.nseg - 1;            // invariant: first_block[lo] <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.first_block[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  int s = lo;
+  for (; b < total; b += gridDim.x) {
+    while (s + 1 < t.nseg && t.first_block[s + 1] <= b) ++s;
+    acc_chunk<MODE, THREADS, ITERS>(acc, t.seg[s], (b - t.first_block[s]) * kAccChunk, w);
   }
 }
 
@@ -422,13 +435,22 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
   if (blocks == 0) return HET_OK;
   if (blocks > 0x7fffffff) return fail(HET_EARG, "het_accumulate: too large");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const dim3 grid(static_cast<unsigned>(blocks));
+  // persistent: at most the resident CTAs of the variant (occupancy, cached per variant)
+  static int resident[8][2] = {};
 #define HET_ACC_LAUNCH(T, I)                                                              \
   do {                                                                                    \
-    if (mode == HET_ACC_FIRST)                                                            \
-      accumulate_kernel<HET_ACC_FIRST, T, I><<<grid, T, 0, st>>>(acc, t, scale);          \
-    else                                                                                  \
-      accumulate_kernel<HET_ACC_ADD, T, I><<<grid, T, 0, st>>>(acc, t, scale);            \
+    auto kf = mode == HET_ACC_FIRST ? accumulate_kernel<HET_ACC_FIRST, T, I>              \
+                                    : accumulate_kernel<HET_ACC_ADD, T, I>;               \
+    int& r = resident[g_acc_variant][mode == HET_ACC_FIRST];                              \
+    if (r == 0) {                                                                         \
+      int per_sm = 0, dev = 0, sms = 0;                                                   \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, T, 0);                   \
+      cudaGetDevice(&dev);                                                                \
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                  \
+      r = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);                              \
+    }                                                                                     \
+    const dim3 grid(static_cast<unsigned>(blocks < r ? blocks : r));                      \
+    kf<<<grid, T, 0, st>>>(acc, t, scale);                                                \
   } while (0)
   switch (g_acc_variant) {
     case 1: HET_ACC_LAUNCH(256, 2); break;

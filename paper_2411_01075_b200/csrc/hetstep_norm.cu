@@ -49,8 +49,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 template <int CHUNKS>
 __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-    const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ r,
+    const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ b,
+    __nv_bfloat16* __restrict__ xsum, __nv_bfloat16* __restrict__ y,
     float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows, float eps) {
   constexpr int D = CHUNKS * 256;
   const int lane = threadIdx.x & 31;
@@ -62,6 +63,14 @@ __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(
 #pragma unroll
   for (int c = 0; c < CHUNKS; ++c) {
     load8(xr + c * 256 + lane * 8, v[c]);
+    if (r) {                                   // residual add first: xsum = bf16(x + r)
+      float rv[8];
+      load8(r + row * D + c * 256 + lane * 8, rv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[c][i] = __bfloat162float(__float2bfloat16_rn(v[c][i] + rv[i]));
+      store8(xsum + row * D + c * 256 + lane * 8, v[c]);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += v[c][i];
   }
@@ -92,10 +101,11 @@ __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(
 
 template <int CHUNKS>
 __global__ void __launch_bounds__(kWarps * 32, CHUNKS > 3 ? 1 : 2) ln_bwd_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-    const __nv_bfloat16* __restrict__ w, const float* __restrict__ mean,
-    const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
-    float* __restrict__ partial /* [gridDim.x][2][D] */, int64_t rows) {
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dres,
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    const float* __restrict__ mean, const float* __restrict__ rstd,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ partial /* [gridDim.x][2][D] */,
+    int64_t rows) {
   constexpr int D = CHUNKS * 256;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float dg[CHUNKS][8], db[CHUNKS][8];
@@ -133,6 +143,12 @@ __global__ void __launch_bounds__(kWarps * 32, CHUNKS > 3 ? 1 : 2) ln_bwd_kernel
       load8(w + c * 256 + lane * 8, gv);
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] = rs * (dv[i] * gv[i] - s1 - (xv[i] - mu) * rs * s2);
+      if (dres) {                              // + the residual path's gradient
+        float rv[8];
+        load8(dres + row * D + c * 256 + lane * 8, rv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += rv[i];
+      }
       store8(dx + row * D + c * 256 + lane * 8, o);
     }
   }
@@ -212,45 +228,62 @@ extern "C" {
 
 int64_t het_layernorm_partial_floats(int64_t d) { return static_cast<int64_t>(grid_bwd()) * 2 * d; }
 
-int het_layernorm_fwd(const void* x, const void* w, const void* b, void* y, float* mean,
-                      float* rstd, int64_t rows, int64_t d, float eps, void* stream) {
+int het_layernorm_add_fwd(const void* x, const void* r, const void* w, const void* b, void* xsum,
+                          void* y, float* mean, float* rstd, int64_t rows, int64_t d, float eps,
+                          void* stream) {
   if (!x || !w || !b || !y || !mean || !rstd || rows < 0 || (d != 256 && d != 768 && d != 1024) ||
-      !aligned16(x) || !aligned16(y) || !aligned16(w) || !aligned16(b))
+      !aligned16(x) || !aligned16(y) || !aligned16(w) || !aligned16(b) || (r && !xsum) ||
+      (r && (!aligned16(r) || !aligned16(xsum))))
     return fail(HET_EARG, "het_layernorm_fwd: unsupported shape/alignment (d=%lld)", (long long)d);
   if (rows == 0) return HET_OK;
   const unsigned grid = static_cast<unsigned>((rows + kWarps - 1) / kWarps);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto X = static_cast<const __nv_bfloat16*>(x);
+  auto R = static_cast<const __nv_bfloat16*>(r);
   auto W = static_cast<const __nv_bfloat16*>(w);
   auto B = static_cast<const __nv_bfloat16*>(b);
+  auto S = static_cast<__nv_bfloat16*>(xsum);
   auto Y = static_cast<__nv_bfloat16*>(y);
-  if (d == 256) ln_fwd_kernel<1><<<grid, kWarps * 32, 0, st>>>(X, W, B, Y, mean, rstd, rows, eps);
-  else if (d == 768) ln_fwd_kernel<3><<<grid, kWarps * 32, 0, st>>>(X, W, B, Y, mean, rstd, rows, eps);
-  else ln_fwd_kernel<4><<<grid, kWarps * 32, 0, st>>>(X, W, B, Y, mean, rstd, rows, eps);
+  if (d == 256) ln_fwd_kernel<1><<<grid, kWarps * 32, 0, st>>>(X, R, W, B, S, Y, mean, rstd, rows, eps);
+  else if (d == 768) ln_fwd_kernel<3><<<grid, kWarps * 32, 0, st>>>(X, R, W, B, S, Y, mean, rstd, rows, eps);
+  else ln_fwd_kernel<4><<<grid, kWarps * 32, 0, st>>>(X, R, W, B, S, Y, mean, rstd, rows, eps);
   return het::check_launch("het_layernorm_fwd");
 }
 
-int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float* mean,
-                      const float* rstd, void* dx, void* dgamma, void* dbeta, float* partial,
-                      int64_t rows, int64_t d, void* stream) {
+int het_layernorm_fwd(const void* x, const void* w, const void* b, void* y, float* mean,
+                      float* rstd, int64_t rows, int64_t d, float eps, void* stream) {
+  return het_layernorm_add_fwd(x, nullptr, w, b, nullptr, y, mean, rstd, rows, d, eps, stream);
+}
+
+int het_layernorm_bwd_add(const void* dy, const void* dres, const void* x, const void* w,
+                          const float* mean, const float* rstd, void* dx, void* dgamma, void* dbeta,
+                          float* partial, int64_t rows, int64_t d, void* stream) {
   if (!dy || !x || !w || !mean || !rstd || !dx || !dgamma || !dbeta || !partial || rows < 0 ||
       (d != 256 && d != 768 && d != 1024) || !aligned16(dy) || !aligned16(x) || !aligned16(dx) ||
-      !aligned16(w))
+      !aligned16(w) || (dres && !aligned16(dres)))
     return fail(HET_EARG, "het_layernorm_bwd: unsupported shape/alignment (d=%lld)", (long long)d);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblk = grid_bwd();
   auto DY = static_cast<const __nv_bfloat16*>(dy);
+  auto DR = static_cast<const __nv_bfloat16*>(dres);
   auto X = static_cast<const __nv_bfloat16*>(x);
   auto W = static_cast<const __nv_bfloat16*>(w);
   auto DX = static_cast<__nv_bfloat16*>(dx);
-  if (d == 256) ln_bwd_kernel<1><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
-  else if (d == 768) ln_bwd_kernel<3><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
-  else ln_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, mean, rstd, DX, partial, rows);
+  if (d == 256) ln_bwd_kernel<1><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, mean, rstd, DX, partial, rows);
+  else if (d == 768) ln_bwd_kernel<3><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, mean, rstd, DX, partial, rows);
+  else ln_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, mean, rstd, DX, partial, rows);
   int rc = het::check_launch("het_layernorm_bwd");
   if (rc != HET_OK) return rc;
   ln_bwd_finalize_kernel<<<static_cast<unsigned>((2 * d + 31) / 32), 256, 0, st>>>(
       partial, nblk, d, static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
   return het::check_launch("het_layernorm_bwd(finalize)");
+}
+
+int het_layernorm_bwd(const void* dy, const void* x, const void* w, const float* mean,
+                      const float* rstd, void* dx, void* dgamma, void* dbeta, float* partial,
+                      int64_t rows, int64_t d, void* stream) {
+  return het_layernorm_bwd_add(dy, nullptr, x, w, mean, rstd, dx, dgamma, dbeta, partial, rows, d,
+                               stream);
 }
 
 }  // extern "C"
@@ -395,7 +428,8 @@ namespace {
 
 template <int CHUNKS>
 __global__ void __launch_bounds__(kWarps * 32) rms_fwd_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ r,
+    const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ xsum,
     __nv_bfloat16* __restrict__ y, float* __restrict__ rstd_out, int64_t rows, float eps) {
   constexpr int D = CHUNKS * 256;
   const int lane = threadIdx.x & 31;
@@ -406,6 +440,14 @@ __global__ void __launch_bounds__(kWarps * 32) rms_fwd_kernel(
 #pragma unroll
   for (int c = 0; c < CHUNKS; ++c) {
     load8(x + row * D + c * 256 + lane * 8, v[c]);
+    if (r) {                                   // residual add first: xsum = bf16(x + r)
+      float rv[8];
+      load8(r + row * D + c * 256 + lane * 8, rv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[c][i] = __bfloat162float(__float2bfloat16_rn(v[c][i] + rv[i]));
+      store8(xsum + row * D + c * 256 + lane * 8, v[c]);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) q += v[c][i] * v[c][i];
   }
@@ -423,10 +465,10 @@ __global__ void __launch_bounds__(kWarps * 32) rms_fwd_kernel(
 
 template <int CHUNKS>
 __global__ void __launch_bounds__(kWarps * 32, CHUNKS > 4 ? 1 : 2) rms_bwd_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-    const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
-    __nv_bfloat16* __restrict__ dx, float* __restrict__ partial /* [gridDim.x][D] */,
-    int64_t rows) {
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dres,
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
+    float* __restrict__ partial /* [gridDim.x][D] */, int64_t rows) {
   constexpr int D = CHUNKS * 256;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float dg[CHUNKS][8];
@@ -461,6 +503,12 @@ __global__ void __launch_bounds__(kWarps * 32, CHUNKS > 4 ? 1 : 2) rms_bwd_kerne
       load8(w + c * 256 + lane * 8, gv);
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] = rs * (dv[i] * gv[i] - xv[i] * rs * s);
+      if (dres) {                              // + the residual path's gradient
+        float rv[8];
+        load8(dres + row * D + c * 256 + lane * 8, rv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += rv[i];
+      }
       store8(dx + row * D + c * 256 + lane * 8, o);
     }
   }
@@ -676,49 +724,64 @@ extern "C" {
 
 int64_t het_rmsnorm_partial_floats(int64_t d) { return static_cast<int64_t>(grid_bwd()) * d; }
 
-int het_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int64_t d,
-                    float eps, void* stream) {
+int het_rmsnorm_add_fwd(const void* x, const void* r, const void* w, void* xsum, void* y,
+                        float* rstd, int64_t rows, int64_t d, float eps, void* stream) {
   if (!x || !w || !y || !rstd || rows < 0 || (d != 2048 && d != 1024 && d != 768 && d != 256) ||
-      !aligned16(x) || !aligned16(y) || !aligned16(w))
+      !aligned16(x) || !aligned16(y) || !aligned16(w) || (r && !xsum) ||
+      (r && (!aligned16(r) || !aligned16(xsum))))
     return fail(HET_EARG, "het_rmsnorm_fwd: unsupported shape/alignment (d=%lld)", (long long)d);
   if (rows == 0) return HET_OK;
   const unsigned grid = static_cast<unsigned>((rows + kWarps - 1) / kWarps);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto X = static_cast<const __nv_bfloat16*>(x);
+  auto R = static_cast<const __nv_bfloat16*>(r);
   auto W = static_cast<const __nv_bfloat16*>(w);
+  auto S = static_cast<__nv_bfloat16*>(xsum);
   auto Y = static_cast<__nv_bfloat16*>(y);
   switch (d) {
-    case 256: rms_fwd_kernel<1><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps); break;
-    case 768: rms_fwd_kernel<3><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps); break;
-    case 1024: rms_fwd_kernel<4><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps); break;
-    default: rms_fwd_kernel<8><<<grid, kWarps * 32, 0, st>>>(X, W, Y, rstd, rows, eps);
+    case 256: rms_fwd_kernel<1><<<grid, kWarps * 32, 0, st>>>(X, R, W, S, Y, rstd, rows, eps); break;
+    case 768: rms_fwd_kernel<3><<<grid, kWarps * 32, 0, st>>>(X, R, W, S, Y, rstd, rows, eps); break;
+    case 1024: rms_fwd_kernel<4><<<grid, kWarps * 32, 0, st>>>(X, R, W, S, Y, rstd, rows, eps); break;
+    default: rms_fwd_kernel<8><<<grid, kWarps * 32, 0, st>>>(X, R, W, S, Y, rstd, rows, eps);
   }
   return het::check_launch("het_rmsnorm_fwd");
 }
 
-int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, void* dx,
-                    void* dgamma, float* partial, int64_t rows, int64_t d, void* stream) {
+int het_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int64_t d,
+                    float eps, void* stream) {
+  return het_rmsnorm_add_fwd(x, nullptr, w, nullptr, y, rstd, rows, d, eps, stream);
+}
+
+int het_rmsnorm_bwd_add(const void* dy, const void* dres, const void* x, const void* w,
+                        const float* rstd, void* dx, void* dgamma, float* partial, int64_t rows,
+                        int64_t d, void* stream) {
   if (!dy || !x || !w || !rstd || !dx || !dgamma || !partial || rows < 0 ||
       (d != 2048 && d != 1024 && d != 768 && d != 256) || !aligned16(dy) || !aligned16(x) ||
-      !aligned16(dx) || !aligned16(w))
+      !aligned16(dx) || !aligned16(w) || (dres && !aligned16(dres)))
     return fail(HET_EARG, "het_rmsnorm_bwd: unsupported shape/alignment (d=%lld)", (long long)d);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblk = grid_bwd();
   auto DY = static_cast<const __nv_bfloat16*>(dy);
+  auto DR = static_cast<const __nv_bfloat16*>(dres);
   auto X = static_cast<const __nv_bfloat16*>(x);
   auto W = static_cast<const __nv_bfloat16*>(w);
   auto DX = static_cast<__nv_bfloat16*>(dx);
   switch (d) {
-    case 256: rms_bwd_kernel<1><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows); break;
-    case 768: rms_bwd_kernel<3><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows); break;
-    case 1024: rms_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows); break;
-    default: rms_bwd_kernel<8><<<nblk, kWarps * 32, 0, st>>>(DY, X, W, rstd, DX, partial, rows);
+    case 256: rms_bwd_kernel<1><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, rstd, DX, partial, rows); break;
+    case 768: rms_bwd_kernel<3><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, rstd, DX, partial, rows); break;
+    case 1024: rms_bwd_kernel<4><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, rstd, DX, partial, rows); break;
+    default: rms_bwd_kernel<8><<<nblk, kWarps * 32, 0, st>>>(DY, DR, X, W, rstd, DX, partial, rows);
   }
   int rc = het::check_launch("het_rmsnorm_bwd");
   if (rc != HET_OK) return rc;
   rms_bwd_finalize_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(
       partial, nblk, d, static_cast<__nv_bfloat16*>(dgamma));
   return het::check_launch("het_rmsnorm_bwd(finalize)");
+}
+
+int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd, void* dx,
+                    void* dgamma, float* partial, int64_t rows, int64_t d, void* stream) {
+  return het_rmsnorm_bwd_add(dy, nullptr, x, w, rstd, dx, dgamma, partial, rows, d, stream);
 }
 
 int het_rope_inplace(void* x, int64_t rows, int heads, int dh, int64_t seq, int inverse,

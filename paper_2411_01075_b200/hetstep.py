@@ -30,7 +30,9 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
            "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
            "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace",
-           "het_swiglu_fwd", "het_swiglu_bwd", "het_rope_qkv_split", "het_rope_qkv_merge", "het_colsum_partial_floats", "het_bias_grad",
+           "het_swiglu_fwd", "het_swiglu_bwd", "het_rope_qkv_split", "het_rope_qkv_merge",
+           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_rmsnorm_add_fwd",
+           "het_rmsnorm_bwd_add", "het_colsum_partial_floats", "het_bias_grad",
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
@@ -78,6 +80,10 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
         "het_swiglu_fwd": ([vp, vp, i64, vp, i64, i64, vp], i32),
         "het_rope_qkv_split": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
+        "het_layernorm_add_fwd": ([vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
+        "het_layernorm_bwd_add": ([vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
+        "het_rmsnorm_add_fwd": ([vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
+        "het_rmsnorm_bwd_add": ([vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
         "het_rope_qkv_merge": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
         "het_colsum_partial_floats": ([i64, i64], i64),
         "het_bias_grad": ([vp, i64, i64, vp, vp, vp], i32),
@@ -325,6 +331,98 @@ class RMSNormFn(torch.autograd.Function):
 
 def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
     return RMSNormFn.apply(x, w, eps)
+
+
+def _ptr_or_none(t: torch.Tensor | None):
+    return None if t is None else t.contiguous().data_ptr()
+
+
+class AddLayerNormFn(torch.autograd.Function):
+    """(s, LN(s)) with s = x + r: the residual add fused into the LayerNorm pass;
+    the backward adds the residual path's gradient ds to LN's input gradient in
+    the same pass and hands the sum to both x and r (no add kernels either way)."""
+
+    @staticmethod
+    def forward(ctx, x, r, w, b, eps):
+        d = x.shape[-1]
+        xc, rc = x.contiguous(), r.contiguous()
+        rows = xc.numel() // d
+        sm, y = torch.empty_like(xc), torch.empty_like(xc)
+        mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        _check(load().het_layernorm_add_fwd(_cuda(xc, torch.bfloat16, "x"),
+                                            _cuda(rc, torch.bfloat16, "r"),
+                                            _cuda(w, torch.bfloat16, "w"),
+                                            _cuda(b, torch.bfloat16, "b"), sm.data_ptr(),
+                                            y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), rows,
+                                            d, float(eps), _stream(None)), "het_layernorm_add_fwd")
+        ctx.save_for_backward(sm, w, mean, rstd)
+        return sm, y
+
+    @staticmethod
+    def backward(ctx, ds, dy):
+        sm, w, mean, rstd = ctx.saved_tensors
+        d = sm.shape[-1]
+        rows = sm.numel() // d
+        if dy is None:
+            return ds, ds, None, None, None
+        dyc = dy.contiguous()
+        dx = torch.empty_like(sm)
+        dw, db = torch.empty_like(w), torch.empty_like(w)
+        part = torch.empty(int(load().het_layernorm_partial_floats(d)), dtype=torch.float32,
+                           device=sm.device)
+        _check(load().het_layernorm_bwd_add(_cuda(dyc, torch.bfloat16, "dy"), _ptr_or_none(ds),
+                                            sm.data_ptr(), w.data_ptr(), mean.data_ptr(),
+                                            rstd.data_ptr(), dx.data_ptr(), dw.data_ptr(),
+                                            db.data_ptr(), part.data_ptr(), rows, d,
+                                            _stream(None)), "het_layernorm_bwd_add")
+        return dx, dx, dw, db, None
+
+
+class AddRMSNormFn(torch.autograd.Function):
+    """(s, RMSNorm(s)) with s = x + r, residual add fused both ways (as
+    AddLayerNormFn)."""
+
+    @staticmethod
+    def forward(ctx, x, r, w, eps):
+        d = x.shape[-1]
+        xc, rc = x.contiguous(), r.contiguous()
+        rows = xc.numel() // d
+        sm, y = torch.empty_like(xc), torch.empty_like(xc)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        _check(load().het_rmsnorm_add_fwd(_cuda(xc, torch.bfloat16, "x"),
+                                          _cuda(rc, torch.bfloat16, "r"),
+                                          _cuda(w, torch.bfloat16, "w"), sm.data_ptr(),
+                                          y.data_ptr(), rstd.data_ptr(), rows, d, float(eps),
+                                          _stream(None)), "het_rmsnorm_add_fwd")
+        ctx.save_for_backward(sm, w, rstd)
+        return sm, y
+
+    @staticmethod
+    def backward(ctx, ds, dy):
+        sm, w, rstd = ctx.saved_tensors
+        d = sm.shape[-1]
+        rows = sm.numel() // d
+        if dy is None:
+            return ds, ds, None, None
+        dyc = dy.contiguous()
+        dx = torch.empty_like(sm)
+        dw = torch.empty_like(w)
+        part = torch.empty(int(load().het_rmsnorm_partial_floats(d)), dtype=torch.float32,
+                           device=sm.device)
+        _check(load().het_rmsnorm_bwd_add(_cuda(dyc, torch.bfloat16, "dy"), _ptr_or_none(ds),
+                                          sm.data_ptr(), w.data_ptr(), rstd.data_ptr(),
+                                          dx.data_ptr(), dw.data_ptr(), part.data_ptr(), rows, d,
+                                          _stream(None)), "het_rmsnorm_bwd_add")
+        return dx, dx, dw, None
+
+
+def add_layer_norm(x, r, w, b, eps: float = 1e-5):
+    return AddLayerNormFn.apply(x, r, w, b, eps)
+
+
+def add_rms_norm(x, r, w, eps: float = 1e-6):
+    return AddRMSNormFn.apply(x, r, w, eps)
 
 
 class RopeFn(torch.autograd.Function):

@@ -148,6 +148,11 @@ def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
     return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)).to(x.dtype) * w
 
 
+# residual add fused into the following norm (hetstep.add_layer_norm / add_rms_norm);
+# a switch so tools/ab_step.py can A/B it on the same box
+FUSE_RESIDUAL_NORM = True
+
+
 def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -> torch.Tensor:
     b, s, d = x.shape
     H, dh = arch.heads, d // arch.heads
@@ -161,8 +166,12 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
             qkv = h @ _K.adjacent_rows(p["wq"], p["wk"], p["wv"]).t()
             q, k, v = (t.transpose(1, 2) for t in _K.rope_qkv(qkv, H))
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-            x = x + a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
-            h = _K.rms_norm(x, p["rms2"])
+            o = a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
+            if FUSE_RESIDUAL_NORM:
+                x, h = _K.add_rms_norm(x, o, p["rms2"])
+            else:
+                x = x + o
+                h = _K.rms_norm(x, p["rms2"])
             w13 = _K.adjacent_rows(p["w1"], p["w3"])
             return x + _K.swiglu_packed(h @ w13.t()) @ p["w2"].t()
         h = _rms(x, p["rms1"])
@@ -184,8 +193,12 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     q, k, v = lin(h, p["qkv_w"], p["qkv_b"]).split(d, dim=-1)
     q, k, v = (t.view(b, s, H, dh).transpose(1, 2) for t in (q, k, v))
     a = F.scaled_dot_product_attention(q, k, v, is_causal=arch.kind == "gpt")
-    x = x + lin(a.transpose(1, 2).reshape(b, s, d), p["proj_w"], p["proj_b"])
-    h = _ln(x, p["ln2_w"], p["ln2_b"])
+    attn = lin(a.transpose(1, 2).reshape(b, s, d), p["proj_w"], p["proj_b"])
+    if fused and d in _K.LN_DIMS and FUSE_RESIDUAL_NORM:   # add fused into LN2, both ways
+        x, h = _K.add_layer_norm(x, attn, p["ln2_w"], p["ln2_b"])
+    else:
+        x = x + attn
+        h = _ln(x, p["ln2_w"], p["ln2_b"])
     if fused:
         h = _K.linear_gelu(h, p["fc_w"], p["fc_b"])
     else:

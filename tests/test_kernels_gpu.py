@@ -351,3 +351,37 @@ def test_rope_qkv_split_merge_and_packed_swiglu(cuda):
     assert torch.equal(c.grad, torch.arange(3, 10, device=cuda)[:, None].expand(7, 8).to(a.dtype))
     with pytest.raises(Exception):
         K.adjacent_rows(c, a)
+
+
+@pytest.mark.parametrize("kind,d", [("ln", 768), ("ln", 1024), ("rms", 2048), ("rms", 256)])
+def test_residual_add_fused_norms(cuda, kind, d):
+    """(s, norm(s)) with s = x + r in one pass; the backward folds the residual
+    path's gradient into the norm's input gradient. Against torch fp32 with
+    both outputs receiving gradient."""
+    rows = 300
+    g = torch.Generator().manual_seed(d)
+    x = torch.randn(rows, d, generator=g).to(torch.bfloat16)
+    r = torch.randn(rows, d, generator=g).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(d, generator=g)).to(torch.bfloat16)
+    bb = (0.1 * torch.randn(d, generator=g)).to(torch.bfloat16)
+    ds = torch.randn(rows, d, generator=g).to(torch.bfloat16)
+    dy = torch.randn(rows, d, generator=g).to(torch.bfloat16)
+    ins = [t.to(cuda).requires_grad_(True) for t in (x, r, w, bb)]
+    if kind == "ln":
+        s, y = K.add_layer_norm(ins[0], ins[1], ins[2], ins[3])
+    else:
+        s, y = K.add_rms_norm(ins[0], ins[1], ins[2])
+    torch.autograd.backward([s, y], [ds.to(cuda), dy.to(cuda)])
+    ref = [t.float().requires_grad_(True) for t in (x, r, w, bb)]
+    sr = ref[0] + ref[1]
+    if kind == "ln":
+        yr = torch.nn.functional.layer_norm(sr, (d,), ref[2], ref[3], 1e-5)
+    else:
+        yr = sr * torch.rsqrt(sr.pow(2).mean(-1, keepdim=True) + 1e-6) * ref[2]
+    torch.autograd.backward([sr, yr], [ds.float(), dy.float()])
+    assert torch.equal(s.detach().cpu(), (x.float() + r.float()).to(torch.bfloat16))
+    pairs = [(y, yr), (ins[0].grad, ref[0].grad), (ins[1].grad, ref[1].grad),
+             (ins[2].grad, ref[2].grad)] + ([(ins[3].grad, ref[3].grad)] if kind == "ln" else [])
+    for got, want in pairs:
+        rel = float((got.float().cpu() - want.detach()).norm() / want.detach().norm())
+        assert rel <= 1e-2, rel
