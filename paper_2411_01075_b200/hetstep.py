@@ -161,13 +161,19 @@ def pack_bf16(src: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
 
 
 def accumulate(acc: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]], first: bool,
-               scale: float, stream=None) -> None:
-    """acc[off:off+g.numel()] (=|+=) scale * g for every (g, off); g bf16."""
+               scale: float, stream=None, events=None) -> None:
+    """acc[off:off+g.numel()] (=|+=) scale * g for every (g, off); g bf16.
+    `events` = (start, end) CUDA events recorded right around the launch(es),
+    after the host built the segment table (so a timer sees the kernel, not
+    the host work)."""
     if not grads:
         return
     if len(grads) > HET_MAX_SEGS:
-        for i in range(0, len(grads), HET_MAX_SEGS):
-            accumulate(acc, grads[i:i + HET_MAX_SEGS], first, scale, stream)
+        parts = range(0, len(grads), HET_MAX_SEGS)
+        for j, i in enumerate(parts):
+            ev = None if events is None else (events[0] if j == 0 else None,
+                                              events[1] if j == len(parts) - 1 else None)
+            accumulate(acc, grads[i:i + HET_MAX_SEGS], first, scale, stream, ev)
         return
     cap = acc.numel()
     rows: list[list[int]] = []      # [src, dst_off, n]; back-to-back segments coalesce
@@ -182,9 +188,13 @@ def accumulate(acc: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]], fir
     segs = (HetSeg * len(rows))()
     for i, (src, off, n) in enumerate(rows):
         segs[i].src, segs[i].dst_off, segs[i].n = src, off, n
-    _check(load().het_accumulate(_cuda(acc, torch.float32, "acc"), segs, len(rows),
-                                 ACC_FIRST if first else ACC_ADD, float(scale), _stream(stream)),
-           "het_accumulate")
+    accp = _cuda(acc, torch.float32, "acc")
+    if events is not None and events[0] is not None:
+        events[0].record()
+    _check(load().het_accumulate(accp, segs, len(rows), ACC_FIRST if first else ACC_ADD,
+                                 float(scale), _stream(stream)), "het_accumulate")
+    if events is not None and events[1] is not None:
+        events[1].record()
 
 
 def adamw(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,

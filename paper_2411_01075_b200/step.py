@@ -453,21 +453,14 @@ class UnevenFSDPTrainer:
             pairs += [(g, off + seg[nm]) for g, nm in zip(grads, names)]
             n += sum(g.numel() for g in grads)
         a, b = self.timers.pair("accumulate", n * 6.0)
-        if a is not None:
-            a.record()
-        K.accumulate(base, pairs, True, self.w)
-        if b is not None:
-            b.record()
+        K.accumulate(base, pairs, True, self.w, events=None if a is None else (a, b))
         self.launches += 1
 
     def _accumulate(self, acc, grads, names, seg, first):
         n = sum(g.numel() for g in grads)
         a, b = self.timers.pair("accumulate", n * (6.0 if first else 10.0))
-        if a is not None:
-            a.record()
-        K.accumulate(acc, [(g, seg[nm]) for g, nm in zip(grads, names)], first, self.w)
-        if b is not None:
-            b.record()
+        K.accumulate(acc, [(g, seg[nm]) for g, nm in zip(grads, names)], first, self.w,
+                     events=None if a is None else (a, b))
         self.launches += 1
 
     # ------------------------------------------------------------------ step

@@ -45,7 +45,7 @@ def pack_bf16(src, dst, stream=None):
     dst.view(torch.int16).copy_(torch.from_numpy(O.pack(src.numpy()).view(np.int16)))
 
 
-def accumulate(acc, grads, first, scale, stream=None):
+def accumulate(acc, grads, first, scale, stream=None, events=None):
     calls.append("accumulate")
     for g, off in grads:
         n = g.numel()
