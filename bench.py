@@ -216,7 +216,8 @@ def route_summary(tr) -> dict | str:
         return "none"
     return {"ag": {r: tr.ag_route.count(r) for r in sorted(set(tr.ag_route))},
             "rs": {r: tr.rs_route.count(r) for r in sorted(set(tr.rs_route))},
-            "symm_self_check": tr.route_check, "symm_error": tr.symm_error}
+            "symm_self_check": tr.route_check, "symm_error": tr.symm_error,
+            "rs_bf16_wire_units": sum(tr.wire16)}
 
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -293,7 +294,8 @@ def main() -> None:
         barrier()
     launches = K.LAUNCHES - launches0
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
-    kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate")}
+    kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate", "gather")}
+    kern = {k: v for k, v in kern.items() if v["launches"]}
     tr.timers.enabled = False
 
     # ---- end to end through the public API with host buffers (e2e) --------

@@ -260,6 +260,23 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
                             const int64_t* counts, const int64_t* offsets, uint32_t epoch,
                             int channel, int end_barrier, int policy, int ctas, void* stream);
 
+/* (3) fused, bf16 wire: out[0:counts[r]] = sum_j weights[j] * grad_j[offsets[r] : +counts[r]]
+ * in fp32, where grad_j is rank j's UNSCALED bf16 unit gradient at grad_off
+ * (l_j = 1: the microbatch gradient itself) and weights[j] = m_j / B (Eq. 1).
+ * The per-rank weighting and the bf16 -> fp32 cast happen inside the
+ * reduce-scatter; half the link bytes of the fp32 form. Peer loads, summed
+ * in rank order (so equal, bit for bit, to het_symm_reduce_scatter's peer
+ * route over pre-scaled fp32 accumulators). */
+int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* out,
+                                 const int64_t* counts, const int64_t* offsets,
+                                 const float* weights, uint32_t epoch, int channel,
+                                 int end_barrier, int ctas, void* stream);
+
+/* bf16 gradient segments copied (unscaled) into one bf16 unit buffer:
+ * dst[segs[i].dst_off : +n] = segs[i].src. The l_i = 1 staging of the bf16-wire
+ * reduce-scatter (4 B/param instead of the fp32 accumulate's 6). */
+int het_gather_bf16(void* dst, const het_seg_t* segs, int nseg, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -238,6 +238,36 @@ __global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__
   }
 }
 
+// bf16 segments copied into one bf16 buffer (persistent grid, as accumulate)
+__global__ void __launch_bounds__(512) gather_bf16_kernel(__nv_bfloat16* __restrict__ dst,
+                                                          const __grid_constant__ SegTable t) {
+  constexpr int64_t kChunk = 512 * 8;
+  const int64_t total = t.first_block[t.nseg];
+  int64_t b = blockIdx.x;
+  if (b >= total) return;
+  int lo = 0, hi = t.nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.first_block[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  int s = lo;
+  for (; b < total; b += gridDim.x) {
+    while (s + 1 < t.nseg && t.first_block[s + 1] <= b) ++s;
+    const het_seg_t sg = t.seg[s];
+    const int64_t base = (b - t.first_block[s]) * kChunk;
+    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(sg.src);
+    __nv_bfloat16* d = dst + sg.dst_off;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(d)) & 15) == 0;
+    const int64_t e = base + threadIdx.x * 8;
+    if (vec && base + kChunk <= sg.n) {
+      *reinterpret_cast<uint4*>(d + e) = __ldcs(reinterpret_cast<const uint4*>(src + e));
+    } else {
+      const int64_t end = base + kChunk < sg.n ? base + kChunk : sg.n;
+      for (int64_t i = base + threadIdx.x; i < end; i += 512) d[i] = src[i];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- AdamW
 
 struct AdamCoef {
@@ -462,6 +492,35 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
   }
 #undef HET_ACC_LAUNCH
   return het::check_launch("het_accumulate");
+}
+
+int het_gather_bf16(void* dst, const het_seg_t* segs, int nseg, void* stream) {
+  if (!dst || !segs || nseg < 1 || nseg > HET_MAX_SEGS)
+    return fail(HET_EARG, "het_gather_bf16: bad args (nseg=%d)", nseg);
+  SegTable t;
+  t.nseg = nseg;
+  int64_t blocks = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (segs[s].n < 0 || segs[s].dst_off < 0 || (segs[s].n > 0 && !segs[s].src))
+      return fail(HET_EARG, "het_gather_bf16: bad segment %d", s);
+    t.seg[s] = segs[s];
+    t.first_block[s] = blocks;
+    blocks += (segs[s].n + 4095) / 4096;
+  }
+  for (int s = nseg; s <= HET_MAX_SEGS; ++s) t.first_block[s] = blocks;
+  if (blocks == 0) return HET_OK;
+  static int resident = 0;
+  if (resident == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_bf16_kernel, 512, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  }
+  const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
+  gather_bf16_kernel<<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<__nv_bfloat16*>(dst), t);
+  return het::check_launch("het_gather_bf16");
 }
 
 int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,

@@ -322,6 +322,99 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading my acc
 }
 
+// ---------------------------------------------------------------- reduce-scatter, bf16 wire
+
+struct Weights {
+  float w[HET_MAX_RANKS];
+};
+
+__device__ __forceinline__ void bf8_to_f(const uint4& raw, float (&f)[8]) {
+  const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float((u[i] & 0xffffu) << 16);
+    f[2 * i + 1] = __uint_as_float(u[i] & 0xffff0000u);
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restrict__ out,
+                                                                const __grid_constant__ Args a,
+                                                                const __grid_constant__ Weights wt) {
+  __shared__ uint64_t peer[HET_MAX_RANKS];
+  HET_STAGE_PEERS(a, peer);
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off};
+  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's gradient is staged
+  const int64_t n = a.count;
+  const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;
+  const int nr = NR > 0 ? NR : s.nranks;
+  constexpr int kMaxR = NR > 0 ? NR : HET_MAX_RANKS;
+  int64_t head = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / 2);
+  if (head > n) head = n;
+  const int64_t nvec = (n - head) / 8;
+  const int64_t body_end = head + nvec * 8;
+  const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  constexpr int kB = NR > 0 ? (16 / NR > 1 ? 16 / NR : 2) : 2;   // vectors per batch
+  for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kB) {
+    uint4 x[kB][kMaxR];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {          // all (vector, rank) loads before any math
+      const int64_t v = v0 + u * gsz;
+      if (v < nvec) {
+        const uint64_t off = src0 + static_cast<uint64_t>(head + v * 8) * 2;
+#pragma unroll
+        for (int p = 0; p < kMaxR; ++p)      // ranks with no batch (w = 0) are not read
+          if (p < nr && wt.w[p] != 0.f)
+            x[u][p] = __ldcg(reinterpret_cast<const uint4*>(peer[p] + off));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < nvec) {
+        // explicit rounding: fl(w_j g_j) summed in rank order, exactly as the fp32
+        // route's (accumulate FIRST, then peer-pull sum) arithmetic
+        float r[8], f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = 0.f;
+#pragma unroll
+        for (int p = 0; p < kMaxR; ++p) {
+          if (p < nr && wt.w[p] != 0.f) {
+            bf8_to_f(x[u][p], f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = __fadd_rn(r[i], __fmul_rn(wt.w[p], f[i]));
+          }
+        }
+        const int64_t e = head + v * 8;
+        if (out_vec) {
+          __stcs(reinterpret_cast<float4*>(out + e), make_float4(r[0], r[1], r[2], r[3]));
+          __stcs(reinterpret_cast<float4*>(out + e + 4), make_float4(r[4], r[5], r[6], r[7]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) out[e + i] = r[i];
+        }
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    auto one = [&](int64_t e) {
+      const uint64_t off = src0 + static_cast<uint64_t>(e) * 2;
+      float r = 0.f;
+      for (int p = 0; p < nr; ++p) {
+        if (wt.w[p] == 0.f) continue;
+        const float g = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(peer[p] + off));
+        r = __fadd_rn(r, __fmul_rn(wt.w[p], g));
+      }
+      out[e] = r;
+    };
+    for (int64_t e = threadIdx.x; e < head; e += blockDim.x) one(e);
+    for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
+  }
+  if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading mine
+}
+
 // multicast kernels do not loop over ranks; peer kernels get the rank count
 // as a template constant for 2/4/8 ranks so their per-rank loops unroll
 #define HET_DISPATCH_NR(mc, n, LAUNCH) \
@@ -422,6 +515,29 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   HET_DISPATCH_NR(mc, s->nranks, HET_RS);
 #undef HET_RS
   return het::check_launch("het_symm_reduce_scatter");
+}
+
+int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* out,
+                                 const int64_t* counts, const int64_t* offsets,
+                                 const float* weights, uint32_t epoch, int channel,
+                                 int end_barrier, int ctas, void* stream) {
+  int rc = check_symm(s, counts, offsets, ctas);
+  if (rc != HET_OK) return rc;
+  if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
+  if (!weights) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: null weights");
+  if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: null out");
+  if (grad_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: grad offset not 16B aligned");
+  Args a{*s, grad_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
+  Weights wt{};
+  for (int j = 0; j < s->nranks; ++j) wt.w[j] = weights[j];
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (s->nranks) {
+    case 2: symm_rs_bf16_kernel<2><<<ctas, kThreads, 0, st>>>(out, a, wt); break;
+    case 4: symm_rs_bf16_kernel<4><<<ctas, kThreads, 0, st>>>(out, a, wt); break;
+    case 8: symm_rs_bf16_kernel<8><<<ctas, kThreads, 0, st>>>(out, a, wt); break;
+    default: symm_rs_bf16_kernel<0><<<ctas, kThreads, 0, st>>>(out, a, wt);
+  }
+  return het::check_launch("het_symm_reduce_scatter_bf16");
 }
 
 }  // extern "C"

@@ -35,7 +35,8 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_rmsnorm_bwd_add", "het_colsum_partial_floats", "het_bias_grad",
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
-           "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter")
+           "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
+           "het_symm_reduce_scatter_bf16", "het_gather_bf16")
 
 
 class HetSeg(ctypes.Structure):
@@ -106,6 +107,11 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_symm_reduce_scatter": ([ctypes.POINTER(HetSymm), ctypes.c_uint64, vp,
                                      ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
                                      i32, i32, i32, i32, vp], i32),
+        "het_symm_reduce_scatter_bf16": ([ctypes.POINTER(HetSymm), ctypes.c_uint64, vp,
+                                          ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                          ctypes.POINTER(f32), ctypes.c_uint32, i32, i32, i32,
+                                          vp], i32),
+        "het_gather_bf16": ([vp, ctypes.POINTER(HetSeg), i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -195,6 +201,26 @@ def accumulate(acc: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]], fir
                                  float(scale), _stream(stream)), "het_accumulate")
     if events is not None and events[1] is not None:
         events[1].record()
+
+
+def gather_bf16(dst: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]],
+                stream=None) -> None:
+    """dst[off:off+g.numel()] = g for every (g, off); bf16, unscaled."""
+    if not grads:
+        return
+    if len(grads) > HET_MAX_SEGS:
+        for i in range(0, len(grads), HET_MAX_SEGS):
+            gather_bf16(dst, grads[i:i + HET_MAX_SEGS], stream)
+        return
+    cap = dst.numel()
+    segs = (HetSeg * len(grads))()
+    for i, (g, off) in enumerate(grads):
+        if off < 0 or off + g.numel() > cap:
+            raise InputError(f"gather_bf16: segment {i} [{off}, {off + g.numel()}) outside {cap}")
+        segs[i].src, segs[i].dst_off, segs[i].n = _cuda(g, torch.bfloat16, f"grad[{i}]"), off, \
+            g.numel()
+    _check(load().het_gather_bf16(_cuda(dst, torch.bfloat16, "dst"), segs, len(grads),
+                                  _stream(stream)), "het_gather_bf16")
 
 
 def adamw(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,
@@ -857,6 +883,22 @@ class SymmWorkspace:
                                               _i64(offsets), self.epoch[1], 1, int(end_barrier),
                                               self.policy, self.ctas, _stream(stream)),
                "het_symm_reduce_scatter")
+
+    def reduce_scatter_bf16(self, region: str, elem_off: int, out: torch.Tensor,
+                            counts: Sequence[int], offsets: Sequence[int],
+                            weights: Sequence[float], end_barrier: bool = False,
+                            stream=None) -> None:
+        """out <- sum_j weights[j] * bf16 gradient of rank j at `region`[elem_off:]
+        (my range), in fp32: Eq. 1 weighting and the cast inside the RS."""
+        self.epoch[1] += 1
+        o = _cuda(out, torch.float32, "out") if out.numel() else None
+        byte_off = self.offsets[region] + 2 * elem_off
+        w = (ctypes.c_float * len(weights))(*[float(x) for x in weights])
+        _check(load().het_symm_reduce_scatter_bf16(ctypes.byref(self.desc), byte_off, o,
+                                                   _i64(counts), _i64(offsets), w, self.epoch[1],
+                                                   1, int(end_barrier), self.ctas,
+                                                   _stream(stream)),
+               "het_symm_reduce_scatter_bf16")
 
     @staticmethod
     def status(reset: bool = False) -> int:

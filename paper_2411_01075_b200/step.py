@@ -57,6 +57,7 @@ class StepTimers:
     enabled: bool = False
     adamw: list = field(default_factory=list)
     accumulate: list = field(default_factory=list)
+    gather: list = field(default_factory=list)
 
     def pair(self, kind: str, nbytes: float):
         """Start/end events for one launch moving `nbytes` algorithmic bytes."""
@@ -69,6 +70,7 @@ class StepTimers:
     def reset(self) -> None:
         self.adamw.clear()
         self.accumulate.clear()
+        self.gather.clear()
 
     def summary(self, kind: str) -> dict:
         """launches, total ms, algorithmic bytes and GB/s over the recorded launches."""
@@ -118,7 +120,8 @@ class UnevenFSDPTrainer:
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
                  algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64,
-                 offload_activations: bool = False, check_routes: bool = True):
+                 offload_activations: bool = False, check_routes: bool = True,
+                 bf16_wire: bool = True):
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
         self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo
@@ -154,7 +157,8 @@ class UnevenFSDPTrainer:
                 self.symm = K.SymmWorkspace(
                     [("ub0", U, torch.bfloat16), ("ub1", U, torch.bfloat16),
                      ("rbuf", E, torch.bfloat16), ("acc0", U, torch.float32),
-                     ("acc1", U, torch.float32), ("racc", E, torch.float32)],
+                     ("acc1", U, torch.float32), ("racc", E, torch.float32),
+                     ("gb0", U, torch.bfloat16), ("gb1", U, torch.bfloat16)],
                     gname, dev, rank, self.N, ctas=symm_ctas)
             except Exception as e:            # e.g. no peer mapping on this fabric
                 err = f"{type(e).__name__}: {e}"
@@ -176,6 +180,9 @@ class UnevenFSDPTrainer:
         # overlap the next pair's backward); with one rank nothing overlaps, so the whole
         # backward's bf16 -> fp32 scale-cast is one launch (holds 2 B/param of bf16 grads)
         self.acc_group = self.L.blocks if self.N == 1 else 2
+        self.bf16_wire = bf16_wire
+        # Eq. 1 weights of every rank (the bf16-wire reduce-scatter applies them itself)
+        self.rank_weights = [a.microbatch / plan.total_batch for a in plan.assignments]
         self._set_routes(self.symm is not None)
         self.route_check = None
         if self.symm is not None and check_routes:
@@ -222,6 +229,11 @@ class UnevenFSDPTrainer:
                        (i + 1 == len(order) or self.rs_route[order[i + 1]] != "symm")
                        for i, u in enumerate(order)}
         self.need_shadow = not sym or "nccl" in self.ag_route
+        # l_i <= 1 on every rank: a fused-route unit's gradient crosses the wire as the
+        # unscaled bf16 microbatch gradient; the reduce-scatter applies w_j and the
+        # cast (het_symm_reduce_scatter_bf16), half the link bytes of the fp32 form
+        self.wire16 = [sym and self.bf16_wire and self.pair_units and u < self.L.blocks and
+                       self.rs_route[u] == "symm" for u in units]
         if self.pair_units:
             for u in range(self.L.blocks):
                 second = (self.L.blocks - 1 - u) % 2 == 1 or u == 0
@@ -260,6 +272,23 @@ class UnevenFSDPTrainer:
                 want = pattern(torch.arange(size, device=dev), 0).to(torch.bfloat16)
                 bad += int(not torch.equal(self.symm[ub][:size], want))
                 checked += 1
+            if rs and self.wire16[u]:        # bf16 wire: weights and cast in the RS
+                gb = self.symm["gb0"]
+                gb[:size].copy_(pattern(torch.arange(size, device=dev), self.rank))
+                out = torch.full((cnt,), float("nan"), device=dev)
+                torch.cuda.synchronize(dev)
+                self.symm.handle.barrier()
+                self.symm.reduce_scatter_bf16("gb0", 0, out, counts, offsets, self.rank_weights,
+                                              end_barrier=True, stream=self._current())
+                idx = torch.arange(lo, lo + cnt, device=dev)
+                want = torch.zeros(cnt, device=dev)
+                for r, w in enumerate(self.rank_weights):
+                    if w != 0.0:
+                        want = want + torch.tensor(w, dtype=torch.float32, device=dev) * \
+                            pattern(idx, r)
+                bad += int(not torch.equal(out, want))
+                checked += 1
+                gb.zero_()
             if rs:
                 self.symm[acc][:size].copy_(pattern(torch.arange(size, device=dev), self.rank))
                 out = torch.full((cnt,), float("nan"), device=dev)
@@ -275,7 +304,7 @@ class UnevenFSDPTrainer:
         status = K.SymmWorkspace.status(reset=True)
         failures = _sum_ranks(bad + (1 if status else 0), dev)
         self.symm.handle.barrier()
-        for name in ("ub0", "acc0", "rbuf", "racc"):
+        for name in ("ub0", "acc0", "rbuf", "racc", "gb0"):
             self.symm[name].zero_()
         torch.cuda.synchronize(dev)
         self.symm.handle.barrier()
@@ -410,7 +439,12 @@ class UnevenFSDPTrainer:
         return self._event(self.rs_stream)
 
     def _rs_issue(self, u: int, src: torch.Tensor) -> None:
-        if self.rs_route[u] == "symm":   # switch/peer reduction straight into the fp32 shard
+        if self.wire16[u]:               # bf16 wire: weighting + cast inside the RS
+            self.symm.reduce_scatter_bf16(f"gb{u % 2}", 0, self._local(self.g32, u),
+                                          self.L.counts[u], self.L.offsets[u], self.rank_weights,
+                                          end_barrier=self.rs_end[u], stream=self.rs_stream)
+            self.launches += 1
+        elif self.rs_route[u] == "symm":   # switch/peer reduction straight into the fp32 shard
             self.symm.reduce_scatter(self._region(src), 0, self._local(self.g32, u),
                                      self.L.counts[u], self.L.offsets[u],
                                      end_barrier=self.rs_end[u], stream=self.rs_stream)
@@ -443,7 +477,27 @@ class UnevenFSDPTrainer:
         return a0.as_strided((span,), (1,), a0.storage_offset()), off
 
     def _accumulate_units(self, items, names, seg):
-        """One het_accumulate (FIRST) over [(u, grads), ...] of several units."""
+        """One het_accumulate (FIRST) over [(u, grads), ...] of several units; units
+        on the bf16 wire are staged unscaled into their bf16 buffer instead."""
+        w16 = [(u, g) for u, g in items if self.wire16[u]]
+        items = [(u, g) for u, g in items if not self.wire16[u]]
+        if w16:
+            stage = []
+            for u, grads in w16:
+                off = (self.symm[f"gb{u % 2}"].data_ptr() - self.symm["gb0"].data_ptr()) // 2
+                stage += [(g, off + seg[nm]) for g, nm in zip(grads, names)]
+            n16 = sum(g.numel() for g, _ in stage)
+            gb = self.symm["gb0"]
+            span = (self.symm["gb1"].data_ptr() - gb.data_ptr()) // 2 + self.symm["gb1"].numel()
+            a, b = self.timers.pair("gather", n16 * 4.0)
+            if a is not None:
+                a.record()
+            K.gather_bf16(gb.as_strided((span,), (1,), gb.storage_offset()), stage)
+            if b is not None:
+                b.record()
+            self.launches += 1
+        if not items:
+            return
         base = None
         pairs = []
         n = 0

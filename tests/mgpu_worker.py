@@ -83,7 +83,8 @@ def main(out_dir: str) -> None:
         # fused symmetric-memory collectives (NVLS multicast when available, then peer)
         maxu = max(sum(c) for c in shard_cases(world)) + 64
         for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO)):
-            ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32)],
+            ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32),
+                                  ("g16", maxu, torch.bfloat16)],
                                  dist.group.WORLD.group_name, dev, rank, world,
                                  use_multicast=use_mc, policy=policy)
             use_mc = f"{int(use_mc)}{policy}"
@@ -109,6 +110,24 @@ def main(out_dir: str) -> None:
                 torch.cuda.synchronize()
                 report[f"symm_rs{ci}_{use_mc}"] = float(
                     max_rel(out.cpu().numpy(), want) if counts[rank] else 0.0)
+                # bf16 wire: unscaled bf16 gradients, Eq. 1 weights applied in the RS;
+                # expected = sum_j fl32(w_j * g_j) in rank order (IEEE fp32 in numpy)
+                wts = [0.0 if r == 1 and world > 2 else (r + 1) / (world * (world + 1) / 2)
+                       for r in range(world)]
+                g16 = [torch.from_numpy(x).to(torch.bfloat16) for x in srcs]
+                ws["g16"][:total].copy_(g16[rank].to(dev))
+                want16 = np.zeros(total, np.float32)
+                for r in range(world):
+                    if wts[r] != 0.0:
+                        want16 = want16 + np.float32(wts[r]) * g16[r].float().numpy()
+                lo = offs[rank]
+                out16 = torch.empty(counts[rank], dtype=torch.float32, device=dev)
+                torch.cuda.synchronize()
+                dist.barrier()
+                ws.reduce_scatter_bf16("g16", 0, out16, counts, offs, wts, end_barrier=True)
+                torch.cuda.synchronize()
+                report[f"bf16wire_rs{ci}_{use_mc}"] = int(np.array_equal(
+                    out16.cpu().numpy(), want16[lo:lo + counts[rank]]))
             report[f"symm_status_{use_mc}"] = float(K.SymmWorkspace.status(reset=True))
             dist.barrier()
             del ws
@@ -154,6 +173,26 @@ def main(out_dir: str) -> None:
         gs = [t.cpu().numpy() for t in trs.full_units("g32")]
         ps = [t.cpu().numpy() for t in trs.full_units("p32")]
         report["symm_status_step"] = float(K.SymmWorkspace.status(reset=True))
+        # l_i <= 1 on every rank: the bf16-wire reduce-scatter against the fp32 one
+        pmicro = [(3, 1), (2, 1), (1, 1), (0, 0)][:world] if world > 2 else [(3, 1), (2, 1)]
+        pB = sum(m * l for m, l in pmicro)
+        pmodel = ModelSpec(arch.layers, arch.unit_params, pB)
+        pplan = TrainPlan(tuple(GpuAssignment(f"g{i}", m, l, m * l, r, 0.0, r * pmodel.state_bytes)
+                                for i, ((m, l), r) in enumerate(zip(pmicro, ratios))),
+                          1.0, 1.0, 2.0 * arch.layers, True, assign_unit_shards(ratios, pmodel))
+        ptok = torch.from_numpy(rank_tokens(pplan, rank, arch.seq, arch.vocab, seed=13,
+                                            step=0)).to(dev)
+        pair = {}
+        for wire in (True, False):
+            t2 = UnevenFSDPTrainer(arch, pplan, rank, comm_ag=cag, comm_rs=crs, device=dev,
+                                   algo=K.ALGO_SYMM, bf16_wire=wire)
+            t2.load_full_units(units)
+            if wire:
+                report["bf16_wire_units"] = float(sum(t2.wire16))
+            t2.step(ptok)
+            pair[wire] = [t.cpu().numpy() for t in t2.full_units("g32")]
+            del t2
+        report["symm_status_pair"] = float(K.SymmWorkspace.status(reset=True))
         torch.cuda.synchronize()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), loss=float(loss),
                  micro=np.array(micro), ratios=np.array(ratios),
@@ -162,7 +201,10 @@ def main(out_dir: str) -> None:
                  loss_symm=float(loss_s),
                  **{f"g{u}": x for u, x in enumerate(g)}, **{f"p{u}": x for u, x in enumerate(p)},
                  **{f"gs{u}": x for u, x in enumerate(gs)},
-                 **{f"ps{u}": x for u, x in enumerate(ps)})
+                 **{f"ps{u}": x for u, x in enumerate(ps)},
+                 **{f"gw{u}": x for u, x in enumerate(pair[True])},
+                 **{f"gf{u}": x for u, x in enumerate(pair[False])},
+                 pmicro=np.array(pmicro))
     finally:
         cag.close()
         crs.close()

@@ -47,6 +47,10 @@ def test_multigpu_collectives_and_step(tmp_path):
                 assert v <= FP32_RTOL, f"reduce-scatter {k}: {v}"
             elif k.startswith("symm_status"):
                 assert v == 0.0, f"symmetric barrier timed out ({k})"
+            elif k.startswith("bf16wire_rs"):
+                assert v == 1.0, f"bf16-wire reduce-scatter {k} not bit-exact vs the fp32 sum"
+            elif k == "bf16_wire_units":
+                assert v > 0, "the l<=1 plan did not use the bf16-wire reduce-scatter"
             elif k == "symm_route_check_ok":
                 assert v == 1.0, "fused collectives failed their startup known-answer check"
             elif k == "trace_lint_problems":
@@ -84,3 +88,19 @@ def test_multigpu_collectives_and_step(tmp_path):
         rps, _, _ = SO.adamw(units[u].numpy(), gs, z, z, step=1, **opt)
         assert max_rel(r[0][f"ps{u}"], rps) <= FP32_RTOL
     assert abs(float(r[0]["loss_symm"]) - float(r[0]["loss"])) <= 1e-5 * abs(loss)
+    # l_i <= 1 plan: bf16-wire reduce-scatter (weights + cast inside the RS) against the
+    # fp32-wire route and the CPU oracle
+    pmicro = [tuple(int(x) for x in mi) for mi in r[0]["pmicro"]]
+    pB = sum(m * l for m, l in pmicro)
+    pmodel = ModelSpec(arch.layers, arch.unit_params, pB)
+    pplan = TrainPlan(tuple(GpuAssignment(f"g{i}", m, l, m * l, rr, 0.0, rr * pmodel.state_bytes)
+                            for i, ((m, l), rr) in enumerate(zip(pmicro, ratios))),
+                      1.0, 1.0, 2.0 * arch.layers, True, assign_unit_shards(ratios, pmodel))
+    ptoks = [rank_tokens(pplan, i, arch.seq, arch.vocab, seed=13, step=0) for i in range(world)]
+    plive = [(t, mi) for t, mi in zip(ptoks, pmicro) if mi[0] > 0]
+    pgu, pgr, _ = MO.weighted_gradient(arch, units[:-1], units[-1], [t for t, _ in plive],
+                                       [mi for _, mi in plive])
+    for u, ref in enumerate(pgu + [pgr]):
+        gw, gf = r[0][f"gw{u}"], r[0][f"gf{u}"]
+        assert norm_rel(gw, gf) <= 1e-6, f"bf16 wire vs fp32 wire, unit {u}"
+        assert norm_rel(gw, ref.numpy()) <= BF16_GRAD_RTOL, f"bf16 wire vs oracle, unit {u}"
