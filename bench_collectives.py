@@ -31,7 +31,8 @@ from paper_2411_01075_b200 import hetstep as K  # noqa: E402
 from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
-         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route"}
+         "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route",
+         "symm_bf16wire": "symm_bf16wire"}
 SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
         "symm_peer": (False, K.SYMM_PEER)}
 
@@ -109,9 +110,11 @@ def main() -> None:
     maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
     ws = {}
     for an, (mc, policy) in SYMM.items():
-        if an in args.algos or (an == "symm" and "route" in args.algos):
+        if an in args.algos or (an == "symm" and ("route" in args.algos or
+                                                "symm_bf16wire" in args.algos)):
             ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
-                                                                         torch.float32)],
+                                                                         torch.float32),
+                                      ("g16", maxel // 2 + 64, torch.bfloat16)],
                                      dist.group.WORLD.group_name, dev, rank, world,
                                      ctas=args.ctas, use_multicast=mc, policy=policy)
             if rank == 0:
@@ -136,7 +139,15 @@ def main() -> None:
                             pick = K.route_collective("ag" if op == "allgather" else "rs", c,
                                                       world, "symm" in ws)
                             algo = "symm" if pick == "symm" else K.ALGO_AUTO
-                        if isinstance(algo, str):
+                        if algo == "symm_bf16wire":
+                            if op != "reduce_scatter":
+                                continue
+                            w = ws["symm"]
+                            w["g16"][:total].normal_()
+                            out = torch.empty(c[rank], device=dev)
+                            wts = [1.0 / world] * world
+                            fn = lambda: w.reduce_scatter_bf16("g16", 0, out, c, o, wts)  # noqa: E731
+                        elif isinstance(algo, str):
                             w = ws[algo]
                             if op == "allgather":
                                 src32 = torch.randn(c[rank], device=dev)
@@ -154,6 +165,7 @@ def main() -> None:
                             out = torch.empty(c[rank], device=dev)
                             fn = lambda: K.reduce_scatter_uneven(src, out, c, o, comm, rank, algo)  # noqa: E731
                         ms = time_op(fn, args.iters, args.warmup)
+                        # bus bytes of the fp32 result (the bf16 wire moves half of them)
                         S = total * esize
                         ingest = max(S - x * esize for x in c)
                         bus = ingest / (ms * 1e-3) / 1e9
