@@ -38,8 +38,11 @@ def full_summary(rep: str, algo_bytes: dict[str, float], config: str) -> dict:
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
         key = ("het_adamw" if "adamw" in name
-               else "het_accumulate_first" if "accumulate_kernel<1>" in name
+               else "het_accumulate_first" if "accumulate_kernel<1" in name
                else "het_accumulate" if "accumulate" in name
+               else "het_gather_bf16" if "gather_bf16" in name
+               else "het_bias_grad" if "colsum_kernel<" in name and "BiasOnly" in name
+               else "het_gelu_bwd_bias" if "colsum_kernel<" in name and "GeluBwd" in name
                else "het_pack" if "pack" in name else name.split("(")[0])
         rec = {}
         for m in METRICS:
@@ -82,14 +85,18 @@ def launch_shares(path: str) -> tuple[str, dict]:
         cnt[key] += 1
     T = sum(tot.values())
     owned = {k: v for k, v in tot.items() if "adamw" in k or "accumulate" in k or "pack" in k
-             or "fill_kernel" in k}
+             or "fill_kernel" in k or "gather_bf16" in k or "symm_" in k}
+    model_side = {k: v for k, v in tot.items() if any(t in k for t in (
+        "ln_", "rms_", "xent", "rope", "swiglu", "colsum", "gelu_fwd", "embedding_grad"))}
     nccl = {k: v for k, v in tot.items() if "nccl" in k.lower()}
     lines = ["| share | total us | launches | kernel |", "|---:|---:|---:|---|"]
     for k, v in tot.most_common(30):
         lines.append(f"| {v / T * 100:.2f}% | {v / 1e3:.1f} | {cnt[k]} | `{k}` |")
     stats = {"step_kernels": e - s, "step_device_us": T / 1e3,
              "owned_share": sum(owned.values()) / T, "nccl_share": sum(nccl.values()) / T,
-             "owned": {k: v / T for k, v in owned.items()}}
+             "owned": {k: v / T for k, v in owned.items()},
+             "model_side_share": sum(model_side.values()) / T,
+             "model_side": {k: v / T for k, v in model_side.items()}}
     return "\n".join(lines), stats
 
 

@@ -79,6 +79,28 @@ def test_step_weighting_exact_without_noise():
         assert max_rel(red, H.weighted_combine(rounded, b)) <= FP32_RTOL
 
 
+def test_bf16_wire_reduce_scatter_is_eq1():
+    """The bf16-wire reduce-scatter (weights and cast inside the RS) equals the
+    fp32-accumulate route bit for bit (same fl(w g) products, same rank-order
+    sums) and the reference formula to fp32 precision."""
+    g = json.loads((GOLD / "weighted_combine.json").read_text())
+    for c in g["cases"]:
+        b, B = c["batches"], sum(c["batches"])
+        bits = [O.bf16_bits(np.asarray(m, np.float32)) for m in c["means"]]
+        w = [bi / B for bi in b]
+        dim = len(c["means"][0])
+        counts = [dim // 2, dim - dim // 2]
+        offs = [0, counts[0]]
+        got = np.concatenate(O.reduce_scatter_bf16(bits, w, counts, offs))
+        accs = [O.accumulate(None, q, True, wi) for q, wi in zip(bits, w)]
+        fp32 = np.zeros(dim, np.float32)
+        for a in accs:
+            fp32 = fp32 + a
+        assert np.array_equal(got, fp32)
+        ref = H.weighted_combine([O.bf16_to_f32(q).astype(np.float64) for q in bits], b)
+        assert max_rel(got, ref) <= FP32_RTOL
+
+
 def test_rs_scale_is_eq1():
     plan = H.TrainPlan(tuple(H.GpuAssignment(f"g{i}", m, l, m * l, r, 0.0, 0.0)
                              for i, (m, l, r) in enumerate([(3, 2, 0.5), (1, 4, 0.5), (0, 0, 0.0)])),
