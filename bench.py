@@ -209,6 +209,13 @@ def run_reference(args) -> None:
 
 
 
+def tier_capacity(job, no_emulate: bool) -> float:
+    from paper_2411_01075_b200.configs import TIERS
+    if no_emulate:
+        return float(len(job.cluster.gpus))
+    return float(sum(TIERS[g.profile_key][0] for g in job.cluster.gpus))
+
+
 def route_summary(tr) -> dict | str:
     """Which collective route each unit took and the fused kernels' startup
     known-answer check (step._check_symm_routes)."""
@@ -356,6 +363,9 @@ def main() -> None:
                        "planner_predicted_iteration_ms": plan.predicted_iteration_ms,
                        "parallelism": f"uneven-fsdp{world}",
                        "emulation_rank0": emu.describe(),
+                       # sum over ranks of the emulated tiers' SM fractions (N=1: 1.0);
+                       # value / tier_capacity is the throughput per full-B200 equivalent
+                       "tier_capacity": tier_capacity(job, args.no_emulate),
                        "collectives": route_summary(tr),
                        "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",

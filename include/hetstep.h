@@ -120,6 +120,13 @@ int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* r
 /* Rotary position embedding in place on bf16 [rows, heads, dh] (row r at
  * position r % seq, rotate-half pairs); inverse=1 applies the backward
  * (inverse) rotation. */
+/* Cross-entropy loss and gradient in one pass (the head's upstream gradient
+ * is known: grad_scale, normally 1): loss[r] = logsumexp(row) - row[target],
+ * and the row is overwritten in place with grad_scale/rows * (softmax - onehot).
+ * vocab % 8 == 0, vocab <= 65536. */
+int het_xent_fused(void* logits, const int64_t* target, int64_t rows, int64_t vocab,
+                   float grad_scale, float* loss, void* stream);
+
 /* Residual add fused into the norms: xsum = bf16(x + r) is written and
  * normalised (forward); the backward adds the residual path's gradient dres
  * to the norm's input gradient in the same pass (dres may be NULL). */

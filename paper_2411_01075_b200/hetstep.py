@@ -31,7 +31,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
            "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace",
            "het_swiglu_fwd", "het_swiglu_bwd", "het_rope_qkv_split", "het_rope_qkv_merge",
-           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_rmsnorm_add_fwd",
+           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_xent_fused", "het_rmsnorm_add_fwd",
            "het_rmsnorm_bwd_add", "het_colsum_partial_floats", "het_bias_grad",
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
@@ -79,6 +79,7 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_rmsnorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
         "het_rope_inplace": ([vp, i64, i32, i32, i64, i32, vp], i32),
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
+        "het_xent_fused": ([vp, vp, i64, i64, f32, vp, vp], i32),
         "het_swiglu_fwd": ([vp, vp, i64, vp, i64, i64, vp], i32),
         "het_rope_qkv_split": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
         "het_layernorm_add_fwd": ([vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
@@ -328,6 +329,20 @@ class CrossEntropyFn(torch.autograd.Function):
         _check(load().het_xent_bwd(lg.data_ptr(), tgt.data_ptr(), rows, vocab, lse.data_ptr(),
                                    g.data_ptr(), lg.data_ptr(), _stream(None)), "het_xent_bwd")
         return lg, None
+
+
+def xent_value_and_grad(logits: torch.Tensor, target: torch.Tensor,
+                        grad_scale: float = 1.0) -> torch.Tensor:
+    """Mean cross-entropy of bf16 [rows, vocab] logits AND its gradient in one
+    pass: returns the loss (device scalar) and overwrites `logits` in place with
+    grad_scale * d(mean loss)/d(logits)."""
+    rows, vocab = logits.shape
+    tgt = target.reshape(-1).to(torch.int64).contiguous()
+    loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    _check(load().het_xent_fused(_cuda(logits, torch.bfloat16, "logits"), tgt.data_ptr(), rows,
+                                 vocab, float(grad_scale), loss.data_ptr(), _stream(None)),
+           "het_xent_fused")
+    return loss.mean()
 
 
 RMS_DIMS = (256, 768, 1024, 2048)

@@ -222,6 +222,29 @@ def embed_forward(arch: ArchSpec, p: dict[str, torch.Tensor], tokens: torch.Tens
     return x
 
 
+def head_value_and_grad(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor,
+                        targets: torch.Tensor, wrt: list[torch.Tensor]):
+    """Mean next-token loss of one microbatch and its gradients w.r.t. `wrt`
+    (head parameters and the head input). On CUDA the loss and dlogits come
+    from one fused pass over the logits (het_xent_fused), written over the
+    logits in place, and autograd takes it from the logits GEMM down."""
+    with torch.enable_grad():
+        if arch.kind == "llama":
+            h = (_K.rms_norm(x, p["normf"]) if x.is_cuda and x.dtype == torch.bfloat16 and
+                 x.shape[-1] in _K.RMS_DIMS else _rms(x, p["normf"]))
+        else:
+            h = _ln(x, p["lnf_w"], p["lnf_b"])
+        logits = h @ p["wte"].t()
+        flat = logits.view(-1, logits.shape[-1])
+        if flat.is_cuda and flat.dtype == torch.bfloat16 and flat.shape[-1] % 8 == 0 and \
+                flat.shape[-1] <= 65536:
+            loss = _K.xent_value_and_grad(flat.detach(), targets.reshape(-1))
+            # the matmul's backward keeps h and wte, not the logits: their buffer is free
+            return loss, torch.autograd.grad(logits, wrt, logits.detach())
+        loss = F.cross_entropy(flat, targets.reshape(-1).long())
+        return loss.detach(), torch.autograd.grad(loss, wrt)
+
+
 def head_loss(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor,
               targets: torch.Tensor) -> torch.Tensor:
     """Mean next-token cross-entropy of one microbatch (tied LM head)."""

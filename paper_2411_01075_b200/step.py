@@ -40,7 +40,8 @@ import torch
 from . import hetstep as K
 from .core import InputError, TrainPlan
 from .layout import RankLayout
-from .model import ArchSpec, block_forward, embed_forward, head_loss, init_flat, segment_offsets, views
+from .model import (ArchSpec, block_forward, embed_forward, head_value_and_grad, init_flat,
+                    segment_offsets, views)
 
 
 @dataclass(frozen=True)
@@ -603,9 +604,8 @@ class UnevenFSDPTrainer:
                     # head + loss of microbatch k right behind the last unit's forward
                     with self._span("head", root, k + 1, "fwd", comp):
                         y.requires_grad_(True)
-                        with torch.enable_grad():
-                            lk = head_loss(arch, leaves, y, mb[k][1])
-                            grads = torch.autograd.grad(lk, [leaves[nm] for nm in head_names] + [y])
+                        lk, grads = head_value_and_grad(arch, leaves, y, mb[k][1],
+                                                        [leaves[nm] for nm in head_names] + [y])
                         self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
                         loss += lk.detach() * self.w
                     if deep:
