@@ -151,6 +151,8 @@ def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
 # residual add fused into the following norm (hetstep.add_layer_norm / add_rms_norm);
 # a switch so tools/ab_step.py can A/B it on the same box
 FUSE_RESIDUAL_NORM = True
+# cross-entropy loss and gradient in one pass over the logits (het_xent_fused)
+FUSE_XENT = True
 
 
 def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -> torch.Tensor:
@@ -236,12 +238,15 @@ def head_value_and_grad(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Ten
             h = _ln(x, p["lnf_w"], p["lnf_b"])
         logits = h @ p["wte"].t()
         flat = logits.view(-1, logits.shape[-1])
-        if flat.is_cuda and flat.dtype == torch.bfloat16 and flat.shape[-1] % 8 == 0 and \
-                flat.shape[-1] <= 65536:
+        if FUSE_XENT and flat.is_cuda and flat.dtype == torch.bfloat16 and \
+                flat.shape[-1] % 8 == 0 and flat.shape[-1] <= 65536:
             loss = _K.xent_value_and_grad(flat.detach(), targets.reshape(-1))
             # the matmul's backward keeps h and wte, not the logits: their buffer is free
             return loss, torch.autograd.grad(logits, wrt, logits.detach())
-        loss = F.cross_entropy(flat, targets.reshape(-1).long())
+        if flat.is_cuda and flat.dtype == torch.bfloat16 and flat.shape[-1] % 8 == 0:
+            loss = _K.cross_entropy(flat, targets.reshape(-1))
+        else:
+            loss = F.cross_entropy(flat, targets.reshape(-1).long())
         return loss.detach(), torch.autograd.grad(loss, wrt)
 
 

@@ -36,6 +36,8 @@ tok = torch.from_numpy(rank_tokens(job.plan, 0, job.arch.seq, job.arch.vocab, 1,
 def setting(on: bool) -> None:
     if args.switch == "fuse_residual_norm":
         M.FUSE_RESIDUAL_NORM = on
+    elif args.switch == "fuse_xent":
+        M.FUSE_XENT = on
     elif args.switch == "acc_group":
         tr.acc_group = tr.L.blocks if on else 2
     else:
