@@ -151,8 +151,11 @@ def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
 # residual add fused into the following norm (hetstep.add_layer_norm / add_rms_norm);
 # a switch so tools/ab_step.py can A/B it on the same box
 FUSE_RESIDUAL_NORM = True
-# cross-entropy loss and gradient in one pass over the logits (het_xent_fused)
-FUSE_XENT = True
+# cross-entropy loss and gradient in one pass over the logits (het_xent_fused). Off:
+# measured 0.4-0.5% slower per step than the two-kernel pair (tools/ab_step.py), as
+# its register-resident rows allow one CTA per SM and the read and write phases of
+# a CTA do not overlap
+FUSE_XENT = False
 
 
 def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -> torch.Tensor:

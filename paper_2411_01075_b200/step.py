@@ -205,6 +205,7 @@ class UnevenFSDPTrainer:
         self.timers = StepTimers()
         self.launches = 0          # owned-kernel launches (hetstep.so), this process
         self.tracer = None         # trace.StepTracer: per-event CUDA timelines when set
+        self.keep_last_graph = True  # l_i = 1: keep the last unit's forward graph (no recompute)
         # activation checkpoint offload (schedule sim.py:226-338):
         # unit-boundary checkpoints go to pinned host memory on a D2H stream after the
         # forward uses them and come back one unit ahead of their recompute on an H2D stream
@@ -560,6 +561,11 @@ class UnevenFSDPTrainer:
         nmb = len(mb)
         off = self.offload and nmb > 0
         deep = off and nmb >= 2
+        # one microbatch, no offload: the last unit's forward runs with autograd and its
+        # graph is kept for the backward, which follows right after the head (its
+        # recompute would redo exactly that forward)
+        keep_last = self.keep_last_graph and nmb == 1 and not off
+        kept = None
         h: list[list[torch.Tensor | None]] = [[None] * (nb + 1) for _ in mb]
         dy: list[torch.Tensor | None] = [None] * nmb
         fetched: dict[tuple[str, int, int], tuple] = {}
@@ -590,8 +596,17 @@ class UnevenFSDPTrainer:
                         nk, nu = (k + 1, u) if k + 1 < nmb else (0, u + 1)
                         if 1 <= nu < nb:
                             fetched[("act", nk, nu)] = self._fetch("act", nk, nu, "fwd")
-                    with self._span("fwd_compute", u, k + 1, "fwd", comp):
-                        y = block_forward(arch, p, x)
+                    if keep_last and u == nb - 1:
+                        pk = {nm: t.requires_grad_(True) for nm, t in
+                              views(self._unit_flat(u), arch.unit_layout()).items()}
+                        with self._span("fwd_compute", u, k + 1, "fwd", comp):
+                            x = x.requires_grad_(True)
+                            with torch.enable_grad():
+                                y = block_forward(arch, pk, x)
+                        kept = (x, y, [pk[nm] for nm in unit_names])
+                    else:
+                        with self._span("fwd_compute", u, k + 1, "fwd", comp):
+                            y = block_forward(arch, p, x)
                     if off and (u == 0 or not deep):
                         self._offload("act", k, u, x, comp, u, "fwd")   # recompute input
                     h[k][u] = None if off else x
@@ -603,7 +618,8 @@ class UnevenFSDPTrainer:
                         continue
                     # head + loss of microbatch k right behind the last unit's forward
                     with self._span("head", root, k + 1, "fwd", comp):
-                        y.requires_grad_(True)
+                        if not y.requires_grad:
+                            y.requires_grad_(True)
                         lk, grads = head_value_and_grad(arch, leaves, y, mb[k][1],
                                                         [leaves[nm] for nm in head_names] + [y])
                         self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
@@ -660,10 +676,15 @@ class UnevenFSDPTrainer:
                         fetched[("act", nk, nu)] = self._fetch("act", nk, nu, "bwd")
                 else:
                     x = h[k][u]
-                with self._span("recompute", u, k + 1, "bwd", comp):
-                    x = x.requires_grad_(True)
-                    with torch.enable_grad():
-                        y = block_forward(arch, pl, x)
+                if kept is not None and u == nb - 1:
+                    x, y, plist_u = kept             # graph kept from the forward
+                    kept = None
+                else:
+                    plist_u = plist
+                    with self._span("recompute", u, k + 1, "bwd", comp):
+                        x = x.requires_grad_(True)
+                        with torch.enable_grad():
+                            y = block_forward(arch, pl, x)
                 if deep:
                     g_in = self._take(fetched.pop(("grad", k, u)), comp)
                     if nu >= 0:                   # next upstream gradient (at B start)
@@ -671,7 +692,7 @@ class UnevenFSDPTrainer:
                 else:
                     g_in = dy[k]
                 with self._span("bwd_compute", u, k + 1, "bwd", comp):
-                    grads = torch.autograd.grad(y, plist + [x], g_in)
+                    grads = torch.autograd.grad(y, plist_u + [x], g_in)
                     h[k][u] = dy[k] = None
                     if self.pair_units:
                         unit_grads = list(grads[:-1])
