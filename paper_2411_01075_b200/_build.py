@@ -61,6 +61,11 @@ def step_sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
+def _cublas_root() -> Path:
+    import nvidia.cublas  # torch's cuBLAS wheel (cuBLASLt for the epilogue GEMMs)
+    return Path(list(nvidia.cublas.__path__)[0])
+
+
 def build_step(force: bool = False, verbose: bool = False) -> Path:
     srcs = step_sources()
     if not (force or _stale(STEP_LIB, srcs)):
@@ -73,6 +78,8 @@ def build_step(force: bool = False, verbose: bool = False) -> Path:
            f"-I{INCLUDE}", f"-I{nccl / 'include'}",
            *[str(s) for s in srcs if s.suffix == ".cu"],
            f"-L{nccl / 'lib'}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={nccl / 'lib'}",
+           f"-L{_cublas_root() / 'lib'}", "-l:libcublasLt.so.12",
+           "-Xlinker", f"-rpath={_cublas_root() / 'lib'}",
            "-o", str(tmp)]
     _run(cmd)
     os.replace(tmp, STEP_LIB)

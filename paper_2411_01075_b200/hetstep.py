@@ -31,7 +31,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
            "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace",
            "het_swiglu_fwd", "het_swiglu_bwd", "het_rope_qkv_split", "het_rope_qkv_merge",
-           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_xent_fused", "het_rmsnorm_add_fwd",
+           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_xent_fused", "het_lt_matmul", "het_rmsnorm_add_fwd",
            "het_rmsnorm_bwd_add", "het_colsum_partial_floats", "het_bias_grad",
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
@@ -80,6 +80,8 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_rope_inplace": ([vp, i64, i32, i32, i64, i32, vp], i32),
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
         "het_xent_fused": ([vp, vp, i64, i64, f32, vp, vp], i32),
+        "het_lt_matmul": ([i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp, vp, i64,
+                           vp, i64, vp], i32),
         "het_swiglu_fwd": ([vp, vp, i64, vp, i64, i64, vp], i32),
         "het_rope_qkv_split": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
         "het_layernorm_add_fwd": ([vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
@@ -592,6 +594,120 @@ class LinearGeluFn(torch.autograd.Function):
         dx = (dpre @ w).view(x.shape) if ctx.needs_input_grad[0] else None
         dw = dpre.t() @ x.reshape(-1, x.shape[-1])
         return dx, dw, db
+
+
+LT_NONE, LT_BIAS, LT_GELU_BIAS, LT_GELU_AUX_BIAS, LT_DGELU_BGRAD, LT_BGRADB = range(6)
+_LT_WS: dict = {}
+_LT_WS_BYTES = 32 << 20
+
+
+def _lt_workspace(device) -> torch.Tensor:
+    ws = _LT_WS.get(device)
+    if ws is None:
+        ws = _LT_WS[device] = torch.empty(_LT_WS_BYTES, dtype=torch.uint8, device=device)
+    return ws
+
+
+def lt_matmul(ta: int, tb: int, m: int, n: int, k: int, a: torch.Tensor, lda: int,
+              b: torch.Tensor, ldb: int, d: torch.Tensor, ldd: int, epilogue: int = LT_NONE,
+              bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
+              ldaux: int = 0) -> None:
+    """het_lt_matmul (cuBLASLt GEMM + fused epilogue), column-major arguments."""
+    ws = _lt_workspace(d.device)
+    _check(load().het_lt_matmul(ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
+                                d.data_ptr(), ldd, epilogue,
+                                None if bias is None else bias.data_ptr(),
+                                None if aux is None else aux.data_ptr(), ldaux, ws.data_ptr(),
+                                _LT_WS_BYTES, _stream(None)), "het_lt_matmul")
+
+
+def _rows(x: torch.Tensor) -> torch.Tensor:
+    x2 = x.reshape(-1, x.shape[-1])
+    return x2 if x2.is_contiguous() else x2.contiguous()
+
+
+def _lt_forward(x2, w, b, epilogue, aux=None):
+    """y[M, N] = x2[M, K] W[N, K]^T + b with the epilogue (row-major views)."""
+    M, K = x2.shape
+    N = w.shape[0]
+    y = torch.empty(M, N, dtype=torch.bfloat16, device=x2.device)
+    lt_matmul(1, 0, N, M, K, w, K, x2, K, y, N, epilogue, b, aux, N if aux is not None else 0)
+    return y
+
+
+def _lt_wgrad(x2, g2, with_bias: bool):
+    """dW[N, K] = g2^T x2 (+ db[N] = column sums of g2 from the same GEMM)."""
+    M, K = x2.shape
+    N = g2.shape[1]
+    dw = torch.empty(N, K, dtype=torch.bfloat16, device=x2.device)
+    db = torch.empty(N, dtype=torch.bfloat16, device=x2.device) if with_bias else None
+    lt_matmul(0, 1, K, N, M, x2, K, g2, N, dw, K, LT_BGRADB if with_bias else LT_NONE, db)
+    return dw, db
+
+
+class LtLinearFn(torch.autograd.Function):
+    """y = x W^T + b: cuBLASLt bias epilogue forward; the weight-gradient GEMM
+    also produces the bias gradient (BGRADB epilogue), so no reduction pass."""
+
+    @staticmethod
+    def forward(ctx, x, w, b):
+        x2 = _rows(x)
+        ctx.save_for_backward(x2, w)
+        ctx.shape = x.shape
+        return _lt_forward(x2, w, b, LT_BIAS).view(*x.shape[:-1], w.shape[0])
+
+    @staticmethod
+    def backward(ctx, g):
+        x2, w = ctx.saved_tensors
+        g2 = _rows(g)
+        dx = (g2 @ w).view(ctx.shape) if ctx.needs_input_grad[0] else None
+        dw, db = _lt_wgrad(x2, g2, True)
+        return dx, dw, db
+
+
+class LtMLPFn(torch.autograd.Function):
+    """out = gelu_tanh(x W1^T + b1) W2^T + b2 with every elementwise pass inside
+    the GEMMs: GELU+bias (+ the pre-activation) in the up-projection, bias in
+    the down-projection; backward: fc2's weight GEMM gives db2 (BGRADB), fc2's
+    input-gradient GEMM applies GELU' and gives db1 (DGELU_BGRAD)."""
+
+    @staticmethod
+    def forward(ctx, x, w1, b1, w2, b2):
+        x2 = _rows(x)
+        M, f = x2.shape[0], w1.shape[0]
+        pre = torch.empty(M, f, dtype=torch.bfloat16, device=x.device)
+        y = _lt_forward(x2, w1, b1, LT_GELU_AUX_BIAS, pre)
+        out = _lt_forward(y, w2, b2, LT_BIAS)
+        ctx.save_for_backward(x2, w1, w2, y, pre)
+        ctx.shape = x.shape
+        return out.view(*x.shape[:-1], w2.shape[0])
+
+    @staticmethod
+    def backward(ctx, g):
+        x2, w1, w2, y, pre = ctx.saved_tensors
+        g2 = _rows(g)
+        M, d = g2.shape
+        f = w1.shape[0]
+        dw2, db2 = _lt_wgrad(y, g2, True)
+        dpre = torch.empty(M, f, dtype=torch.bfloat16, device=g.device)
+        db1 = torch.empty(f, dtype=torch.bfloat16, device=g.device)
+        lt_matmul(0, 0, f, M, d, w2, f, g2, d, dpre, f, LT_DGELU_BGRAD, db1, pre, f)
+        dw1 = dpre.t() @ x2
+        dx = (dpre @ w1).view(ctx.shape) if ctx.needs_input_grad[0] else None
+        return dx, dw1, db1, dw2, db2
+
+
+def lt_linear(x, w, b):
+    if not torch.is_grad_enabled():
+        return _lt_forward(_rows(x), w, b, LT_BIAS).view(*x.shape[:-1], w.shape[0])
+    return LtLinearFn.apply(x, w, b)
+
+
+def lt_mlp(x, w1, b1, w2, b2):
+    if not torch.is_grad_enabled():
+        y = _lt_forward(_rows(x), w1, b1, LT_GELU_BIAS)
+        return _lt_forward(y, w2, b2, LT_BIAS).view(*x.shape[:-1], w2.shape[0])
+    return LtMLPFn.apply(x, w1, b1, w2, b2)
 
 
 def linear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:

@@ -151,6 +151,9 @@ def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
 # residual add fused into the following norm (hetstep.add_layer_norm / add_rms_norm);
 # a switch so tools/ab_step.py can A/B it on the same box
 FUSE_RESIDUAL_NORM = True
+# GPT/BERT linears through cuBLASLt epilogue GEMMs (hetstep.lt_linear / lt_mlp: bias,
+# GELU and both bias gradients inside the GEMMs) instead of torch GEMMs + fused passes
+LT_EPILOGUES = True
 # cross-entropy loss and gradient in one pass over the logits (het_xent_fused). Off:
 # measured 0.4-0.5% slower per step than the two-kernel pair (tools/ab_step.py), as
 # its register-resident rows allow one CTA per SM and the read and write phases of
@@ -190,7 +193,8 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     # CUDA: linears with the fused bias-gradient column sum, and the MLP
     # up-projection + GELU as one epilogue GEMM (no-grad) / fused GELU passes
     fused = x.is_cuda and x.dtype == torch.bfloat16
-    lin = _K.linear if fused else F.linear
+    lt = fused and LT_EPILOGUES
+    lin = _K.lt_linear if lt else _K.linear if fused else F.linear
     h = _ln(x, p["ln1_w"], p["ln1_b"])
     # q/k/v as views of the fused projection in (b, s, H, dh) memory order: SDPA
     # (cuDNN) keeps that layout for its output, so neither the head split nor
@@ -204,6 +208,8 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     else:
         x = x + attn
         h = _ln(x, p["ln2_w"], p["ln2_b"])
+    if lt:
+        return x + _K.lt_mlp(h, p["fc_w"], p["fc_b"], p["fc2_w"], p["fc2_b"])
     if fused:
         h = _K.linear_gelu(h, p["fc_w"], p["fc_b"])
     else:

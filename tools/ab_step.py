@@ -38,6 +38,8 @@ def setting(on: bool) -> None:
         M.FUSE_RESIDUAL_NORM = on
     elif args.switch == "fuse_xent":
         M.FUSE_XENT = on
+    elif args.switch == "lt_epilogues":
+        M.LT_EPILOGUES = on
     elif args.switch == "keep_last":
         tr.keep_last_graph = on
     elif args.switch == "acc_group":
