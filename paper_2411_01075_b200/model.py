@@ -153,7 +153,7 @@ def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
 FUSE_RESIDUAL_NORM = True
 # GPT/BERT linears through cuBLASLt epilogue GEMMs (hetstep.lt_linear / lt_mlp: bias,
 # GELU and both bias gradients inside the GEMMs) instead of torch GEMMs + fused passes
-LT_EPILOGUES = True
+LT_EPILOGUES = False
 # cross-entropy loss and gradient in one pass over the logits (het_xent_fused). Off:
 # measured 0.4-0.5% slower per step than the two-kernel pair (tools/ab_step.py), as
 # its register-resident rows allow one CTA per SM and the read and write phases of
