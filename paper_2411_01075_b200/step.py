@@ -9,14 +9,18 @@ Schedule (the reference's executable spec, sim.py:342-368):
                          all l_i microbatches through unit u, keeping only
                          the unit-boundary activations (checkpoints; with
                          offload_activations they go to pinned host memory)
-       head: loss_k and dL/dh_L for every microbatch; root grads accumulate
+       head: loss_k and dL/dh_L of microbatch k right behind the last unit's
+       forward; root grads accumulate
   BWD  for u in L-1..0:  prefetch AG(u-1) (units L-1 and L-2 are still
                          resident from the forward: no re-gather)
-                         for each microbatch: recompute unit u, backward,
-                         het_accumulate(acc_u, grads, w = m_i/B)  (kernel 4;
-                         plans with l_i == 1 accumulate units in pairs)
-                         then RS(acc_u -> rank's fp32 grad shard)  [rs stream]
-       het_embedding_grad straight into the root accumulator, RS(root)
+                         for each microbatch: recompute unit u (skipped for
+                         the last unit when l_i == 1: its forward graph is
+                         kept), backward, het_accumulate(acc_u, grads,
+                         w = m_i/B)  (kernel 4; l_i <= 1 plans group units:
+                         pairs under collectives, the whole backward on one
+                         GPU) then RS(acc_u -> rank's fp32 grad shard)  [rs stream]
+                         unit 0's backward feeds het_embedding_grad straight
+                         into the root accumulator; RS(root)
   OPT  one het_adamw over the rank's whole flat shard (kernel 5), writing the
        bf16 shadow only when some unit's all-gather goes through NCCL
 
@@ -25,10 +29,13 @@ symmetric-memory kernels (pack + all-gather from the fp32 master; switch or
 peer reduction straight into the fp32 shard) or NCCL rings.
 
 Eq. 1 weighting (gradcheck.py:30-46) is the w = m_i/B pre-scale inside
-het_accumulate, so RS is a plain SUM. Idle ranks (m_i = 0, core.py:224-226)
-skip compute but still take part in every AG/RS with zero contributions.
-On one GPU the unit views point straight into the bf16 shadow and the
-accumulator is the grad shard itself: no collectives, no copies.
+het_accumulate, so RS is a plain SUM; when every rank has l_i <= 1, fused-route
+units instead cross the wire as unscaled bf16 gradients and the reduce-scatter
+applies every rank's weight and the cast (het_symm_reduce_scatter_bf16). Idle
+ranks (m_i = 0, core.py:224-226) skip compute but still take part in every
+AG/RS with zero contributions. On one GPU the unit views point straight into
+the bf16 shadow and the accumulator is the grad shard itself: no collectives,
+no copies.
 """
 from __future__ import annotations
 
