@@ -195,7 +195,7 @@ def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    job = build_job(args.config, max(args.gpus, world))
+    job = build_job(args.config, max(args.gpus, world), measured=True)   # our arm's plan
     ref = cpu_reference_rate(job, steps=args.steps, warmup=args.warmup)
     line = {"metric": "train samples/s", "value": ref["value"], "unit": "samples/s",
             "impl": "reference", "n_gpus": max(args.gpus, world), "steps": args.steps,
@@ -243,6 +243,9 @@ def main() -> None:
     ap.add_argument("--no-emulate", action="store_true",
                     help="run every rank on the full B200 (no green-context SM partition or "
                          "memory cap from the cluster spec)")
+    ap.add_argument("--offload", default="auto", choices=["auto", "on", "off"],
+                    help="activation-checkpoint offload to pinned host memory; auto = on "
+                         "for ranks the plan gives l_i > 1 (layered GA, PAPER.md:388-392)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
                     help="collective route for N>1: 4 = fused symmetric-memory kernels "
                          "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")
@@ -262,8 +265,11 @@ def main() -> None:
     compute_stream = emu.stream if emu.stream is not None else torch.cuda.current_stream()
     ctx = torch.cuda.stream(compute_stream)
     ctx.__enter__()
+    layered = job.plan.assignments[rank].num_microbatches > 1
+    offload = args.offload == "on" or (args.offload == "auto" and layered)
     tr = UnevenFSDPTrainer(job.arch, job.plan, rank, comm_ag=comm_ag, comm_rs=comm_rs, opt=OPT,
-                           device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO)
+                           device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO,
+                           offload_activations=offload)
     tr.init_params(seed=0)
     arch, plan = job.arch, job.plan
     nsteps = args.warmup + args.steps
@@ -334,6 +340,23 @@ def main() -> None:
         with open(os.path.join(args.trace_dir, f"rank{rank}.report.json"), "w") as fh:
             json.dump(trace_report, fh, indent=1)
     ctx.__exit__(None, None, None)
+    # per-rank peak of the caching allocator against the emulated HBM cap
+    mem = torch.tensor([torch.cuda.max_memory_allocated(dev) / 2 ** 30,
+                        emu.memory_cap_bytes / 2 ** 30], device=dev, dtype=torch.float64)
+    if world > 1:
+        allm = [torch.zeros_like(mem) for _ in range(world)]
+        dist.all_gather(allm, mem)
+    else:
+        allm = [mem]
+    peak_mem = [[round(float(x[0]), 3), round(float(x[1]), 3)] for x in allm]
+    # every rank's owned-kernel rates (rank 0's are the line's "kernels")
+    mine = {k: [v["launches"], round(v["gbs"] or 0.0, 1), round(v["ms_total"] / args.steps, 4)]
+            for k, v in kern.items()}
+    if world > 1:
+        kern_by_rank = [None] * world
+        dist.all_gather_object(kern_by_rank, mine)
+    else:
+        kern_by_rank = [mine]
 
     B = plan.total_batch
     hbm, hbm_kind = peaks()
@@ -358,6 +381,13 @@ def main() -> None:
                        "plan": [[a.microbatch, a.num_microbatches, a.state_ratio]
                                 for a in plan.assignments],
                        "uneven_units": plan.unit_shards.uneven_units,
+                       "peak_vs_cap_gib": peak_mem,
+                       # per rank: {kernel: [launches, algorithmic GB/s, ms per step]}
+                       "kernels_by_rank": kern_by_rank,
+                       "activation_offload_ranks": [
+                           i for i, a in enumerate(plan.assignments)
+                           if args.offload == "on" or (args.offload == "auto"
+                                                       and a.num_microbatches > 1)],
                        "profiles": ("measured" if any(d.get("profile_key") for d in job.profile_docs)
                                     and not args.analytic_profiles else "analytic"),
                        "planner_predicted_iteration_ms": plan.predicted_iteration_ms,

@@ -63,6 +63,17 @@ int het_pack_bf16(const float* src, void* dst_bf16, int64_t n, void* stream);
 int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float scale,
                    void* stream);
 
+/* (4') layered accumulate of nsrc consecutive microbatches in one pass:
+ * segs is [nsrc][nseg] (source j of segment s at segs[j*nseg + s]; every
+ * source of a segment has the same dst_off and n). Per element, in registers:
+ * a = (FIRST ? scale*g_0 : fma(scale, g_0, acc)); a = fma(scale, g_j, a) for
+ * j = 1..nsrc-1; acc = a — bit-identical to nsrc het_accumulate calls, with
+ * one read and one write of acc instead of nsrc (2*nsrc+4 B/param FIRST,
+ * 2*nsrc+8 ADD). 1 <= nsrc <= HET_MAX_ACC_SRC. */
+#define HET_MAX_ACC_SRC 4
+int het_accumulate_multi(float* acc, const het_seg_t* segs, int nseg, int nsrc, int mode,
+                         float scale, void* stream);
+
 /* (5) sharded AdamW over one rank's flat local shard (torch.optim.AdamW
  * formula, decoupled weight decay). Optional bf16 shadow write (the next
  * step's all-gather send buffer; fuses kernel (1)). 28 B/param, 30 with

@@ -62,10 +62,13 @@ def tier_profile(arch: ArchSpec, tier: str, max_m: int = 8) -> dict:
     return {"profile_key": tier, "fwd_ms": fwd, "bwd_ms": bwd, "compute_mem_gib": mem}
 
 
-def cluster_doc(arch: ArchSpec, tiers: list[str], mem_cap_fraction: float = 0.8) -> dict:
+def cluster_doc(arch: ArchSpec, tiers: list[str], mem_cap_fraction: float = 0.8,
+                memory_gib: dict[str, float] | None = None) -> dict:
+    """Cluster JSON (core.py:298-327); `memory_gib` overrides a tier's HBM budget."""
     ag = arch.unit_params * 2 / (NVLINK_GBS * 1e6)
     rs = arch.unit_params * 4 / (NVLINK_GBS * 1e6)
-    return {"gpus": [{"id": f"{t}-{i}", "memory_gib": TIERS[t][1], "profile_key": t}
+    mem = {t: TIERS[t][1] for t in tiers} | dict(memory_gib or {})
+    return {"gpus": [{"id": f"{t}-{i}", "memory_gib": mem[t], "profile_key": t}
                      for i, t in enumerate(tiers)],
             "comm": {"allgather_ms": ag, "reducescatter_ms": rs, "uneven_overhead": 0.15},
             "mem_cap_fraction": mem_cap_fraction}
@@ -78,6 +81,8 @@ class BenchConfig:
     tiers: tuple[str, ...]        # 8-GPU tier list; N GPUs take the first N
     batch_per_gpu: int            # global batch = batch_per_gpu * N (weak scaling)
     description: str
+    # per-config HBM budgets (GiB) overriding configs.TIERS for the named tiers
+    memory_gib: tuple[tuple[str, float], ...] = ()
 
 
 CONFIGS: dict[str, BenchConfig] = {
@@ -85,9 +90,13 @@ CONFIGS: dict[str, BenchConfig] = {
                             "tiny GPT (4 layers, d=256), 2:1 emulated ranks"),
     "gpt2_small": BenchConfig("gpt2_small", "gpt2_small", ("b200", "b200_half") * 4, 64,
                               "GPT-2 small uneven-FSDP, emulated 2:1 compute and memory"),
+    # the three smaller tiers get HBM budgets below their compute memory at the
+    # batch they can process, so the planner gives them l_i > 1 (layered GA,
+    # PAPER.md:377-386) and puts the whole training state on the full tier
     "bert_large": BenchConfig("bert_large", "bert_large",
-                              ("b200", "b200_3q", "b200_half", "b200_quarter") * 2, 32,
-                              "BERT-large bf16, 4-tier emulated cluster, layered GA"),
+                              ("b200", "b200_3q", "b200_half", "b200_quarter") * 2, 48,
+                              "BERT-large bf16, 4-tier emulated cluster, layered GA",
+                              (("b200_3q", 2.5), ("b200_half", 2.0), ("b200_quarter", 1.5))),
     "llama_1b3": BenchConfig("llama_1b3", "llama_1b3",
                              ("b200_tight", "b200_small") * 4, 16,
                              "Llama-style 1.3B, tight per-rank HBM caps"),
@@ -141,7 +150,7 @@ def build_job(name: str, n_gpus: int, global_batch: int | None = None,
             perf_from_docs(docs)
         except FitError:   # launch-bound tables with no linear tail: keep the analytic model
             docs = tuple(tier_profile(arch, t) for t in sorted(set(tiers)))
-    cluster = cluster_from_dict(cluster_doc(arch, tiers))
+    cluster = cluster_from_dict(cluster_doc(arch, tiers, memory_gib=dict(cfg.memory_gib)))
     batch = global_batch if global_batch is not None else cfg.batch_per_gpu * n_gpus
     model = model_from_dict({"layers": arch.layers, "params_per_layer": arch.unit_params,
                              "global_batch": batch})

@@ -238,10 +238,94 @@ __global__ void __launch_bounds__(THREADS) accumulate_kernel(float* __restrict__
   }
 }
 
-// bf16 segments copied into one bf16 buffer (persistent grid, as accumulate)
+// Several microbatches' gradients of the same segments in one pass (layered
+// GA with l_i > 1): source 0 comes from the SegTable, sources 1..NSRC-1 from
+// `more`. All NSRC gradient loads (and the acc load) are issued before the
+// arithmetic, which runs in microbatch order in registers, so the result is
+// bit-identical to NSRC sequential accumulate_kernel passes.
+struct MoreSrc {
+  const void* src[HET_MAX_ACC_SRC - 1][HET_MAX_SEGS];
+};
+
+template <int MODE, int NSRC>
+__global__ void __launch_bounds__(512) accumulate_multi_kernel(float* __restrict__ acc,
+                                                               const __grid_constant__ SegTable t,
+                                                               const __grid_constant__ MoreSrc ms,
+                                                               float w) {
+  constexpr int64_t kChunk = 512 * kAccVec;
+  const int64_t total = t.first_block[t.nseg];
+  int64_t b = blockIdx.x;
+  if (b >= total) return;
+  int lo = 0, hi = t.nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t.first_block[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  int s = lo;
+  for (; b < total; b += gridDim.x) {
+    while (s + 1 < t.nseg && t.first_block[s + 1] <= b) ++s;
+    const het_seg_t& sg = t.seg[s];
+    const int64_t base = (b - t.first_block[s]) * kChunk;
+    const __nv_bfloat16* src[NSRC];
+    src[0] = static_cast<const __nv_bfloat16*>(sg.src);
+    uintptr_t bits = reinterpret_cast<uintptr_t>(src[0]);
+#pragma unroll
+    for (int j = 1; j < NSRC; ++j) {
+      src[j] = static_cast<const __nv_bfloat16*>(ms.src[j - 1][s]);
+      bits |= reinterpret_cast<uintptr_t>(src[j]);
+    }
+    float* dst = acc + sg.dst_off;
+    if (((bits | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 && base + kChunk <= sg.n) {
+      const int64_t e = base + threadIdx.x * kAccVec;
+      uint4 raw[NSRC];
+#pragma unroll
+      for (int j = 0; j < NSRC; ++j) raw[j] = __ldcs(reinterpret_cast<const uint4*>(src[j] + e));
+      const bool wide = aligned32(dst);
+      F8 a;
+      if (MODE == HET_ACC_FIRST) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a.x[k] = 0.f;
+      } else if (wide) {
+        a = ld8(dst + e);
+      } else {
+        const float4 lo4 = *reinterpret_cast<const float4*>(dst + e);
+        const float4 hi4 = *reinterpret_cast<const float4*>(dst + e + 4);
+        a = F8{{lo4.x, lo4.y, lo4.z, lo4.w, hi4.x, hi4.y, hi4.z, hi4.w}};
+      }
+#pragma unroll
+      for (int j = 0; j < NSRC; ++j) {
+        float g[8];
+        unpack8(raw[j], g);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          a.x[k] = (j == 0) ? acc_op<MODE>(a.x[k], g[k], w) : fmaf(w, g[k], a.x[k]);
+      }
+      if (wide) {
+        st8(dst + e, a);
+      } else {
+        *reinterpret_cast<float4*>(dst + e) = make_float4(a.x[0], a.x[1], a.x[2], a.x[3]);
+        *reinterpret_cast<float4*>(dst + e + 4) = make_float4(a.x[4], a.x[5], a.x[6], a.x[7]);
+      }
+    } else {
+      const int64_t end = base + kChunk < sg.n ? base + kChunk : sg.n;
+      for (int64_t e = base + threadIdx.x; e < end; e += 512) {
+        float a = acc_op<MODE>((MODE & HET_ACC_FIRST) ? 0.f : dst[e],
+                               __bfloat162float(src[0][e]), w);
+#pragma unroll
+        for (int j = 1; j < NSRC; ++j) a = fmaf(w, __bfloat162float(src[j][e]), a);
+        dst[e] = a;
+      }
+    }
+  }
+}
+
+// bf16 segments copied into one bf16 buffer (persistent grid, as accumulate);
+// a CTA chunk is 512 threads x 2 x 16 B, both loads issued before the stores
+constexpr int kGatherIters = 2;
+constexpr int64_t kGatherChunk = 512 * 8 * kGatherIters;
+
 __global__ void __launch_bounds__(512) gather_bf16_kernel(__nv_bfloat16* __restrict__ dst,
                                                           const __grid_constant__ SegTable t) {
-  constexpr int64_t kChunk = 512 * 8;
   const int64_t total = t.first_block[t.nseg];
   int64_t b = blockIdx.x;
   if (b >= total) return;
@@ -254,15 +338,20 @@ __global__ void __launch_bounds__(512) gather_bf16_kernel(__nv_bfloat16* __restr
   for (; b < total; b += gridDim.x) {
     while (s + 1 < t.nseg && t.first_block[s + 1] <= b) ++s;
     const het_seg_t sg = t.seg[s];
-    const int64_t base = (b - t.first_block[s]) * kChunk;
+    const int64_t base = (b - t.first_block[s]) * kGatherChunk;
     const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(sg.src);
     __nv_bfloat16* d = dst + sg.dst_off;
     const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(d)) & 15) == 0;
-    const int64_t e = base + threadIdx.x * 8;
-    if (vec && base + kChunk <= sg.n) {
-      *reinterpret_cast<uint4*>(d + e) = __ldcs(reinterpret_cast<const uint4*>(src + e));
+    if (vec && base + kGatherChunk <= sg.n) {
+      uint4 r[kGatherIters];
+#pragma unroll
+      for (int it = 0; it < kGatherIters; ++it)
+        r[it] = __ldcs(reinterpret_cast<const uint4*>(src + base + (it * 512 + threadIdx.x) * 8));
+#pragma unroll
+      for (int it = 0; it < kGatherIters; ++it)
+        *reinterpret_cast<uint4*>(d + base + (it * 512 + threadIdx.x) * 8) = r[it];
     } else {
-      const int64_t end = base + kChunk < sg.n ? base + kChunk : sg.n;
+      const int64_t end = base + kGatherChunk < sg.n ? base + kGatherChunk : sg.n;
       for (int64_t i = base + threadIdx.x; i < end; i += 512) d[i] = src[i];
     }
   }
@@ -494,6 +583,67 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
   return het::check_launch("het_accumulate");
 }
 
+int het_accumulate_multi(float* acc, const het_seg_t* segs, int nseg, int nsrc, int mode,
+                         float scale, void* stream) {
+  if (!acc || !segs || nseg < 1 || nseg > HET_MAX_SEGS || nsrc < 1 || nsrc > HET_MAX_ACC_SRC ||
+      (mode != HET_ACC_ADD && mode != HET_ACC_FIRST))
+    return fail(HET_EARG, "het_accumulate_multi: bad args (nseg=%d nsrc=%d mode=%d)", nseg,
+                nsrc, mode);
+  SegTable t;
+  MoreSrc ms;
+  std::memset(&ms, 0, sizeof(ms));
+  t.nseg = nseg;
+  constexpr int64_t chunk = 512 * kAccVec;
+  int64_t blocks = 0;
+  for (int s = 0; s < nseg; ++s) {
+    const het_seg_t& s0 = segs[s];
+    if (s0.n < 0 || s0.dst_off < 0 || (s0.n > 0 && !s0.src))
+      return fail(HET_EARG, "het_accumulate_multi: bad segment %d", s);
+    for (int j = 1; j < nsrc; ++j) {
+      const het_seg_t& sj = segs[static_cast<int64_t>(j) * nseg + s];
+      if (sj.n != s0.n || sj.dst_off != s0.dst_off || (s0.n > 0 && !sj.src))
+        return fail(HET_EARG, "het_accumulate_multi: source %d of segment %d differs in shape",
+                    j, s);
+      ms.src[j - 1][s] = sj.src;
+    }
+    t.seg[s] = s0;
+    t.first_block[s] = blocks;
+    blocks += (s0.n + chunk - 1) / chunk;
+  }
+  for (int s = nseg; s <= HET_MAX_SEGS; ++s) t.first_block[s] = blocks;
+  if (blocks == 0) return HET_OK;
+  if (blocks > 0x7fffffff) return fail(HET_EARG, "het_accumulate_multi: too large");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static int resident = 0;
+  if (resident == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
+                                                  accumulate_multi_kernel<HET_ACC_ADD, 4>, 512, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  }
+  const dim3 grid(static_cast<unsigned>(blocks < resident ? blocks : resident));
+#define HET_ACCM(M, K) accumulate_multi_kernel<M, K><<<grid, 512, 0, st>>>(acc, t, ms, scale)
+  if (mode == HET_ACC_FIRST) {
+    switch (nsrc) {
+      case 1: HET_ACCM(HET_ACC_FIRST, 1); break;
+      case 2: HET_ACCM(HET_ACC_FIRST, 2); break;
+      case 3: HET_ACCM(HET_ACC_FIRST, 3); break;
+      default: HET_ACCM(HET_ACC_FIRST, 4);
+    }
+  } else {
+    switch (nsrc) {
+      case 1: HET_ACCM(HET_ACC_ADD, 1); break;
+      case 2: HET_ACCM(HET_ACC_ADD, 2); break;
+      case 3: HET_ACCM(HET_ACC_ADD, 3); break;
+      default: HET_ACCM(HET_ACC_ADD, 4);
+    }
+  }
+#undef HET_ACCM
+  return het::check_launch("het_accumulate_multi");
+}
+
 int het_gather_bf16(void* dst, const het_seg_t* segs, int nseg, void* stream) {
   if (!dst || !segs || nseg < 1 || nseg > HET_MAX_SEGS)
     return fail(HET_EARG, "het_gather_bf16: bad args (nseg=%d)", nseg);
@@ -505,7 +655,7 @@ int het_gather_bf16(void* dst, const het_seg_t* segs, int nseg, void* stream) {
       return fail(HET_EARG, "het_gather_bf16: bad segment %d", s);
     t.seg[s] = segs[s];
     t.first_block[s] = blocks;
-    blocks += (segs[s].n + 4095) / 4096;
+    blocks += (segs[s].n + kGatherChunk - 1) / kGatherChunk;
   }
   for (int s = nseg; s <= HET_MAX_SEGS; ++s) t.first_block[s] = blocks;
   if (blocks == 0) return HET_OK;

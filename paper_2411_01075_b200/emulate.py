@@ -2,7 +2,8 @@
 budgets are set with a memory-fraction cap, and per-rank SM partitions are
 set with CUDA green contexts").
 
-A rank's tier comes from the cluster spec: its `memory_gib` becomes a cap on
+A rank's tier comes from the cluster spec: its `memory_gib` (the emulated
+physical HBM, not the planner's 0.8 effective capacity) becomes a cap on
 the torch caching allocator (`set_per_process_memory_fraction`), and the
 tier's SM fraction (configs.TIERS) becomes a CUDA green context holding that
 many SMs; the rank's compute stream is created inside it, so every model and
@@ -50,7 +51,10 @@ def emulate_tier(cluster: ClusterSpec, rank: int, device: torch.device, *,
     frac, _ = TIERS[gpu.profile_key]
     props = torch.cuda.get_device_properties(device)
     total_sms = props.multi_processor_count
-    cap = int(cluster.effective_capacity(gpu))
+    # the emulated GPU's physical HBM: the planner's mem_cap_fraction headroom
+    # (core.py:143-144) stays available at run time for what its memory model
+    # omits (allocator fragmentation, the N>1 gather/accumulate buffers)
+    cap = int(gpu.memory_capacity)
     if memory_cap:
         torch.cuda.set_per_process_memory_fraction(min(1.0, cap / props.total_memory), device)
     green, stream, nsm = None, None, total_sms

@@ -36,7 +36,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
-           "het_symm_reduce_scatter_bf16", "het_gather_bf16")
+           "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi")
 
 
 class HetSeg(ctypes.Structure):
@@ -67,6 +67,7 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_last_error": ([], ctypes.c_char_p),
         "het_pack_bf16": ([vp, vp, i64, vp], i32),
         "het_accumulate": ([vp, ctypes.POINTER(HetSeg), i32, i32, f32, vp], i32),
+        "het_accumulate_multi": ([vp, ctypes.POINTER(HetSeg), i32, i32, i32, f32, vp], i32),
         "het_adamw": ([vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, i64, vp], i32),
         "het_fill_f32": ([vp, f32, i64, vp], i32),
         "het_tune": ([i32, i32], i32),
@@ -206,24 +207,96 @@ def accumulate(acc: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]], fir
         events[1].record()
 
 
+HET_MAX_ACC_SRC = 4
+
+
+def accumulate_multi(acc: torch.Tensor, sources: Sequence[Sequence[torch.Tensor]],
+                     offsets: Sequence[int], first: bool, scale: float, stream=None,
+                     events=None) -> None:
+    """Layered accumulate of several consecutive microbatches in one pass:
+    sources[j][s] is microbatch j's bf16 gradient of segment s, landing at
+    acc[offsets[s]:]; acc (=|+=) scale*g_0, then += scale*g_j in order, in
+    registers — bit-identical to len(sources) accumulate() calls with one
+    read and one write of acc."""
+    nsrc = len(sources)
+    if nsrc == 0 or not offsets:
+        return
+    if nsrc > HET_MAX_ACC_SRC:
+        raise InputError(f"accumulate_multi: at most {HET_MAX_ACC_SRC} sources, got {nsrc}")
+    if any(len(src) != len(offsets) for src in sources):
+        raise InputError("accumulate_multi: every source needs one tensor per offset")
+    if len(offsets) > HET_MAX_SEGS:
+        parts = range(0, len(offsets), HET_MAX_SEGS)
+        for j, i in enumerate(parts):
+            ev = None if events is None else (events[0] if j == 0 else None,
+                                              events[1] if j == len(parts) - 1 else None)
+            accumulate_multi(acc, [src[i:i + HET_MAX_SEGS] for src in sources],
+                             offsets[i:i + HET_MAX_SEGS], first, scale, stream, ev)
+        return
+    cap = acc.numel()
+    rows: list[list[int]] = []      # [dst_off, n, src_0, ..., src_{nsrc-1}]
+    for i, off in enumerate(offsets):
+        n = sources[0][i].numel()
+        if off < 0 or off + n > cap:
+            raise InputError(f"accumulate_multi: segment {i} [{off}, {off + n}) outside {cap}")
+        ptrs = []
+        for j, src in enumerate(sources):
+            if src[i].numel() != n:
+                raise InputError(f"accumulate_multi: source {j} segment {i} has "
+                                 f"{src[i].numel()} elements, source 0 has {n}")
+            ptrs.append(_cuda(src[i], torch.bfloat16, f"src[{j}][{i}]"))
+        if rows and rows[-1][0] + rows[-1][1] == off and all(
+                rows[-1][2 + j] + 2 * rows[-1][1] == ptrs[j] for j in range(nsrc)):
+            rows[-1][1] += n        # back-to-back in the accumulator and in every source
+        else:
+            rows.append([off, n] + ptrs)
+    segs = (HetSeg * (len(rows) * nsrc))()
+    for j in range(nsrc):
+        for i, r in enumerate(rows):
+            e = segs[j * len(rows) + i]
+            e.src, e.dst_off, e.n = r[2 + j], r[0], r[1]
+    accp = _cuda(acc, torch.float32, "acc")
+    if events is not None and events[0] is not None:
+        events[0].record()
+    _check(load().het_accumulate_multi(accp, segs, len(rows), nsrc,
+                                       ACC_FIRST if first else ACC_ADD, float(scale),
+                                       _stream(stream)), "het_accumulate_multi")
+    if events is not None and events[1] is not None:
+        events[1].record()
+
+
 def gather_bf16(dst: torch.Tensor, grads: Sequence[tuple[torch.Tensor, int]],
-                stream=None) -> None:
-    """dst[off:off+g.numel()] = g for every (g, off); bf16, unscaled."""
+                stream=None, events=None) -> None:
+    """dst[off:off+g.numel()] = g for every (g, off); bf16, unscaled.
+    `events` as for accumulate: recorded right around the launch(es)."""
     if not grads:
         return
     if len(grads) > HET_MAX_SEGS:
-        for i in range(0, len(grads), HET_MAX_SEGS):
-            gather_bf16(dst, grads[i:i + HET_MAX_SEGS], stream)
+        parts = range(0, len(grads), HET_MAX_SEGS)
+        for j, i in enumerate(parts):
+            ev = None if events is None else (events[0] if j == 0 else None,
+                                              events[1] if j == len(parts) - 1 else None)
+            gather_bf16(dst, grads[i:i + HET_MAX_SEGS], stream, ev)
         return
     cap = dst.numel()
-    segs = (HetSeg * len(grads))()
+    rows: list[list[int]] = []      # [src, dst_off, n]; back-to-back segments coalesce
     for i, (g, off) in enumerate(grads):
         if off < 0 or off + g.numel() > cap:
             raise InputError(f"gather_bf16: segment {i} [{off}, {off + g.numel()}) outside {cap}")
-        segs[i].src, segs[i].dst_off, segs[i].n = _cuda(g, torch.bfloat16, f"grad[{i}]"), off, \
-            g.numel()
-    _check(load().het_gather_bf16(_cuda(dst, torch.bfloat16, "dst"), segs, len(grads),
-                                  _stream(stream)), "het_gather_bf16")
+        src, n = _cuda(g, torch.bfloat16, f"grad[{i}]"), g.numel()
+        if rows and rows[-1][0] + 2 * rows[-1][2] == src and rows[-1][1] + rows[-1][2] == off:
+            rows[-1][2] += n
+        else:
+            rows.append([src, off, n])
+    segs = (HetSeg * len(rows))()
+    for i, (src, off, n) in enumerate(rows):
+        segs[i].src, segs[i].dst_off, segs[i].n = src, off, n
+    dstp = _cuda(dst, torch.bfloat16, "dst")
+    if events is not None and events[0] is not None:
+        events[0].record()
+    _check(load().het_gather_bf16(dstp, segs, len(rows), _stream(stream)), "het_gather_bf16")
+    if events is not None and events[1] is not None:
+        events[1].record()
 
 
 def adamw(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,

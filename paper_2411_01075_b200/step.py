@@ -188,6 +188,12 @@ class UnevenFSDPTrainer:
         # overlap the next pair's backward); with one rank nothing overlaps, so the whole
         # backward's bf16 -> fp32 scale-cast is one launch (holds 2 B/param of bf16 grads)
         self.acc_group = self.L.blocks if self.N == 1 else 2
+        # l_i > 1: microbatches per accumulate launch. A unit's gradients of
+        # consecutive microbatches are held (one extra unit of bf16 gradients per
+        # held microbatch) and folded into the fp32 accumulator in one pass
+        # (het_accumulate_multi): one read and one write of the accumulator per
+        # group instead of per microbatch, bit-identical to one pass each
+        self.acc_microbatches = 2
         self.bf16_wire = bf16_wire
         # Eq. 1 weights of every rank (the bf16-wire reduce-scatter applies them itself)
         self.rank_weights = [a.microbatch / plan.total_batch for a in plan.assignments]
@@ -499,11 +505,8 @@ class UnevenFSDPTrainer:
             gb = self.symm["gb0"]
             span = (self.symm["gb1"].data_ptr() - gb.data_ptr()) // 2 + self.symm["gb1"].numel()
             a, b = self.timers.pair("gather", n16 * 4.0)
-            if a is not None:
-                a.record()
-            K.gather_bf16(gb.as_strided((span,), (1,), gb.storage_offset()), stage)
-            if b is not None:
-                b.record()
+            K.gather_bf16(gb.as_strided((span,), (1,), gb.storage_offset()), stage,
+                          events=None if a is None else (a, b))
             self.launches += 1
         if not items:
             return
@@ -524,6 +527,18 @@ class UnevenFSDPTrainer:
         a, b = self.timers.pair("accumulate", n * (6.0 if first else 10.0))
         K.accumulate(acc, [(g, seg[nm]) for g, nm in zip(grads, names)], first, self.w,
                      events=None if a is None else (a, b))
+        self.launches += 1
+
+    def _accumulate_mb(self, acc, held, names, seg, first):
+        """Layered accumulate of consecutive microbatches' gradients of one unit
+        (one launch; a single microbatch goes through het_accumulate)."""
+        if len(held) == 1:
+            self._accumulate(acc, held[0], names, seg, first)
+            return
+        n = sum(g.numel() for g in held[0])
+        a, b = self.timers.pair("accumulate", n * (2.0 * len(held) + (4.0 if first else 8.0)))
+        K.accumulate_multi(acc, held, [seg[nm] for nm in names], first, self.w,
+                           events=None if a is None else (a, b))
         self.launches += 1
 
     # ------------------------------------------------------------------ step
@@ -672,6 +687,7 @@ class UnevenFSDPTrainer:
                     t.record_stream(comp)
                     h[k][u] = t
             acc = self._acc(u)
+            held: list[list[torch.Tensor]] = []      # microbatch gradients awaiting accumulate
             flat = self._unit_flat(u)
             pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}
             plist = [pl[nm] for nm in unit_names]
@@ -704,8 +720,11 @@ class UnevenFSDPTrainer:
                     if self.pair_units:
                         unit_grads = list(grads[:-1])
                     else:
-                        self._accumulate(acc, grads[:-1], unit_names, self.unit_seg,
-                                         first=(k == 0))
+                        held.append(list(grads[:-1]))
+                        if len(held) >= self.acc_microbatches or k == nmb - 1:
+                            self._accumulate_mb(acc, held, unit_names, self.unit_seg,
+                                                first=(k + 1 == len(held)))
+                            held = []
                 if u == 0:
                     # fused embedding backward: token / position rows summed in fp32 straight
                     # into the root accumulator (no dense [vocab, d] bf16 gradient,

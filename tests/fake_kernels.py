@@ -54,6 +54,16 @@ def accumulate(acc, grads, first, scale, stream=None, events=None):
                                                          first, scale))
 
 
+def accumulate_multi(acc, sources, offsets, first, scale, stream=None, events=None):
+    calls.append("accumulate")
+    for j, src in enumerate(sources):
+        for g, off in zip(src, offsets):
+            n = g.numel()
+            cur = acc[off:off + n].numpy()
+            acc[off:off + n] = torch.from_numpy(O.accumulate(
+                cur, _bits(g.contiguous().reshape(-1)), first and j == 0, scale))
+
+
 def adamw(p, g, m, v, shadow, *, lr, beta1, beta2, eps, weight_decay, step, stream=None):
     calls.append("adamw")
     rp, rm, rv = O.adamw(p.numpy(), g.numpy(), m.numpy(), v.numpy(), lr=lr, beta1=beta1,

@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 
 def test_plan_json_roundtrip_and_unknown_fields(tmp_path):
-    job = build_job("bert_large", 4)
+    job = build_job("bert_large", 4, measured=True)
     p = tmp_path / "plan.json"
     H.save_plan(job.plan, p)
     again = H.load_plan(p)

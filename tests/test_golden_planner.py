@@ -100,3 +100,21 @@ def test_validator_verdicts_match():
         v = H.validate_plan(H.plan_from_dict(c["plan"]), H.cluster_from_dict(c["cluster"]),
                             H.model_from_dict(c["model"]), perf.memory_models())
         assert [[x.constraint, x.gpu_id] for x in v] == c["violations"], c["mutation"]
+
+
+def test_bench_plans_bit_exact():
+    """The plans bench.py runs (measured B200 tier profiles, per-config HBM
+    budgets; oracle/gen_golden_bench_plans.py) equal the reference planner's,
+    and build_job reproduces them from the committed profiles."""
+    from paper_2411_01075_b200.configs import build_job
+    for inst in _load("planner_bench_plans.json")["cases"]:
+        assert _json_roundtrip(_run(inst)) == inst["dp"], inst["name"]
+        name, n = inst["name"].split("@")
+        job = build_job(name, int(n), measured=True)
+        assert _json_roundtrip(H.plan_to_dict(job.plan)) == inst["dp"]["plan"], inst["name"]
+        sp = job.plan.unit_shards
+        assert [list(v) for v in sp.shards] == inst["shards"]["shards"], inst["name"]
+        assert [list(v) for v in sp.offsets] == inst["shards"]["offsets"], inst["name"]
+    layered = [c["name"] for c in _load("planner_bench_plans.json")["cases"]
+               if any(a["num_microbatches"] > 1 for a in c["dp"]["plan"]["assignments"])]
+    assert "bert_large@4" in layered and "bert_large@8" in layered

@@ -75,6 +75,71 @@ def test_accumulate_layered(cuda, sizes):
     assert _rel(got, ref) <= RTOL
 
 
+@pytest.mark.parametrize("sizes", [[8], [3, 5, 7], [1, 8191, 8192, 8193, 33000],
+                                   [768 * 2304, 2304, 768 * 768, 768, 3072 * 768]])
+@pytest.mark.parametrize("gap", [0, 1])
+def test_gather_bf16_bit_exact(cuda, sizes, gap):
+    """het_gather_bf16 (bf16-wire staging): every segment lands bit-exact at its
+    offset. gap=0: back-to-back segments, 16-byte vector path; gap=1: one
+    untouched element between segments and a 2-byte-aligned destination
+    (scalar path)."""
+    grads, offs, total = _segments(sizes, 11)
+    offs = [o + gap * i for i, o in enumerate(offs)]
+    total += gap * len(sizes)
+    dst = torch.full((total + gap,), 7.0, dtype=torch.bfloat16, device=cuda)
+    view = dst[gap:]
+    K.gather_bf16(view, [(g.to(cuda), o) for g, o in zip(grads, offs)])
+    torch.cuda.synchronize()
+    ref = np.full(total, _bits(torch.tensor([7.0], dtype=torch.bfloat16))[0], dtype=np.uint16)
+    for g, o in zip(grads, offs):
+        ref[o:o + g.numel()] = _bits(g)
+    assert np.array_equal(_bits(view), ref)
+    with pytest.raises(InputError):
+        K.gather_bf16(view, [(grads[0].to(cuda), total)])
+
+
+@pytest.mark.parametrize("nsrc", [1, 2, 3, 4])
+@pytest.mark.parametrize("sizes", [[3, 5, 7], [1, 8191, 8192, 8193, 33000],
+                                   [768 * 2304, 2304, 768 * 768, 768]])
+def test_accumulate_multi_bit_exact(cuda, nsrc, sizes):
+    """het_accumulate_multi over nsrc microbatches == nsrc het_accumulate passes,
+    bit for bit, in FIRST and ADD mode (and the CPU oracle within RTOL)."""
+    w = 5.0 / 131.0
+    grads, offs, total = _segments(sizes, 3)
+    src = [[(g * (j + 1) - j).to(torch.bfloat16).to(cuda) for g in grads] for j in range(nsrc)]
+    for first in (True, False):
+        init = torch.randn(total, generator=torch.Generator().manual_seed(9)).to(cuda)
+        one, many = init.clone(), init.clone()
+        for j in range(nsrc):
+            K.accumulate(one, list(zip(src[j], offs)), first and j == 0, w)
+        K.accumulate_multi(many, src, offs, first, w)
+        torch.cuda.synchronize()
+        assert torch.equal(one.view(torch.int32), many.view(torch.int32)), (first, nsrc)
+        ref = init.cpu().numpy()
+        for j in range(nsrc):
+            full = np.zeros(total, dtype=np.uint16)
+            for g, o in zip(src[j], offs):
+                full[o:o + g.numel()] = _bits(g)
+            ref = O.accumulate(ref, full, first and j == 0, w)
+        assert _rel(many.cpu().numpy(), ref) <= RTOL
+
+
+def test_accumulate_multi_unaligned_and_rejects(cuda):
+    grads, offs, total = _segments([1000, 4099], 4)
+    acc = torch.zeros(total + 1, device=cuda)[1:]            # 4-byte aligned only
+    src = [[g.to(cuda) for g in grads] for _ in range(2)]
+    ref = torch.zeros_like(acc)
+    K.accumulate_multi(acc, src, offs, True, 0.5)
+    for j in range(2):
+        K.accumulate(ref, list(zip(src[j], offs)), j == 0, 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(acc.view(torch.int32), ref.view(torch.int32))
+    with pytest.raises(InputError):                           # mismatched source shapes
+        K.accumulate_multi(acc, [src[0], [src[1][0], src[1][1][:-1]]], offs, True, 1.0)
+    with pytest.raises(InputError):
+        K.accumulate_multi(acc, [src[0]] * 5, offs, True, 1.0)
+
+
 def test_accumulate_rejects_out_of_range(cuda):
     acc = torch.zeros(10, device=cuda)
     with pytest.raises(InputError):

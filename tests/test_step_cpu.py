@@ -53,7 +53,9 @@ def test_single_rank_step_gradients(fake, m, l):
         assert float((got - g.double()).norm() / g.double().norm()) <= 2e-2
     # one accumulate per (unit, microbatch) + head and embedding passes, one AdamW
     n_acc = fake.calls.count("accumulate")
-    unit_launches = 1 if l == 1 else arch.layers * l     # l=1, one rank: one grouped launch
+    # l=1, one rank: one grouped launch; l>1: microbatches folded in groups of
+    # tr.acc_microbatches per unit
+    unit_launches = 1 if l == 1 else arch.layers * -(-l // tr.acc_microbatches)
     assert n_acc == unit_launches + l            # units + head; embedding is fused
     assert fake.calls.count("embedding_grad") == l
     assert fake.calls.count("adamw") == 1

@@ -23,14 +23,25 @@ ap.add_argument("--config", default="gpt2_small")
 ap.add_argument("--switch", default="fuse_residual_norm")
 ap.add_argument("--blocks", type=int, default=6)
 ap.add_argument("--steps", type=int, default=8)
+ap.add_argument("--ml", default=None,
+                help="M,L: run a one-rank plan with microbatch M and L microbatches "
+                     "(layered GA) instead of the config's N=1 plan")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
 job = build_job(args.config, 1, measured=True)
-tr = UnevenFSDPTrainer(job.arch, job.plan, 0, device=dev)
+plan = job.plan
+if args.ml:
+    from paper_2411_01075_b200.core import GpuAssignment, ModelSpec, TrainPlan
+    from paper_2411_01075_b200.sharding import assign_unit_shards
+    m, l = (int(x) for x in args.ml.split(","))
+    md = ModelSpec(job.arch.layers, job.arch.unit_params, m * l)
+    plan = TrainPlan((GpuAssignment("ab", m, l, m * l, 1.0, 0.0, float(md.state_bytes)),),
+                     1.0, 1.0, 2.0 * job.arch.layers, False, assign_unit_shards([1.0], md))
+tr = UnevenFSDPTrainer(job.arch, plan, 0, device=dev)
 tr.init_params(seed=0)
-tok = torch.from_numpy(rank_tokens(job.plan, 0, job.arch.seq, job.arch.vocab, 1, 0)).to(dev)
+tok = torch.from_numpy(rank_tokens(plan, 0, job.arch.seq, job.arch.vocab, 1, 0)).to(dev)
 
 
 def setting(on: bool) -> None:
@@ -42,6 +53,8 @@ def setting(on: bool) -> None:
         M.LT_EPILOGUES = on
     elif args.switch == "keep_last":
         tr.keep_last_graph = on
+    elif args.switch == "acc_microbatches":
+        tr.acc_microbatches = 2 if on else 1
     elif args.switch == "acc_group":
         tr.acc_group = tr.L.blocks if on else 2
     else:
