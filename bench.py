@@ -246,6 +246,10 @@ def main() -> None:
     ap.add_argument("--offload", default="auto", choices=["auto", "on", "off"],
                     help="activation-checkpoint offload to pinned host memory; auto = on "
                          "for ranks the plan gives l_i > 1 (layered GA, PAPER.md:388-392)")
+    ap.add_argument("--offload-schedule", default="checkpoints",
+                    choices=["checkpoints", "reference"],
+                    help="checkpoints: only unit-input checkpoints make the host round trip; "
+                         "reference: the simulator's full schedule (sim.py:226-338)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
                     help="collective route for N>1: 4 = fused symmetric-memory kernels "
                          "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")
@@ -269,7 +273,8 @@ def main() -> None:
     offload = args.offload == "on" or (args.offload == "auto" and layered)
     tr = UnevenFSDPTrainer(job.arch, job.plan, rank, comm_ag=comm_ag, comm_rs=comm_rs, opt=OPT,
                            device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO,
-                           offload_activations=offload)
+                           offload_activations=offload,
+                           offload_schedule=args.offload_schedule)
     tr.init_params(seed=0)
     arch, plan = job.arch, job.plan
     nsteps = args.warmup + args.steps
@@ -381,6 +386,7 @@ def main() -> None:
                        "plan": [[a.microbatch, a.num_microbatches, a.state_ratio]
                                 for a in plan.assignments],
                        "uneven_units": plan.unit_shards.uneven_units,
+                       "offload_schedule": args.offload_schedule,
                        "peak_vs_cap_gib": peak_mem,
                        # per rank: {kernel: [launches, algorithmic GB/s, ms per step]}
                        "kernels_by_rank": kern_by_rank,

@@ -128,7 +128,8 @@ class UnevenFSDPTrainer:
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
                  algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64,
-                 offload_activations: bool = False, check_routes: bool = True,
+                 offload_activations: bool = False, offload_schedule: str = "reference",
+                 check_routes: bool = True,
                  bf16_wire: bool = True):
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
@@ -223,6 +224,14 @@ class UnevenFSDPTrainer:
         # unit-boundary checkpoints go to pinned host memory on a D2H stream after the
         # forward uses them and come back one unit ahead of their recompute on an H2D stream
         self.offload = offload_activations and self.cuda
+        # "reference": with l_i >= 2 the simulator's full schedule (unit outputs and
+        # upstream gradients make PCIe round trips too: O(1) boundary tensors resident);
+        # "checkpoints": only the unit-input checkpoints go to host (O(L * l_i) bytes),
+        # the l_i in-flight boundary tensors of the current unit stay on the GPU
+        # (O(l_i) bytes) so no round trip sits on the critical path
+        if offload_schedule not in ("reference", "checkpoints"):
+            raise InputError(f"unknown offload schedule {offload_schedule!r}")
+        self.offload_schedule = offload_schedule
         if self.offload:
             self.d2h_stream = torch.cuda.Stream(device=dev)
             self.h2d_stream = torch.cuda.Stream(device=dev)
@@ -582,7 +591,7 @@ class UnevenFSDPTrainer:
               for k in range(self.l)] if active else []
         nmb = len(mb)
         off = self.offload and nmb > 0
-        deep = off and nmb >= 2
+        deep = off and nmb >= 2 and self.offload_schedule == "reference"
         # one microbatch, no offload: the last unit's forward runs with autograd and its
         # graph is kept for the backward, which follows right after the head (its
         # recompute would redo exactly that forward)

@@ -104,7 +104,8 @@ def test_checkpoint_resume_on_gpu(cuda, tmp_path):
     assert _nrel(b.p32.cpu().numpy(), a.p32.cpu().numpy()) <= 1e-5
 
 
-def test_activation_offload_matches_and_saves_memory(cuda):
+@pytest.mark.parametrize("schedule", ["reference", "checkpoints"])
+def test_activation_offload_matches_and_saves_memory(cuda, schedule):
     """Checkpoint offload leaves the step's math
     unchanged, is lint-clean against the simulator's offload rules, and cuts
     the resident boundary activations."""
@@ -114,11 +115,16 @@ def test_activation_offload_matches_and_saves_memory(cuda):
     res = {}
     torch.use_deterministic_algorithms(True)   # deterministic cuDNN attention backward
     try:
-        _offload_runs(arch, plan, tok, cuda, res)
+        _offload_runs(arch, plan, tok, cuda, res, schedule)
     finally:
         torch.use_deterministic_algorithms(False)
-    # l_i = 4: the full reference schedule, activation gradients included
-    assert {"offload_act", "prefetch_act", "offload_grad", "prefetch_grad"} <= res[True][3]
+    if schedule == "reference":
+        # l_i = 4: the full reference schedule, activation gradients included
+        assert {"offload_act", "prefetch_act", "offload_grad", "prefetch_grad"} <= res[True][3]
+    else:
+        # checkpoints only: the in-flight boundary tensors stay on the GPU
+        assert {"offload_act", "prefetch_act"} <= res[True][3]
+        assert not {"offload_grad", "prefetch_grad"} & res[True][3]
     assert res[True][0] == res[False][0]
     assert torch.equal(res[True][1], res[False][1])       # offload moves bytes, not math
     # 12 units x 4 microbatches x [4, 512, 768] bf16 checkpoints = 151 MB resident without
@@ -126,10 +132,11 @@ def test_activation_offload_matches_and_saves_memory(cuda):
     assert res[True][2] < res[False][2] - 120e6, (res[True][2], res[False][2])
 
 
-def _offload_runs(arch, plan, tok, cuda, res):
+def _offload_runs(arch, plan, tok, cuda, res, schedule="reference"):
     from paper_2411_01075_b200.trace import StepTracer, lint_measured_trace
     for off in (False, True):
-        tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda, offload_activations=off)
+        tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda, offload_activations=off,
+                               offload_schedule=schedule)
         tr.init_params(seed=1)
         tr.step(tok)
         torch.cuda.synchronize()

@@ -23,6 +23,7 @@ ap.add_argument("--config", default="gpt2_small")
 ap.add_argument("--switch", default="fuse_residual_norm")
 ap.add_argument("--blocks", type=int, default=6)
 ap.add_argument("--steps", type=int, default=8)
+ap.add_argument("--offload-schedule", default="reference")
 ap.add_argument("--ml", default=None,
                 help="M,L: run a one-rank plan with microbatch M and L microbatches "
                      "(layered GA) instead of the config's N=1 plan")
@@ -39,7 +40,9 @@ if args.ml:
     md = ModelSpec(job.arch.layers, job.arch.unit_params, m * l)
     plan = TrainPlan((GpuAssignment("ab", m, l, m * l, 1.0, 0.0, float(md.state_bytes)),),
                      1.0, 1.0, 2.0 * job.arch.layers, False, assign_unit_shards([1.0], md))
-tr = UnevenFSDPTrainer(job.arch, plan, 0, device=dev)
+tr = UnevenFSDPTrainer(job.arch, plan, 0, device=dev,
+                       offload_activations=args.switch == "offload",
+                       offload_schedule=args.offload_schedule)
 tr.init_params(seed=0)
 tok = torch.from_numpy(rank_tokens(plan, 0, job.arch.seq, job.arch.vocab, 1, 0)).to(dev)
 
@@ -53,6 +56,8 @@ def setting(on: bool) -> None:
         M.LT_EPILOGUES = on
     elif args.switch == "keep_last":
         tr.keep_last_graph = on
+    elif args.switch == "offload":
+        tr.offload = on
     elif args.switch == "acc_microbatches":
         tr.acc_microbatches = 2 if on else 1
     elif args.switch == "acc_group":
