@@ -36,27 +36,49 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&f)[8]) {
 // round to bf16 and back (the value torch's bf16 tensors hold)
 __device__ __forceinline__ float rbf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
-// torch's tanh-approximate GELU and its derivative, in fp32
-constexpr float kBeta = 0.7978845608028654f;   // sqrt(2/pi)
-constexpr float kKappa = 0.044715f;
+// torch's tanh-approximate GELU, y = 0.5 x (1 + tanh(u)), u = b (x + k x^3),
+// and its derivative, evaluated through 0.5 (1 + tanh(u)) = sigmoid(2u):
+//   y = x s,  dy/dx = s + x s (1 - s) 2u' = s (1 + x e s (c0 + 3 c1 x^2)),
+//   s = 1 / (1 + e), e = exp(-2u), 2u = x (c0 + c1 x^2), c0 = 2b, c1 = 2bk.
+// One ex2 and one rcp (MUFU) and about ten FP32 instructions per element, no
+// cancellation (1 + tanh(u) is never formed), against torch's tanhf form at
+// about twenty (both kernels were issue-bound on it: 78% issue slots busy at
+// 0.65 of HBM in ncu). Agrees with torch's fp32 formula to a few fp32 ulps;
+// after bf16 rounding the outputs match torch's except for rare 1-ulp ties
+// (tests/test_kernels_gpu.py bounds both).
+constexpr float kC0 = 1.5957691216057308f;          // 2 sqrt(2/pi)
+constexpr float kC1 = 0.07135481627159701f;         // 2 sqrt(2/pi) 0.044715
+constexpr float kNegLog2e = -1.4426950408889634f;
 
-// (operation order as in torch's GeluCUDAKernelImpl / GeluBackwardCUDAKernelImpl)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// e = exp(-2u), clamped at 2^80 so that e * s stays finite for very negative x
+__device__ __forceinline__ float gelu_e(float x, float x_sq) {
+  const float t = x * fmaf(kC1 * kNegLog2e, x_sq, kC0 * kNegLog2e);
+  return ex2_approx(fminf(t, 80.f));
+}
+
 __device__ __forceinline__ float gelu_f(float x) {
-  const float x_cube = x * x * x;
-  const float inner = kBeta * (x + kKappa * x_cube);
-  return 0.5f * x * (1.f + tanhf(inner));
+  const float e = gelu_e(x, x * x);
+  return x * rcp_approx(1.f + e);
 }
 
 __device__ __forceinline__ float gelu_grad_f(float dy, float x) {
   const float x_sq = x * x;
-  const float x_cube = x_sq * x;
-  const float t = tanhf(kBeta * (x + kKappa * x_cube));
-  const float left = 0.5f * x, right = 1.f + t;
-  const float left_d = 0.5f * right;
-  const float tanh_d = 1.f - t * t;
-  const float inner_d = kBeta * (1.f + 3.f * kKappa * x_sq);
-  const float right_d = left * tanh_d * inner_d;
-  return dy * (left_d + right_d);
+  const float e = gelu_e(x, x_sq);
+  const float s = rcp_approx(1.f + e);
+  const float du = fmaf(3.f * kC1, x_sq, kC0);
+  return dy * (s * fmaf(x * e * s, du, 1.f));
 }
 
 // What a column-sum pass sums, per element: the bias gradient sums g itself;
@@ -105,8 +127,11 @@ struct GeluBwd {
   }
 };
 
+// 4 CTAs per SM (<= 64 registers): plan_colsum sizes the grid to one full
+// wave of 148 * 4 CTAs; at 3 resident CTAs (75 registers, the GELU backward
+// before the bound) the same grid ran 1.3 waves
 template <class Op, int V>
-__global__ void __launch_bounds__(32 * kRowLanes) colsum_kernel(Op op, int64_t rows, int64_t n,
+__global__ void __launch_bounds__(32 * kRowLanes, 4) colsum_kernel(Op op, int64_t rows, int64_t n,
                                                                 int64_t chunk_rows,
                                                                 float* __restrict__ partial) {
   __shared__ float red[kRowLanes][32 * V];
@@ -178,23 +203,30 @@ __global__ void __launch_bounds__(256) colsum_finalize_kernel(const float* __res
   }
 }
 
+// grid-stride; the vector form keeps two 16-byte loads in flight per thread
 template <int V>
 __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                 int64_t n) {
   const int64_t items = n / V;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < items;
-       t += stride) {
-    if constexpr (V == 8) {
-      float f[8];
-      ld8(x + t * 8, f);
-      __nv_bfloat16 o[8];
+  int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if constexpr (V == 8) {
+    for (; t < items; t += 2 * stride) {
+      const bool two = t + stride < items;
+      float f[2][8];
+      ld8(x + t * 8, f[0]);
+      if (two) ld8(x + (t + stride) * 8, f[1]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16_rn(gelu_f(f[i]));
-      *reinterpret_cast<uint4*>(y + t * 8) = *reinterpret_cast<const uint4*>(o);
-    } else {
-      y[t] = __float2bfloat16_rn(gelu_f(__bfloat162float(x[t])));
+      for (int k = 0; k < 2; ++k) {
+        if (k == 1 && !two) break;
+        __nv_bfloat16 o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = __float2bfloat16_rn(gelu_f(f[k][i]));
+        *reinterpret_cast<uint4*>(y + (t + k * stride) * 8) = *reinterpret_cast<const uint4*>(o);
+      }
     }
+  } else {
+    for (; t < items; t += stride) y[t] = __float2bfloat16_rn(gelu_f(__bfloat162float(x[t])));
   }
 }
 

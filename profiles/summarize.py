@@ -38,6 +38,8 @@ def full_summary(rep: str, algo_bytes: dict[str, float], config: str) -> dict:
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
         key = ("het_adamw" if "adamw" in name
+               else "het_accumulate_multi_first" if "accumulate_multi_kernel<1" in name
+               else "het_accumulate_multi" if "accumulate_multi_kernel<0" in name
                else "het_accumulate_first" if "accumulate_kernel<1" in name
                else "het_accumulate" if "accumulate" in name
                else "het_gather_bf16" if "gather_bf16" in name
@@ -109,6 +111,8 @@ def main() -> None:
     ap.add_argument("--adamw-bytes", type=float, default=0.0)
     ap.add_argument("--acc-bytes", type=float, default=0.0)
     ap.add_argument("--acc-first-bytes", type=float, default=0.0)
+    ap.add_argument("--acc-multi-bytes", type=float, default=0.0)
+    ap.add_argument("--acc-multi-first-bytes", type=float, default=0.0)
     a = ap.parse_args()
     if a.full:
         algo = {}
@@ -118,6 +122,10 @@ def main() -> None:
             algo["het_accumulate"] = a.acc_bytes
         if a.acc_first_bytes:
             algo["het_accumulate_first"] = a.acc_first_bytes
+        if a.acc_multi_bytes:
+            algo["het_accumulate_multi"] = a.acc_multi_bytes
+        if a.acc_multi_first_bytes:
+            algo["het_accumulate_multi_first"] = a.acc_multi_first_bytes
         summ = full_summary(a.full, algo, a.config)
         dst = HERE / "ncu_summary.json"
         prev = json.loads(dst.read_text()) if dst.exists() else {}

@@ -58,6 +58,31 @@ for n in (789_760, 7_087_872, 12_596_224, 51_384_320, 4 * 7_087_872):
                                          6.0 * n)
     out[f"accumulate_add_{n}"] = timed(lambda: K.accumulate(acc, [(grads[0], 0)], False, 0.5),
                                        10.0 * n)
+for n in (7_087_872, 2 * 7_087_872, 12_596_224, 51_384_320):
+    g16 = torch.randn(n, device=dev).to(torch.bfloat16)
+    dst16 = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    out[f"gather_bf16_{n}"] = timed(lambda: K.gather_bf16(dst16, [(g16, 0)]), 4.0 * n)
+    g2 = [torch.randn(n, device=dev).to(torch.bfloat16) for _ in range(2)]
+    acc = torch.empty(n, device=dev)
+    out[f"accumulate_multi2_first_{n}"] = timed(
+        lambda: K.accumulate_multi(acc, [[g2[0]], [g2[1]]], [0], True, 0.5), 8.0 * n)
+    out[f"accumulate_multi2_add_{n}"] = timed(
+        lambda: K.accumulate_multi(acc, [[g2[0]], [g2[1]]], [0], False, 0.5), 12.0 * n)
+    del g16, dst16, g2, acc
+for rows, n in ((32768, 3072), (16384, 4096)):        # GPT-2 / BERT MLP up-projection
+    pre = torch.randn(rows, n, device=dev).to(torch.bfloat16)
+    dy = torch.randn(rows, n, device=dev).to(torch.bfloat16)
+    y, dpre = torch.empty_like(pre), torch.empty_like(pre)
+    db = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    part = K._colsum_scratch(rows, n, dev)
+    lib = K.load()
+    out[f"gelu_fwd_{rows}x{n}"] = timed(
+        lambda: lib.het_gelu_fwd(pre.data_ptr(), y.data_ptr(), pre.numel(), 0), 4.0 * rows * n)
+    out[f"gelu_bwd_bias_{rows}x{n}"] = timed(
+        lambda: lib.het_gelu_bwd_bias(dy.data_ptr(), pre.data_ptr(), dpre.data_ptr(), rows, n,
+                                      db.data_ptr(), part.data_ptr(), 0), 6.0 * rows * n)
+    out[f"bias_grad_{rows}x{n}"] = timed(lambda: K.bias_grad(dy), 2.0 * rows * n)
+    del pre, dy, y, dpre
 for n in (7_087_872 * 12, 124_082_688, 1_300_000_000 // 4):
     p, g, m, v = (torch.zeros(n, device=dev) for _ in range(4))
     sh = torch.empty(n, dtype=torch.bfloat16, device=dev)
