@@ -19,7 +19,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -53,53 +52,71 @@ def peaks() -> tuple[float, str]:
 
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled while the timed
-    region runs: NVML every 20 ms (nvidia-smi every 200 ms if NVML is absent)."""
+    region runs: NVML every 20 ms (nvidia-smi every 200 ms if NVML is absent),
+    in a separate PROCESS, so the sampler never takes the launching thread's
+    GIL (a sampler thread measurably slowed launch-heavy steps)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
     # NVML clocks-event reason bits, in the order of the query above
     BITS = (0x8, 0x40, 0x20, 0x4)
+    # the sampler process: prints "ready", then one CSV row per sample until stdin closes
+    SCRIPT = r"""
+import subprocess, sys, threading
+idx, q, bits = int(sys.argv[1]), sys.argv[2], [int(b) for b in sys.argv[3].split(",")]
+stop = threading.Event()
+threading.Thread(target=lambda: (sys.stdin.read(), stop.set()), daemon=True).start()
+try:
+    import pynvml as nv
+    nv.nvmlInit()
+    h = nv.nvmlDeviceGetHandleByIndex(idx)
+except Exception:
+    nv = None
+print("ready", flush=True)
+while not stop.is_set():
+    try:
+        if nv is not None:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            row = [str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in bits]
+        else:
+            out = subprocess.run(["nvidia-smi", "-i", str(idx), "--query-gpu=" + q,
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=5).stdout.strip()
+            row = [x.strip() for x in out.split(",")] if out else None
+        if row:
+            print(",".join(row), flush=True)
+    except Exception:
+        pass
+    stop.wait(0.02 if nv is not None else 0.2)
+"""
 
     def __init__(self, index: int):
-        self.index, self.rows, self._stop = index, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _nvml(self):
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
-        except Exception:
-            return None, None
-
-    def _run(self):
-        nv, h = self._nvml()
-        while not self._stop.is_set():
-            try:
-                if nv is not None:
-                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.rows.append([str(sm), str(mx)] +
-                                     ["Active" if rs & b else "Not Active" for b in self.BITS])
-                else:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.02 if nv is not None else 0.2)
+        self.index, self.rows, self._p = index, [], None
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(
+                [sys.executable, "-c", self.SCRIPT, str(self.index), self.Q,
+                 ",".join(str(b) for b in self.BITS)],
+                stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self._p.stdout.readline()           # "ready": sampling before the region starts
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        try:
+            out, _ = self._p.communicate(input="", timeout=10)
+        except Exception:
+            self._p.kill()
+            out = ""
+        self.rows = [line.split(",") for line in out.splitlines() if "," in line]
 
     def summary(self) -> dict:
         if not self.rows:
@@ -250,6 +267,9 @@ def main() -> None:
                     choices=["checkpoints", "reference"],
                     help="checkpoints: only unit-input checkpoints make the host round trip; "
                          "reference: the simulator's full schedule (sim.py:226-338)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as one CUDA graph (auto: on where eligible: "
+                         "one rank, no activation offload)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
                     help="collective route for N>1: 4 = fused symmetric-memory kernels "
                          "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")
@@ -276,6 +296,9 @@ def main() -> None:
                            offload_activations=offload,
                            offload_schedule=args.offload_schedule)
     tr.init_params(seed=0)
+    tr.graph = args.graph != "off" and tr.graph_eligible()
+    if args.graph == "on" and not tr.graph:
+        raise SystemExit("--graph on: the step is not graph-eligible here (N>1 or offload)")
     arch, plan = job.arch, job.plan
     nsteps = args.warmup + args.steps
     host = [torch.from_numpy(rank_tokens(plan, rank, arch.seq, arch.vocab, SEED, s)).pin_memory()
@@ -295,11 +318,16 @@ def main() -> None:
         return float(t)
 
     # ---- device-resident timing (value) ------------------------------------
+    # graph mode: the owned-kernel timers are captured with the step (external
+    # events the replays re-record), so they are on before the warm-up capture and
+    # the summary below reads the last timed replay
+    tr.timers.enabled = tr.graph
     for s in range(args.warmup):
         tr.step(resident[s])
     barrier()
     tr.timers.enabled = True
-    tr.timers.reset()
+    if not tr.graph_active:
+        tr.timers.reset()
     launches0 = K.LAUNCHES
     comp = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -314,6 +342,7 @@ def main() -> None:
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
     kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate", "gather")}
     kern = {k: v for k, v in kern.items() if v["launches"]}
+    steps_timed = 1 if tr.graph_active else args.steps     # graph: the last replay
     tr.timers.enabled = False
 
     # ---- end to end through the public API with host buffers (e2e) --------
@@ -355,7 +384,7 @@ def main() -> None:
         allm = [mem]
     peak_mem = [[round(float(x[0]), 3), round(float(x[1]), 3)] for x in allm]
     # every rank's owned-kernel rates (rank 0's are the line's "kernels")
-    mine = {k: [v["launches"], round(v["gbs"] or 0.0, 1), round(v["ms_total"] / args.steps, 4)]
+    mine = {k: [v["launches"], round(v["gbs"] or 0.0, 1), round(v["ms_total"] / steps_timed, 4)]
             for k, v in kern.items()}
     if world > 1:
         kern_by_rank = [None] * world
@@ -390,6 +419,7 @@ def main() -> None:
                        "peak_vs_cap_gib": peak_mem,
                        # per rank: {kernel: [launches, algorithmic GB/s, ms per step]}
                        "kernels_by_rank": kern_by_rank,
+                       "cuda_graph": tr.graph_active,
                        "activation_offload_ranks": [
                            i for i, a in enumerate(plan.assignments)
                            if args.offload == "on" or (args.offload == "auto"
@@ -410,8 +440,8 @@ def main() -> None:
                          "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
                          "frac": achieved / hbm if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": kern[dom]["bytes_per_launch"],
-                         "step_share": kern[dom]["ms_total"] / args.steps / ms},
-            "kernels": {k: dict(v, ms_per_step=v["ms_total"] / args.steps)
+                         "step_share": kern[dom]["ms_total"] / steps_timed / ms},
+            "kernels": {k: dict(v, ms_per_step=v["ms_total"] / steps_timed)
                         for k, v in kern.items()},
             "gpu_launches": launches,
             "clocks": clocks.summary(),

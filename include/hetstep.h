@@ -85,6 +85,16 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
               double lr, double beta1, double beta2, double eps, double weight_decay,
               int64_t step, void* stream);
 
+/* The 7 fp32 AdamW coefficients het_adamw derives (in double, as torch) for
+ * one step: {1-lr*wd, 1-b1, b2, 1-b2, sqrt(1-b2^t), eps, -lr/(1-b1^t)}. */
+int het_adamw_coef(double lr, double beta1, double beta2, double eps, double weight_decay,
+                   int64_t step, float* out7);
+/* het_adamw with the coefficients read from device memory (coef7_dev, as
+ * het_adamw_coef writes them) instead of kernel arguments: a CUDA graph of the
+ * step replays it unchanged while the host refreshes the 28 bytes per step. */
+int het_adamw_devcoef(float* p, const float* g, float* m, float* v, void* p_bf16_or_null,
+                      int64_t n, const float* coef7_dev, void* stream);
+
 /* (4b) embedding backward fused with layered accumulation of the root unit:
  *   acc[wte_off + t*d + c] += scale * sum_{i : token[i] == t} dy[i, c]
  *   acc[wpe_off + s*d + c] += scale * sum_{i : i % seq == s} dy[i, c]   (wpe_off >= 0)
@@ -99,6 +109,15 @@ int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void*
                        int64_t rows, int64_t d, const int32_t* order, const int32_t* seg_start,
                        const int32_t* seg_token, int64_t nseg, int64_t seq, float scale,
                        void* stream);
+
+/* (4b') the same without a host round trip (CUDA-graph capturable): the run
+ * count stays on the device (*nseg_dev), rows bounds it (one CTA per possible
+ * run; CTAs past the live count exit), and sorted_tok is the stably sorted
+ * token array, read at each run's start seg_start[b]. */
+int het_embedding_grad_dev(float* acc, int64_t wte_off, int64_t wpe_off, const void* dy_bf16,
+                           int64_t rows, int64_t d, const int32_t* order,
+                           const int32_t* seg_start, const int32_t* sorted_tok,
+                           const int32_t* nseg_dev, int64_t seq, float scale, void* stream);
 
 /* Fused LayerNorm of the transformer units (bf16 activations, fp32 stats),
  * d in {256, 768, 1024}. Forward writes y, per-row mean and rstd; backward

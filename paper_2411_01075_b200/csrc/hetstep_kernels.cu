@@ -385,7 +385,9 @@ __global__ void __launch_bounds__(kThreads) adamw_vec_kernel(float4* __restrict_
                                                              float4* __restrict__ m,
                                                              float4* __restrict__ v,
                                                              uint2* __restrict__ shadow,
-                                                             int64_t n4, AdamCoef c) {
+                                                             int64_t n4, AdamCoef c,
+                                                             const AdamCoef* __restrict__ cdev) {
+  if (cdev != nullptr) c = *cdev;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += 2 * stride) {
@@ -428,7 +430,9 @@ __global__ void __launch_bounds__(kThreads) adamw_v8_kernel(float* __restrict__ 
                                                             float* __restrict__ m,
                                                             float* __restrict__ v,
                                                             uint4* __restrict__ shadow,
-                                                            int64_t n8, AdamCoef c) {
+                                                            int64_t n8, AdamCoef c,
+                                                            const AdamCoef* __restrict__ cdev) {
+  if (cdev != nullptr) c = *cdev;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
        i += stride) {
@@ -446,7 +450,9 @@ __global__ void __launch_bounds__(kThreads) adamw_v8_kernel(float* __restrict__ 
 
 __global__ void adamw_scalar_kernel(float* __restrict__ p, const float* __restrict__ g,
                                     float* __restrict__ m, float* __restrict__ v,
-                                    __nv_bfloat16* __restrict__ shadow, int64_t n, AdamCoef c) {
+                                    __nv_bfloat16* __restrict__ shadow, int64_t n, AdamCoef c,
+                                    const AdamCoef* __restrict__ cdev) {
+  if (cdev != nullptr) c = *cdev;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += stride) {
@@ -469,8 +475,17 @@ __global__ void __launch_bounds__(kThreads) embedding_grad_kernel(
     float* __restrict__ acc, int64_t wte_off, int64_t wpe_off,
     const __nv_bfloat16* __restrict__ dy, int64_t rows, int64_t d,
     const int32_t* __restrict__ order, const int32_t* __restrict__ seg_start,
-    const int32_t* __restrict__ seg_token, int64_t nseg, int64_t seq, float w) {
-  const int64_t b = blockIdx.x;
+    const int32_t* __restrict__ seg_token, int64_t nseg, int64_t seq, float w,
+    const int32_t* __restrict__ nseg_dev) {
+  int64_t b = blockIdx.x;
+  if (nseg_dev != nullptr) {
+    // device-side run count: blocks [0, nseg) are token runs (nseg = the host's
+    // upper bound on runs), blocks past the live count exit; seg_token is the
+    // sorted token array, read at each run's start
+    if (b < nseg) {
+      if (b >= *nseg_dev) return;
+    }
+  }
   for (int64_t c0 = static_cast<int64_t>(threadIdx.x) * kVecE; c0 < d;
        c0 += static_cast<int64_t>(blockDim.x) * kVecE) {
     float sum[kVecE];
@@ -491,7 +506,8 @@ __global__ void __launch_bounds__(kThreads) embedding_grad_kernel(
     int64_t dst;
     if (b < nseg) {
       for (int32_t i = seg_start[b]; i < seg_start[b + 1]; ++i) add_row(order[i]);
-      dst = wte_off + static_cast<int64_t>(seg_token[b]) * d + c0;
+      const int32_t tok = nseg_dev != nullptr ? seg_token[seg_start[b]] : seg_token[b];
+      dst = wte_off + static_cast<int64_t>(tok) * d + c0;
     } else {
       const int64_t s = b - nseg;
       for (int64_t r = s; r < rows; r += seq) add_row(r);
@@ -673,13 +689,10 @@ int het_gather_bf16(void* dst, const het_seg_t* segs, int nseg, void* stream) {
   return het::check_launch("het_gather_bf16");
 }
 
-int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
-              double lr, double beta1, double beta2, double eps, double weight_decay,
-              int64_t step, void* stream) {
-  if (n < 0 || step < 1 || (n > 0 && (!p || !g || !m || !v)))
-    return fail(HET_EARG, "het_adamw: bad args (n=%lld step=%lld)", (long long)n,
-                (long long)step);
-  if (n == 0) return HET_OK;
+int het_adamw_coef(double lr, double beta1, double beta2, double eps, double weight_decay,
+                   int64_t step, float* out7) {
+  if (step < 1 || !out7) return fail(HET_EARG, "het_adamw_coef: bad args (step=%lld)",
+                                     (long long)step);
   // scalar coefficients in double, as torch's _single_tensor_adamw computes them
   const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
   const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
@@ -691,6 +704,15 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
   c.bc2_sqrt = static_cast<float>(std::sqrt(bc2));
   c.eps = static_cast<float>(eps);
   c.neg_step = static_cast<float>(-(lr / bc1));
+  static_assert(sizeof(AdamCoef) == 7 * sizeof(float), "AdamCoef layout");
+  std::memcpy(out7, &c, sizeof(c));
+  return HET_OK;
+}
+
+namespace {
+
+int adamw_launch(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
+                 const AdamCoef& c, const AdamCoef* cdev, void* stream, const char* what) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool wide = n % 8 == 0 && aligned32(p) && aligned32(g) && aligned32(m) && aligned32(v) &&
                     (!p_bf16_or_null || aligned16(p_bf16_or_null));
@@ -700,10 +722,10 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
     const int64_t n8 = n / 8;
     const int grid = het::grid_for(n8, kThreads);
     if (p_bf16_or_null)
-      adamw_v8_kernel<true><<<grid, kThreads, 0, st>>>(p, g, m, v,
-                                                       static_cast<uint4*>(p_bf16_or_null), n8, c);
+      adamw_v8_kernel<true><<<grid, kThreads, 0, st>>>(
+          p, g, m, v, static_cast<uint4*>(p_bf16_or_null), n8, c, cdev);
     else
-      adamw_v8_kernel<false><<<grid, kThreads, 0, st>>>(p, g, m, v, nullptr, n8, c);
+      adamw_v8_kernel<false><<<grid, kThreads, 0, st>>>(p, g, m, v, nullptr, n8, c, cdev);
   } else if (vec) {
     const int64_t n4 = n / 4;
     const int grid = het::grid_for((n4 + 1) / 2, kThreads);
@@ -711,16 +733,40 @@ int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null
       adamw_vec_kernel<true><<<grid, kThreads, 0, st>>>(
           reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
           reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
-          static_cast<uint2*>(p_bf16_or_null), n4, c);
+          static_cast<uint2*>(p_bf16_or_null), n4, c, cdev);
     else
       adamw_vec_kernel<false><<<grid, kThreads, 0, st>>>(
           reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
-          reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), nullptr, n4, c);
+          reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), nullptr, n4, c, cdev);
   } else {
     adamw_scalar_kernel<<<het::grid_for(n, kThreads), kThreads, 0, st>>>(
-        p, g, m, v, static_cast<__nv_bfloat16*>(p_bf16_or_null), n, c);
+        p, g, m, v, static_cast<__nv_bfloat16*>(p_bf16_or_null), n, c, cdev);
   }
-  return het::check_launch("het_adamw");
+  return het::check_launch(what);
+}
+
+}  // namespace
+
+int het_adamw(float* p, const float* g, float* m, float* v, void* p_bf16_or_null, int64_t n,
+              double lr, double beta1, double beta2, double eps, double weight_decay,
+              int64_t step, void* stream) {
+  if (n < 0 || step < 1 || (n > 0 && (!p || !g || !m || !v)))
+    return fail(HET_EARG, "het_adamw: bad args (n=%lld step=%lld)", (long long)n,
+                (long long)step);
+  if (n == 0) return HET_OK;
+  AdamCoef c;
+  het_adamw_coef(lr, beta1, beta2, eps, weight_decay, step, reinterpret_cast<float*>(&c));
+  return adamw_launch(p, g, m, v, p_bf16_or_null, n, c, nullptr, stream, "het_adamw");
+}
+
+int het_adamw_devcoef(float* p, const float* g, float* m, float* v, void* p_bf16_or_null,
+                      int64_t n, const float* coef7_dev, void* stream) {
+  if (n < 0 || !coef7_dev || (n > 0 && (!p || !g || !m || !v)))
+    return fail(HET_EARG, "het_adamw_devcoef: bad args (n=%lld)", (long long)n);
+  if (n == 0) return HET_OK;
+  AdamCoef unused{};
+  return adamw_launch(p, g, m, v, p_bf16_or_null, n, unused,
+                      reinterpret_cast<const AdamCoef*>(coef7_dev), stream, "het_adamw_devcoef");
 }
 
 int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void* dy_bf16,
@@ -735,8 +781,24 @@ int het_embedding_grad(float* acc, int64_t wte_off, int64_t wpe_off, const void*
   embedding_grad_kernel<<<static_cast<unsigned>(blocks), kThreads, 0,
                           static_cast<cudaStream_t>(stream)>>>(
       acc, wte_off, wpe_off, static_cast<const __nv_bfloat16*>(dy_bf16), rows, d, order,
-      seg_start, seg_token, nseg, seq, scale);
+      seg_start, seg_token, nseg, seq, scale, nullptr);
   return het::check_launch("het_embedding_grad");
+}
+
+int het_embedding_grad_dev(float* acc, int64_t wte_off, int64_t wpe_off, const void* dy_bf16,
+                           int64_t rows, int64_t d, const int32_t* order,
+                           const int32_t* seg_start, const int32_t* sorted_tok,
+                           const int32_t* nseg_dev, int64_t seq, float scale, void* stream) {
+  if (!acc || !dy_bf16 || rows < 0 || d <= 0 || seq <= 0 || wte_off < 0 ||
+      (rows > 0 && (!order || !seg_start || !sorted_tok || !nseg_dev)))
+    return fail(HET_EARG, "het_embedding_grad_dev: bad args");
+  if (rows == 0) return HET_OK;
+  const int64_t blocks = rows + (wpe_off >= 0 ? seq : 0);   // rows bounds the token runs
+  embedding_grad_kernel<<<static_cast<unsigned>(blocks), kThreads, 0,
+                          static_cast<cudaStream_t>(stream)>>>(
+      acc, wte_off, wpe_off, static_cast<const __nv_bfloat16*>(dy_bf16), rows, d, order,
+      seg_start, sorted_tok, rows, seq, scale, nseg_dev);
+  return het::check_launch("het_embedding_grad_dev");
 }
 
 int het_tune(int key, int value) {

@@ -36,7 +36,8 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
-           "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi")
+           "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi",
+           "het_embedding_grad_dev", "het_adamw_coef", "het_adamw_devcoef")
 
 
 class HetSeg(ctypes.Structure):
@@ -69,6 +70,8 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_accumulate": ([vp, ctypes.POINTER(HetSeg), i32, i32, f32, vp], i32),
         "het_accumulate_multi": ([vp, ctypes.POINTER(HetSeg), i32, i32, i32, f32, vp], i32),
         "het_adamw": ([vp, vp, vp, vp, vp, i64, f64, f64, f64, f64, f64, i64, vp], i32),
+        "het_adamw_coef": ([f64, f64, f64, f64, f64, i64, ctypes.POINTER(f32)], i32),
+        "het_adamw_devcoef": ([vp, vp, vp, vp, vp, i64, vp, vp], i32),
         "het_fill_f32": ([vp, f32, i64, vp], i32),
         "het_tune": ([i32, i32], i32),
         "het_layernorm_partial_floats": ([i64], i64),
@@ -96,6 +99,8 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_gelu_bwd_bias": ([vp, vp, vp, i64, i64, vp, vp, vp], i32),
         "het_swiglu_bwd": ([vp, vp, vp, i64, vp, vp, i64, i64, i64, vp], i32),
         "het_embedding_grad": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, i64, i64, f32, vp], i32),
+        "het_embedding_grad_dev": ([vp, i64, i64, vp, i64, i64, vp, vp, vp, vp, i64, f32, vp],
+                                   i32),
         "het_comm_unique_id": ([ctypes.c_char_p], i32),
         "het_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, i32, i32], i32),
         "het_comm_destroy": ([vp], i32),
@@ -131,7 +136,8 @@ def version() -> str:
 
 LAUNCHES = 0      # owned kernel launches issued by this process (incl. model-side kernels)
 _NOT_LAUNCHES = ("het_comm_unique_id", "het_comm_init", "het_comm_destroy", "het_tune",
-                 "het_symm_status", "het_allgather_uneven", "het_reduce_scatter_uneven")  # NCCL
+                 "het_symm_status", "het_allgather_uneven", "het_reduce_scatter_uneven",  # NCCL
+                 "het_adamw_coef")                                                 # host-only
 
 
 def _check(rc: int, what: str) -> None:
@@ -313,6 +319,32 @@ def adamw(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,
            "het_adamw")
 
 
+def adamw_coef(*, lr: float, beta1: float, beta2: float, eps: float, weight_decay: float,
+               step: int) -> list[float]:
+    """The 7 fp32 coefficients het_adamw derives for `step` (het_adamw_coef)."""
+    out = (ctypes.c_float * 7)()
+    _check(load().het_adamw_coef(lr, beta1, beta2, eps, weight_decay, int(step), out),
+           "het_adamw_coef")
+    return list(out)
+
+
+def adamw_devcoef(p: torch.Tensor, g: torch.Tensor, m: torch.Tensor, v: torch.Tensor,
+                  shadow: torch.Tensor | None, coef: torch.Tensor, stream=None) -> None:
+    """het_adamw with its coefficients read from `coef` (7 fp32 on the device,
+    as adamw_coef returns them): the form a captured CUDA graph replays."""
+    n = p.numel()
+    if not (g.numel() == m.numel() == v.numel() == n) or (shadow is not None and
+                                                        shadow.numel() != n):
+        raise InputError("adamw: size mismatch")
+    if coef.numel() != 7:
+        raise InputError("adamw_devcoef: coef holds 7 floats")
+    sh = _cuda(shadow, torch.bfloat16, "shadow") if shadow is not None else None
+    _check(load().het_adamw_devcoef(_cuda(p, torch.float32, "p"), _cuda(g, torch.float32, "g"),
+                                    _cuda(m, torch.float32, "m"), _cuda(v, torch.float32, "v"),
+                                    sh, n, _cuda(coef, torch.float32, "coef"), _stream(stream)),
+           "het_adamw_devcoef")
+
+
 def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: torch.Tensor,
                    tokens: torch.Tensor, seq: int, scale: float, stream=None) -> None:
     """Fused embedding backward + layered accumulate into the fp32 root
@@ -322,18 +354,28 @@ def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: tor
     tok = tokens.reshape(-1)
     if tok.numel() != rows:
         raise InputError("embedding_grad: one token per gradient row")
-    srt, order = torch.sort(tok.to(torch.int64), stable=True)
-    uniq, counts = torch.unique_consecutive(srt, return_counts=True)
-    seg = torch.zeros(uniq.numel() + 1, dtype=torch.int32, device=dy.device)
-    torch.cumsum(counts, 0, out=seg[1:])
+    if rows == 0:
+        return
+    # token runs of the stably sorted ids, built on the device without a host
+    # round trip (no data-dependent shapes): run id per sorted row by a cumsum of
+    # "differs from the previous id", run starts by a min-scatter, run count on
+    # the device (het_embedding_grad_dev)
+    dev = dy.device
+    srt, order = torch.sort(tok.to(torch.int32), stable=True)
+    newrun = torch.ones(rows, dtype=torch.int32, device=dev)
+    torch.ne(srt[1:], srt[:-1], out=newrun[1:])
+    rid = torch.cumsum(newrun, 0, dtype=torch.int32)         # 1-based run id
+    pos = torch.arange(rows, dtype=torch.int32, device=dev)
+    seg = torch.full((rows + 1,), rows, dtype=torch.int32, device=dev)
+    seg.scatter_reduce_(0, (rid - 1).to(torch.int64), pos, reduce="amin")
+    nseg = rid[-1:]
     order32 = order.to(torch.int32)
-    uniq32 = uniq.to(torch.int32)
     dyc = dy.reshape(rows, d).contiguous()
-    _check(load().het_embedding_grad(
+    _check(load().het_embedding_grad_dev(
         _cuda(acc, torch.float32, "acc"), int(wte_off), -1 if wpe_off is None else int(wpe_off),
         _cuda(dyc, torch.bfloat16, "dy"), rows, d, order32.data_ptr(), seg.data_ptr(),
-        uniq32.data_ptr(), uniq.numel(), int(seq), float(scale), _stream(stream)),
-        "het_embedding_grad")
+        srt.data_ptr(), nseg.data_ptr(), int(seq), float(scale), _stream(stream)),
+        "het_embedding_grad_dev")
 
 
 HET_TUNE_ACC_VARIANT = 1

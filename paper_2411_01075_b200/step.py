@@ -63,6 +63,7 @@ class AdamWConfig:
 class StepTimers:
     """CUDA events around the owned kernels (enabled for roofline runs)."""
     enabled: bool = False
+    external: bool = False     # events recorded inside a CUDA-graph capture
     adamw: list = field(default_factory=list)
     accumulate: list = field(default_factory=list)
     gather: list = field(default_factory=list)
@@ -71,7 +72,8 @@ class StepTimers:
         """Start/end events for one launch moving `nbytes` algorithmic bytes."""
         if not self.enabled:
             return None, None
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a = torch.cuda.Event(enable_timing=True, external=self.external)
+        b = torch.cuda.Event(enable_timing=True, external=self.external)
         getattr(self, kind).append((a, b, nbytes))
         return a, b
 
@@ -211,8 +213,11 @@ class UnevenFSDPTrainer:
             self._acc_pair = torch.zeros(2 * pad_u, dtype=torch.float32, device=dev)
             self.acc = [self._acc_pair[:U], self._acc_pair[pad_u:pad_u + U]]
             self.racc = torch.zeros(E, dtype=torch.float32, device=dev)
-        self.ag_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
-        self.rs_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
+        # collective streams at high priority: their CTAs (fused kernels or NCCL's)
+        # go ahead of pending compute CTAs, so a full-GPU rank's GEMMs do not hold
+        # back the gather or reduce the other ranks are waiting on
+        self.ag_stream = torch.cuda.Stream(device=dev, priority=-1) if self.cuda else _NoStream()
+        self.rs_stream = torch.cuda.Stream(device=dev, priority=-1) if self.cuda else _NoStream()
         self.unit_seg = segment_offsets(arch.unit_layout())
         self.root_seg = segment_offsets(arch.root_layout())
         self.steps = 0
@@ -232,6 +237,15 @@ class UnevenFSDPTrainer:
         if offload_schedule not in ("reference", "checkpoints"):
             raise InputError(f"unknown offload schedule {offload_schedule!r}")
         self.offload_schedule = offload_schedule
+        # CUDA graph of the whole step (one rank, no offload, no tracer): after
+        # `graph_warmup` eager steps the step is captured once and then replayed;
+        # the host only copies the tokens in and refreshes AdamW's 7 coefficients
+        # (het_adamw_devcoef), so the ~550 launches of a GPT-2 step cost one
+        self.graph = False
+        self.graph_warmup = 2
+        self._graph = None
+        self._graph_launches = 0
+        self._eager_steps = 0
         if self.offload:
             self.d2h_stream = torch.cuda.Stream(device=dev)
             self.h2d_stream = torch.cuda.Stream(device=dev)
@@ -555,6 +569,74 @@ class UnevenFSDPTrainer:
         """One iteration on this rank's [b_i, seq+1] int32 token block (device).
         Returns this rank's Eq. 1-weighted loss contribution sum_k (m_i/B) loss_k
         (a device scalar; the global loss is its sum over ranks)."""
+        if self.graph and self.graph_eligible():
+            return self._graph_step(tok)
+        self._eager_steps += 1
+        return self._step(tok)
+
+    def graph_eligible(self) -> bool:
+        return (self.cuda and self.N == 1 and not self.offload and self.tracer is None
+                and self.m > 0)
+
+    @property
+    def graph_active(self) -> bool:
+        return self._graph is not None
+
+    def _graph_step(self, tok: torch.Tensor) -> torch.Tensor:
+        if self._graph is None and self._eager_steps < self.graph_warmup:
+            self._eager_steps += 1
+            return self._step(tok)
+        if self._graph is None:
+            self._capture(tok)
+        self._g_tok.copy_(tok, non_blocking=True)
+        self._stage_coef()
+        self._graph.replay()
+        self.steps += 1
+        K.LAUNCHES += self._graph_launches
+        self.launches += self._graph_own
+        return self._g_loss.clone()
+
+    def _stage_coef(self) -> None:
+        """AdamW coefficients of the coming step into the device buffer the graph's
+        het_adamw_devcoef reads: host math (het_adamw_coef, as het_adamw), a pinned
+        slot per step from a small ring (an event guards each slot's reuse), and
+        an async H2D copy stream-ordered before the replay."""
+        k = self.steps % len(self._coef_pin)
+        self._coef_ev[k].synchronize()
+        c = K.adamw_coef(lr=self.opt.lr, beta1=self.opt.betas[0], beta2=self.opt.betas[1],
+                         eps=self.opt.eps, weight_decay=self.opt.weight_decay,
+                         step=self.steps + 1)
+        self._coef_pin[k].copy_(torch.tensor(c, dtype=torch.float32))
+        self._coef_dev.copy_(self._coef_pin[k], non_blocking=True)
+        self._coef_ev[k].record()
+
+    def _capture(self, tok: torch.Tensor) -> None:
+        self._g_tok = torch.empty_like(tok)
+        self._g_tok.copy_(tok)
+        self._coef_dev = torch.zeros(7, dtype=torch.float32, device=self.device)
+        self._coef_pin = [torch.zeros(7, dtype=torch.float32).pin_memory() for _ in range(4)]
+        self._coef_ev = [torch.cuda.Event() for _ in range(4)]
+        for ev in self._coef_ev:
+            ev.record()
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        timers_on = self.timers.enabled
+        if timers_on:           # the replays re-record these (external) events
+            self.timers.reset()
+            self.timers.external = True
+        n0, s0, l0 = K.LAUNCHES, self.steps, self.launches
+        try:
+            with torch.cuda.graph(g):
+                self._g_loss = self._step(self._g_tok, coef=self._coef_dev)
+        finally:
+            self.timers.external = False
+        # the capture issued no work: every replay counts the captured launches
+        self._graph_launches = K.LAUNCHES - n0
+        self._graph_own = self.launches - l0
+        K.LAUNCHES, self.steps, self.launches = n0, s0, l0
+        self._graph = g
+
+    def _step(self, tok: torch.Tensor, coef: torch.Tensor | None = None) -> torch.Tensor:
         arch, L, comp = self.arch, self.L, self._current()
         nb, root = L.blocks, L.root
         if self.m > 0 and (tok.shape[0] != self.m * self.l or tok.shape[1] != arch.seq + 1):
@@ -783,9 +865,12 @@ class UnevenFSDPTrainer:
             a.record()
         shadow = self.p16 if self.need_shadow else None   # fused AG reads p32 itself
         with self._span("optimizer", root, 0, "opt", comp):
-            K.adamw(self.p32, self.g32, self.m32, self.v32, shadow, lr=self.opt.lr,
-                    beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
-                    weight_decay=self.opt.weight_decay, step=self.steps)
+            if coef is not None:        # graph capture: coefficients staged per replay
+                K.adamw_devcoef(self.p32, self.g32, self.m32, self.v32, shadow, coef)
+            else:
+                K.adamw(self.p32, self.g32, self.m32, self.v32, shadow, lr=self.opt.lr,
+                        beta1=self.opt.betas[0], beta2=self.opt.betas[1], eps=self.opt.eps,
+                        weight_decay=self.opt.weight_decay, step=self.steps)
         if b is not None:
             b.record()
         self.launches += 1

@@ -168,3 +168,35 @@ def test_llama_unit_step_matches_cpu_oracle(cuda):
     for u, ref in enumerate(gu + [gr]):
         off, cnt = tr.L.local_range(u)
         assert _nrel(tr.g32[off:off + cnt].cpu().numpy(), ref.numpy()) <= 2e-2, f"unit {u}"
+
+
+@pytest.mark.parametrize("m,l", [(4, 1), (2, 3)])
+def test_cuda_graph_step_matches_eager(cuda, m, l):
+    """The N=1 step replayed as one CUDA graph (tokens copied into the captured
+    input, AdamW coefficients staged per replay through het_adamw_devcoef) is
+    bitwise the eager step, step after step, and counts its owned launches."""
+    from paper_2411_01075_b200 import hetstep as K
+    arch = ARCHS["gpt2_small"]
+    plan = one_gpu_plan(arch, m, l)
+    toks = [torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=4, step=s)).to(cuda)
+            for s in range(6)]
+    res = {}
+    torch.use_deterministic_algorithms(True)
+    try:
+        for graph in (False, True):
+            tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda)
+            tr.init_params(seed=2)
+            tr.graph = graph
+            n0 = K.LAUNCHES
+            losses = [float(tr.step(t)) for t in toks]
+            torch.cuda.synchronize()
+            res[graph] = (losses, tr.p32.clone(), tr.v32.clone(), K.LAUNCHES - n0, tr.steps,
+                          tr.graph_active)
+            del tr
+    finally:
+        torch.use_deterministic_algorithms(False)
+    assert res[True][5] and not res[False][5]
+    assert res[True][0] == res[False][0]
+    assert torch.equal(res[True][1], res[False][1])
+    assert torch.equal(res[True][2], res[False][2])
+    assert res[True][3] == res[False][3] and res[True][4] == res[False][4] == 6
