@@ -467,4 +467,20 @@ def main() -> None:
 
 
 if __name__ == "__main__":
-    main()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # tight emulated HBM caps (layered-GA tiers of 1.5-2.5 GiB): expandable
+        # segments keep the caching allocator from failing on fragmentation.
+        # Set before the first CUDA allocation.
+        os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+        try:
+            main()
+        except BaseException:
+            # one failed rank must not leave the others blocked in a collective
+            # (or this process in communicator teardown): report and leave at once,
+            # so the launcher tears the job down
+            import traceback
+            traceback.print_exc()
+            sys.stderr.flush()
+            os._exit(1)
+    else:
+        main()

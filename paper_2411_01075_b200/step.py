@@ -213,11 +213,8 @@ class UnevenFSDPTrainer:
             self._acc_pair = torch.zeros(2 * pad_u, dtype=torch.float32, device=dev)
             self.acc = [self._acc_pair[:U], self._acc_pair[pad_u:pad_u + U]]
             self.racc = torch.zeros(E, dtype=torch.float32, device=dev)
-        # collective streams at high priority: their CTAs (fused kernels or NCCL's)
-        # go ahead of pending compute CTAs, so a full-GPU rank's GEMMs do not hold
-        # back the gather or reduce the other ranks are waiting on
-        self.ag_stream = torch.cuda.Stream(device=dev, priority=-1) if self.cuda else _NoStream()
-        self.rs_stream = torch.cuda.Stream(device=dev, priority=-1) if self.cuda else _NoStream()
+        self.ag_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
+        self.rs_stream = torch.cuda.Stream(device=dev) if self.cuda else _NoStream()
         self.unit_seg = segment_offsets(arch.unit_layout())
         self.root_seg = segment_offsets(arch.root_layout())
         self.steps = 0
