@@ -267,6 +267,9 @@ def main() -> None:
                     choices=["checkpoints", "reference"],
                     help="checkpoints: only unit-input checkpoints make the host round trip; "
                          "reference: the simulator's full schedule (sim.py:226-338)")
+    ap.add_argument("--no-kernel-timers", action="store_true",
+                    help="no per-launch CUDA events around the owned kernels in the timed "
+                         "region (no roofline line)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as one CUDA graph (auto: on where eligible: "
                          "one rank, no activation offload)")
@@ -296,6 +299,7 @@ def main() -> None:
                            offload_activations=offload,
                            offload_schedule=args.offload_schedule)
     tr.init_params(seed=0)
+    torch.cuda.empty_cache()     # the full-model init temporaries, before the capped steps
     tr.graph = args.graph != "off" and tr.graph_eligible()
     if args.graph == "on" and not tr.graph:
         raise SystemExit("--graph on: the step is not graph-eligible here (N>1 or offload)")
@@ -325,10 +329,24 @@ def main() -> None:
     for s in range(args.warmup):
         tr.step(resident[s])
     barrier()
-    tr.timers.enabled = True
+    # under a tight emulated HBM cap the caching allocator can still be
+    # reshuffling its segments (each "alloc retry" frees its cache and
+    # synchronises): keep warming up, at most 12 more steps, until one step
+    # runs with no retry on any rank
+    extra_warmup = 0
+    while extra_warmup < 12:
+        r0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
+        tr.step(resident[(args.warmup + extra_warmup) % len(resident)])
+        extra_warmup += 1
+        barrier()
+        if max_over_ranks(float(torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
+                                - r0)) == 0:
+            break
+    tr.timers.enabled = not args.no_kernel_timers
     if not tr.graph_active:
         tr.timers.reset()
     launches0 = K.LAUNCHES
+    retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     comp = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -339,6 +357,7 @@ def main() -> None:
         t1.record(comp)
         barrier()
     launches = K.LAUNCHES - launches0
+    retries_timed = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
     kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate", "gather")}
     kern = {k: v for k, v in kern.items() if v["launches"]}
@@ -375,14 +394,21 @@ def main() -> None:
             json.dump(trace_report, fh, indent=1)
     ctx.__exit__(None, None, None)
     # per-rank peak of the caching allocator against the emulated HBM cap
+    ms_ = torch.cuda.memory_stats(dev)
     mem = torch.tensor([torch.cuda.max_memory_allocated(dev) / 2 ** 30,
-                        emu.memory_cap_bytes / 2 ** 30], device=dev, dtype=torch.float64)
+                        emu.memory_cap_bytes / 2 ** 30,
+                        torch.cuda.max_memory_reserved(dev) / 2 ** 30,
+                        float(ms_.get("num_alloc_retries", 0)), float(retries_timed)],
+                       device=dev, dtype=torch.float64)
     if world > 1:
         allm = [torch.zeros_like(mem) for _ in range(world)]
         dist.all_gather(allm, mem)
     else:
         allm = [mem]
-    peak_mem = [[round(float(x[0]), 3), round(float(x[1]), 3)] for x in allm]
+    # per rank: [peak allocated GiB, cap GiB, peak reserved GiB, allocator retries
+    # (whole run), allocator retries inside the device-timed region]
+    peak_mem = [[round(float(x[0]), 3), round(float(x[1]), 3), round(float(x[2]), 3),
+                 int(x[3]), int(x[4])] for x in allm]
     # every rank's owned-kernel rates (rank 0's are the line's "kernels")
     mine = {k: [v["launches"], round(v["gbs"] or 0.0, 1), round(v["ms_total"] / steps_timed, 4)]
             for k, v in kern.items()}
@@ -395,6 +421,9 @@ def main() -> None:
     B = plan.total_batch
     hbm, hbm_kind = peaks()
     # dominant owned kernel = the one with the largest share of the timed steps
+    if not kern:                              # --no-kernel-timers
+        kern = {"adamw": {"launches": 0, "ms_total": 0.0, "ms_mean": 0.0, "bytes_total": 0.0,
+                          "bytes_per_launch": 0.0, "gbs": None}}
     dom = max(kern, key=lambda k: kern[k]["ms_total"])
     achieved = kern[dom]["gbs"]
     traffic = traffic_from_profile(dom, kern[dom]["bytes_per_launch"])
@@ -420,6 +449,7 @@ def main() -> None:
                        # per rank: {kernel: [launches, algorithmic GB/s, ms per step]}
                        "kernels_by_rank": kern_by_rank,
                        "cuda_graph": tr.graph_active,
+                       "extra_warmup_steps": extra_warmup,
                        "activation_offload_ranks": [
                            i for i, a in enumerate(plan.assignments)
                            if args.offload == "on" or (args.offload == "auto"

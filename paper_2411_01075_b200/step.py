@@ -250,6 +250,9 @@ class UnevenFSDPTrainer:
             # checkpoint of unit u, "grad" = the upstream gradient of unit u
             self._host: dict[tuple[str, int, int], torch.Tensor] = {}
             self._off_ev: dict[tuple[str, int, int], torch.cuda.Event] = {}
+            # checkpoint prefetch staging (schedule "checkpoints"): two unit slots
+            self._pf_slot: list[list[torch.Tensor] | None] = [None, None]
+            self._pf_free: list[torch.cuda.Event | None] = [None, None]
 
     # ------------------------------------------------------------------ routes
     def _set_routes(self, sym: bool) -> None:
@@ -417,8 +420,31 @@ class UnevenFSDPTrainer:
         return t, ev
 
     def _prefetch_unit(self, u: int, nmb: int) -> tuple[list[torch.Tensor], torch.cuda.Event]:
-        """All microbatch inputs of unit u back to the GPU (one unit of look-ahead)."""
-        out = [self._fetch("act", k, u, "bwd")[0] for k in range(nmb)]
+        """All microbatch inputs of unit u back to the GPU (one unit of look-ahead),
+        into one of two persistent staging slots (unit parity) allocated once on
+        the compute stream: no per-fetch allocation on the H2D stream, whose
+        blocks (freed only once the compute stream passed them) fragmented the
+        caching allocator under tight emulated HBM caps into cudaFree retries.
+        The H2D copies wait for the slot's previous unit (u + 2) to finish its
+        backward."""
+        slot = u % 2
+        host0 = self._host[("act", 0, u)]
+        bufs = self._pf_slot[slot]
+        if bufs is None or len(bufs) != nmb or bufs[0].shape != host0.shape:
+            bufs = [torch.empty(host0.shape, dtype=host0.dtype, device=self.device)
+                    for _ in range(nmb)]
+            self._pf_slot[slot] = bufs
+            self.h2d_stream.wait_stream(self._current())     # allocated on the compute stream
+        if self._pf_free[slot] is not None:
+            self.h2d_stream.wait_event(self._pf_free[slot])
+        out = []
+        for k in range(nmb):
+            key = ("act", k, u)
+            self.h2d_stream.wait_event(self._off_ev[key])
+            with self._span("prefetch_act", u, k + 1, "bwd", self.h2d_stream):
+                with torch.cuda.stream(self.h2d_stream), torch.no_grad():
+                    bufs[k].copy_(self._host[key], non_blocking=True)
+            out.append(bufs[k].detach())
         ev = torch.cuda.Event()
         ev.record(self.h2d_stream)
         return out, ev
@@ -772,7 +798,6 @@ class UnevenFSDPTrainer:
                 tensors, ev = pref.pop(u)
                 comp.wait_event(ev)
                 for k, t in enumerate(tensors):
-                    t.record_stream(comp)
                     h[k][u] = t
             acc = self._acc(u)
             held: list[list[torch.Tensor]] = []      # microbatch gradients awaiting accumulate
@@ -827,6 +852,8 @@ class UnevenFSDPTrainer:
                     dy[k] = grads[-1]
                 del grads, y, x, g_in
             done_ev[u] = self._event(comp)
+            if off and not deep:
+                self._pf_free[u % 2] = done_ev[u]    # staging slot of unit u reusable
             if not self.pair_units:
                 if multi:                            # an idle rank's acc holds zeros
                     rs_ev[u] = self._rs(u, acc, done_ev[u])
