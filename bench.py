@@ -299,6 +299,11 @@ def main() -> None:
                            offload_activations=offload,
                            offload_schedule=args.offload_schedule)
     tr.init_params(seed=0)
+    # a memory-capped rank runs its head in row chunks so the [rows, vocab]
+    # logits transient stays within 10% of its emulated HBM
+    logit_bytes = job.arch.seq * job.arch.vocab * 2
+    if job.plan.assignments[rank].microbatch * logit_bytes > 0.1 * emu.memory_cap_bytes:
+        tr.head_chunk = max(1, int(0.1 * emu.memory_cap_bytes // logit_bytes))
     torch.cuda.empty_cache()     # the full-model init temporaries, before the capped steps
     tr.graph = args.graph != "off" and tr.graph_eligible()
     if args.graph == "on" and not tr.graph:
@@ -398,7 +403,8 @@ def main() -> None:
     mem = torch.tensor([torch.cuda.max_memory_allocated(dev) / 2 ** 30,
                         emu.memory_cap_bytes / 2 ** 30,
                         torch.cuda.max_memory_reserved(dev) / 2 ** 30,
-                        float(ms_.get("num_alloc_retries", 0)), float(retries_timed)],
+                        float(ms_.get("num_alloc_retries", 0)), float(retries_timed),
+                        float(tr.head_chunk or 0)],
                        device=dev, dtype=torch.float64)
     if world > 1:
         allm = [torch.zeros_like(mem) for _ in range(world)]
@@ -406,9 +412,10 @@ def main() -> None:
     else:
         allm = [mem]
     # per rank: [peak allocated GiB, cap GiB, peak reserved GiB, allocator retries
-    # (whole run), allocator retries inside the device-timed region]
+    # (whole run), allocator retries inside the device-timed region, head chunk
+    # (samples; 0 = whole microbatch)]
     peak_mem = [[round(float(x[0]), 3), round(float(x[1]), 3), round(float(x[2]), 3),
-                 int(x[3]), int(x[4])] for x in allm]
+                 int(x[3]), int(x[4]), int(x[5])] for x in allm]
     # every rank's owned-kernel rates (rank 0's are the line's "kernels")
     mine = {k: [v["launches"], round(v["gbs"] or 0.0, 1), round(v["ms_total"] / steps_timed, 4)]
             for k, v in kern.items()}

@@ -234,11 +234,14 @@ def embed_forward(arch: ArchSpec, p: dict[str, torch.Tensor], tokens: torch.Tens
 
 
 def head_value_and_grad(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor,
-                        targets: torch.Tensor, wrt: list[torch.Tensor]):
+                        targets: torch.Tensor, wrt: list[torch.Tensor],
+                        grad_scale: float = 1.0):
     """Mean next-token loss of one microbatch and its gradients w.r.t. `wrt`
-    (head parameters and the head input). On CUDA the loss and dlogits come
-    from one fused pass over the logits (het_xent_fused), written over the
-    logits in place, and autograd takes it from the logits GEMM down."""
+    (head parameters and the head input), the gradients scaled by grad_scale
+    (a row chunk of a microbatch passes its share of the rows). On CUDA the loss
+    and dlogits come from one fused pass over the logits (het_xent_fused),
+    written over the logits in place, and autograd takes it from the logits GEMM
+    down."""
     with torch.enable_grad():
         if arch.kind == "llama":
             h = (_K.rms_norm(x, p["normf"]) if x.is_cuda and x.dtype == torch.bfloat16 and
@@ -249,13 +252,16 @@ def head_value_and_grad(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Ten
         flat = logits.view(-1, logits.shape[-1])
         if FUSE_XENT and flat.is_cuda and flat.dtype == torch.bfloat16 and \
                 flat.shape[-1] % 8 == 0 and flat.shape[-1] <= 65536:
-            loss = _K.xent_value_and_grad(flat.detach(), targets.reshape(-1))
+            loss = _K.xent_value_and_grad(flat.detach(), targets.reshape(-1), grad_scale)
             # the matmul's backward keeps h and wte, not the logits: their buffer is free
             return loss, torch.autograd.grad(logits, wrt, logits.detach())
         if flat.is_cuda and flat.dtype == torch.bfloat16 and flat.shape[-1] % 8 == 0:
             loss = _K.cross_entropy(flat, targets.reshape(-1))
         else:
             loss = F.cross_entropy(flat, targets.reshape(-1).long())
+        if grad_scale != 1.0:
+            return loss.detach(), torch.autograd.grad(loss, wrt,
+                                                      torch.full_like(loss, grad_scale))
         return loss.detach(), torch.autograd.grad(loss, wrt)
 
 

@@ -238,6 +238,9 @@ class UnevenFSDPTrainer:
         # `graph_warmup` eager steps the step is captured once and then replayed;
         # the host only copies the tokens in and refreshes AdamW's 7 coefficients
         # (het_adamw_devcoef), so the ~550 launches of a GPT-2 step cost one
+        # samples per head chunk (None: the whole microbatch); set for memory-capped
+        # ranks so the logits transient stays a small share of the cap
+        self.head_chunk: int | None = None
         self.graph = False
         self.graph_warmup = 2
         self._graph = None
@@ -575,6 +578,30 @@ class UnevenFSDPTrainer:
                      events=None if a is None else (a, b))
         self.launches += 1
 
+    def _head(self, leaves, head_names, y, targets, racc, loss):
+        """Loss and gradients of one microbatch's head (final norm, tied LM head,
+        cross-entropy): head parameter gradients accumulated into the root
+        accumulator, the weighted loss added to `loss`; returns the gradients
+        (last: d loss / d y). With head_chunk set, the head runs over row chunks
+        of head_chunk samples, each with its share of the gradient (grad_scale),
+        so the [rows, vocab] logits transient shrinks by the chunk count: the
+        largest single allocation of a memory-capped rank."""
+        arch, m = self.arch, y.shape[0]
+        c = self.head_chunk if self.head_chunk and self.head_chunk < m else m
+        gy = []
+        for j0 in range(0, m, c):
+            j1 = min(j0 + c, m)
+            yj = y if c == m else y[j0:j1].detach().requires_grad_(True)
+            frac = (j1 - j0) / m
+            lk, grads = head_value_and_grad(arch, leaves, yj, targets[j0:j1],
+                                            [leaves[nm] for nm in head_names] + [yj],
+                                            grad_scale=frac)
+            self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
+            loss += lk.detach() * (self.w * frac)
+            gy.append(grads[-1])
+            del grads
+        return [None] * len(head_names) + [gy[0] if len(gy) == 1 else torch.cat(gy)]
+
     def _accumulate_mb(self, acc, held, names, seg, first):
         """Layered accumulate of consecutive microbatches' gradients of one unit
         (one launch; a single microbatch goes through het_accumulate)."""
@@ -756,10 +783,7 @@ class UnevenFSDPTrainer:
                     with self._span("head", root, k + 1, "fwd", comp):
                         if not y.requires_grad:
                             y.requires_grad_(True)
-                        lk, grads = head_value_and_grad(arch, leaves, y, mb[k][1],
-                                                        [leaves[nm] for nm in head_names] + [y])
-                        self._accumulate(racc, grads[:-1], head_names, self.root_seg, first=False)
-                        loss += lk.detach() * self.w
+                        grads = self._head(leaves, head_names, y, mb[k][1], racc, loss)
                     if deep:
                         self._offload("grad", k, nb - 1, grads[-1], comp, nb, "bwd")
                     else:

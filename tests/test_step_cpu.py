@@ -60,3 +60,24 @@ def test_single_rank_step_gradients(fake, m, l):
     assert fake.calls.count("embedding_grad") == l
     assert fake.calls.count("adamw") == 1
     assert "allgather" not in fake.calls and "reduce_scatter" not in fake.calls
+
+
+def test_head_row_chunks_match_whole_microbatch(fake):
+    """head_chunk (a memory-capped rank's head in row chunks, each with its
+    share of the gradient) gives the whole-microbatch step's loss and
+    gradients to fp32 rounding."""
+    arch = ARCHS["tiny_gpt"]
+    plan = _plan(arch, 3, 1)
+    units = _units(arch)
+    tok = torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=6, step=0))
+    out = {}
+    for chunk in (None, 2):
+        tr = S.UnevenFSDPTrainer(arch, plan, 0, device=torch.device("cpu"))
+        tr.load_full_units(units)
+        tr.head_chunk = chunk
+        fake.calls.clear()
+        out[chunk] = (float(tr.step(tok)), tr.g32.clone(), fake.calls.count("accumulate"))
+    assert abs(out[2][0] - out[None][0]) <= 2e-2 * abs(out[None][0])
+    g0, g2 = out[None][1].double(), out[2][1].double()
+    assert float((g2 - g0).norm() / g0.norm()) <= 2e-2
+    assert out[2][2] == out[None][2] + 1          # two head chunks: one more root accumulate

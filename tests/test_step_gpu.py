@@ -200,3 +200,22 @@ def test_cuda_graph_step_matches_eager(cuda, m, l):
     assert torch.equal(res[True][1], res[False][1])
     assert torch.equal(res[True][2], res[False][2])
     assert res[True][3] == res[False][3] and res[True][4] == res[False][4] == 6
+
+
+def test_head_row_chunks_on_gpu(cuda):
+    """A memory-capped rank's head in row chunks (head_chunk) against the whole
+    microbatch: fp32 loss to 1e-5, reduced gradients within the bf16 bar."""
+    arch = ARCHS["gpt2_small"]
+    plan = one_gpu_plan(arch, 4, 2)
+    tok = torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=8, step=0)).to(cuda)
+    out = {}
+    for chunk in (None, 1):
+        tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda)
+        tr.init_params(seed=3)
+        tr.head_chunk = chunk
+        loss = float(tr.step(tok))
+        torch.cuda.synchronize()
+        out[chunk] = (loss, tr.g32.double().clone())
+        del tr
+    assert abs(out[1][0] - out[None][0]) <= 1e-5 * abs(out[None][0])
+    assert float((out[1][1] - out[None][1]).norm() / out[None][1].norm()) <= 2e-2
