@@ -14,6 +14,7 @@ AdamW) of the named config on N GPUs with global batch batch_per_gpu * N
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -52,7 +53,7 @@ def peaks() -> tuple[float, str]:
 
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled while the timed
-    region runs: NVML every 20 ms (nvidia-smi every 200 ms if NVML is absent),
+    region runs: NVML every 50 ms (nvidia-smi every 200 ms if NVML is absent),
     in a separate PROCESS, so the sampler never takes the launching thread's
     GIL (a sampler thread measurably slowed launch-heavy steps)."""
 
@@ -90,7 +91,7 @@ while not stop.is_set():
             print(",".join(row), flush=True)
     except Exception:
         pass
-    stop.wait(0.02 if nv is not None else 0.2)
+    stop.wait(0.05 if nv is not None else 0.2)
 """
 
     def __init__(self, index: int):
@@ -354,7 +355,9 @@ def main() -> None:
     retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     comp = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    # rank 0 samples its GPU (the line reports rank 0's clocks); one NVML poller
+    # per node instead of one per rank keeps driver calls off the other ranks
+    with (ClockSampler(local) if rank == 0 else contextlib.nullcontext(None)) as clocks:
         barrier()
         t0.record(comp)
         for s in range(args.warmup, nsteps):
