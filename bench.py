@@ -62,12 +62,11 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
     # NVML clocks-event reason bits, in the order of the query above
     BITS = (0x8, 0x40, 0x20, 0x4)
-    # the sampler process: prints "ready", then one CSV row per sample until stdin closes
+    # the sampler process: initialises NVML, prints "ready", waits for a "go" line,
+    # then prints one CSV row per sample until stdin closes
     SCRIPT = r"""
 import subprocess, sys, threading
 idx, q, bits = int(sys.argv[1]), sys.argv[2], [int(b) for b in sys.argv[3].split(",")]
-stop = threading.Event()
-threading.Thread(target=lambda: (sys.stdin.read(), stop.set()), daemon=True).start()
 try:
     import pynvml as nv
     nv.nvmlInit()
@@ -75,6 +74,9 @@ try:
 except Exception:
     nv = None
 print("ready", flush=True)
+sys.stdin.readline()
+stop = threading.Event()
+threading.Thread(target=lambda: (sys.stdin.read(), stop.set()), daemon=True).start()
 while not stop.is_set():
     try:
         if nv is not None:
@@ -95,18 +97,26 @@ while not stop.is_set():
 """
 
     def __init__(self, index: int):
+        """Starts the sampler process (and its NVML init) now, well before the
+        timed region; sampling begins at __enter__."""
         self.index, self.rows, self._p = index, [], None
-
-    def __enter__(self):
         try:
             self._p = subprocess.Popen(
                 [sys.executable, "-c", self.SCRIPT, str(self.index), self.Q,
                  ",".join(str(b) for b in self.BITS)],
                 stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
-            self._p.stdout.readline()           # "ready": sampling before the region starts
         except Exception:
             self._p = None
+
+    def __enter__(self):
+        if self._p is not None:
+            try:
+                self._p.stdout.readline()       # "ready"
+                self._p.stdin.write("go\n")
+                self._p.stdin.flush()
+            except Exception:
+                self._p = None
         return self
 
     def __exit__(self, *a):
@@ -284,6 +294,9 @@ def main() -> None:
         return
 
     world, rank, local = setup_dist()
+    # rank 0's clock sampler process starts (and initialises NVML) now, long
+    # before the timed region it samples
+    sampler = ClockSampler(local) if rank == 0 else None
     dev = torch.device("cuda", local)
     job = build_job(args.config, world, measured=not args.analytic_profiles)
     comm_ag, comm_rs = make_comms(world, rank)
@@ -357,7 +370,7 @@ def main() -> None:
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # rank 0 samples its GPU (the line reports rank 0's clocks); one NVML poller
     # per node instead of one per rank keeps driver calls off the other ranks
-    with (ClockSampler(local) if rank == 0 else contextlib.nullcontext(None)) as clocks:
+    with (sampler if rank == 0 else contextlib.nullcontext(None)) as clocks:
         barrier()
         t0.record(comp)
         for s in range(args.warmup, nsteps):
