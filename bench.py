@@ -373,13 +373,23 @@ def main() -> None:
     with (sampler if rank == 0 else contextlib.nullcontext(None)) as clocks:
         barrier()
         t0.record(comp)
+        marks = [t0]
         for s in range(args.warmup, nsteps):
             tr.step(resident[s])
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(comp)
+            marks.append(ev)
         t1.record(comp)
         barrier()
     launches = K.LAUNCHES - launches0
     retries_timed = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
+    # per-step device times (this rank's compute stream), max over ranks per step
+    step_ms = torch.tensor([a.elapsed_time(b) for a, b in zip(marks, marks[1:])],
+                           device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+    step_ms = [round(float(x), 2) for x in step_ms]
     kern = {k: tr.timers.summary(k) for k in ("adamw", "accumulate", "gather")}
     kern = {k: v for k, v in kern.items() if v["launches"]}
     steps_timed = 1 if tr.graph_active else args.steps     # graph: the last replay
@@ -460,6 +470,7 @@ def main() -> None:
         line = {
             "metric": "train samples/s", "value": B / (ms * 1e-3), "unit": "samples/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "step_ms": step_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens (splitmix64), random-init weights",
             "config": {"workload": job.config.name, "description": job.config.description,
