@@ -251,6 +251,7 @@ def route_summary(tr) -> dict | str:
         return "none"
     return {"ag": {r: tr.ag_route.count(r) for r in sorted(set(tr.ag_route))},
             "rs": {r: tr.rs_route.count(r) for r in sorted(set(tr.rs_route))},
+            "ag_relay_units": sum(1 for p in getattr(tr, "ag_policy", []) if p == 3),
             "symm_self_check": tr.route_check, "symm_error": tr.symm_error,
             "rs_bf16_wire_units": sum(tr.wire16)}
 

@@ -32,9 +32,10 @@ from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
          "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route",
+         "symm_relay": "symm_relay",
          "symm_bf16wire": "symm_bf16wire"}
 SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
-        "symm_peer": (False, K.SYMM_PEER)}
+        "symm_peer": (False, K.SYMM_PEER), "symm_relay": (False, K.SYMM_RELAY)}
 
 
 def skew_counts(skew: str, total: int, n: int) -> list[int]:
@@ -110,8 +111,9 @@ def main() -> None:
     maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
     ws = {}
     for an, (mc, policy) in SYMM.items():
-        if an in args.algos or (an == "symm" and ("route" in args.algos or
-                                                "symm_bf16wire" in args.algos)):
+        if an in args.algos or (an in ("symm", "symm_relay") and world > 2 and
+                                "route" in args.algos) or (an == "symm" and (
+                                    "route" in args.algos or "symm_bf16wire" in args.algos)):
             ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
                                                                          torch.float32),
                                       ("g16", maxel // 2 + 64, torch.bfloat16)],
@@ -133,12 +135,15 @@ def main() -> None:
                     o = offsets(c)
                     for an in args.algos:
                         algo = ALGOS[an]
-                        if op == "reduce_scatter" and algo == K.ALGO_P2P:
+                        if op == "reduce_scatter" and algo in (K.ALGO_P2P, "symm_relay"):
                             continue
                         if algo == "route":   # the train step's per-unit choice
                             pick = K.route_collective("ag" if op == "allgather" else "rs", c,
                                                       world, "symm" in ws)
                             algo = "symm" if pick == "symm" else K.ALGO_AUTO
+                            if (algo == "symm" and op == "allgather" and
+                                    K.ag_symm_policy(c, world) == K.SYMM_RELAY):
+                                algo = "symm_relay"
                         if algo == "symm_bf16wire":
                             if op != "reduce_scatter":
                                 continue

@@ -284,6 +284,10 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
 #define HET_SYMM_AUTO 0
 #define HET_SYMM_MULTICAST 1
 #define HET_SYMM_PEER 2
+/* All-gather only (the reduce-scatter treats it as AUTO): peer push where
+ * each big owner hands a share of its range to a small owner, which forwards
+ * it, balancing link egress on skewed shard vectors (N >= 3). */
+#define HET_SYMM_RELAY 3
 
 /* A buffer allocated at the same byte layout on every rank (torch symmetric
  * memory is the plumbing): peer_base[j] = its address on rank j mapped into

@@ -50,12 +50,18 @@ struct Args {
   uint32_t epoch;
   int channel;
   int end_barrier;
+  // AG relay (HET_SYMM_RELAY, peer route only): my last relay_vecs body
+  // vectors go to me and relay_to only, and relay_to forwards them; I forward
+  // the last from_vecs body vectors of rank relay_from (count from_count at
+  // from_offset). -1 / 0 = none.
+  int relay_to = -1, relay_from = -1;
+  int64_t relay_vecs = 0, from_count = 0, from_offset = 0, from_vecs = 0;
 };
 
 __device__ __forceinline__ uint32_t* slot(uint64_t owner_base, uint64_t signal_off, int channel,
                                           int kind, int cta, int src) {
   const uint64_t idx =
-      ((static_cast<uint64_t>(channel) * 2 + kind) * kMaxCtas + cta) * HET_MAX_RANKS + src;
+      ((static_cast<uint64_t>(channel) * 3 + kind) * kMaxCtas + cta) * HET_MAX_RANKS + src;
   return reinterpret_cast<uint32_t*>(owner_base + signal_off + idx * 4);
 }
 
@@ -145,6 +151,93 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 // ---------------------------------------------------------------- all-gather
 
+// Element geometry of one rank's bf16 range at byte offset dst0: [0,h1)
+// 2-byte edge, [h1,h2) 4-byte words, nvec 16-byte vectors, then the tail.
+// Host twin: ag_geometry() below (the relay plan must agree with it).
+__host__ __device__ inline void ag_geometry(uint64_t dst0, int64_t n, int64_t* h1o, int64_t* h2o,
+                                            int64_t* nveco) {
+  int64_t h1 = (dst0 & 3) ? 1 : 0;
+  if (h1 > n) h1 = n;
+  int64_t h2 = h1 + static_cast<int64_t>(((16 - ((dst0 + h1 * 2) & 15)) & 15) / 2);
+  if (h2 > n) h2 = n;
+  *h1o = h1;
+  *h2o = h2;
+  *nveco = (n - h2) / 8;
+}
+
+// Pack body vectors [lo,hi) of my fp32 range and store each to the peers in
+// `mask` (bit p = rank p); kUnroll vectors per thread in flight, all local
+// loads issued before the remote stores.
+template <int NR>
+__device__ __forceinline__ void ag_push(const float* __restrict__ src, int64_t h2, int64_t lo,
+                                        int64_t hi, uint64_t dst0, const uint64_t* peer, int nr,
+                                        uint32_t mask, bool src_vec) {
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kUnroll) {
+    uint4 w[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < hi) {
+        const float* p = src + h2 + v * 8;
+        float f[8];
+        if (src_vec) {
+          const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+          const float4 y = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+          f[0] = x.x; f[1] = x.y; f[2] = x.z; f[3] = x.w;
+          f[4] = y.x; f[5] = y.y; f[6] = y.z; f[7] = y.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = p[i];
+        }
+        w[u] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                          pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < hi) {
+        const uint64_t off = dst0 + static_cast<uint64_t>(h2 + v * 8) * 2;
+#pragma unroll
+        for (int p = 0; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p)
+          if (p < nr && ((mask >> p) & 1u)) *reinterpret_cast<uint4*>(peer[p] + off) = w[u];
+      }
+    }
+  }
+}
+
+// Forward body vectors [lo,hi) of another rank's range (already landed in my
+// copy of the unit) to the peers in `mask`. Same vector -> CTA mapping as
+// ag_push, so CTA b forwards exactly what the owner's CTA b sent it.
+template <int NR>
+__device__ __forceinline__ void ag_forward(int64_t h2, int64_t lo, int64_t hi, uint64_t dst0,
+                                           const uint64_t* peer, int me, int nr, uint32_t mask) {
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kUnroll) {
+    uint4 w[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < hi)
+        w[u] = __ldcg(reinterpret_cast<const uint4*>(peer[me] + dst0 +
+                                                     static_cast<uint64_t>(h2 + v * 8) * 2));
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * gsz;
+      if (v < hi) {
+        const uint64_t off = dst0 + static_cast<uint64_t>(h2 + v * 8) * 2;
+#pragma unroll
+        for (int p = 0; p < (NR > 0 ? NR : HET_MAX_RANKS); ++p)
+          if (p < nr && ((mask >> p) & 1u)) *reinterpret_cast<uint4*>(peer[p] + off) = w[u];
+      }
+    }
+  }
+}
+
 template <bool MC, int NR>
 __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restrict__ src,
                                                            const __grid_constant__ Args a) {
@@ -167,6 +260,44 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
   // body: 8 bf16 per 16-byte multicast store; kUnroll vectors per thread in
   // flight (all local loads issued before the remote stores)
   const bool src_vec = ((reinterpret_cast<uintptr_t>(src + h2)) & 15) == 0;
+  if (!MC && (a.relay_to >= 0 || a.relay_from >= 0)) {
+    // relay route: the relayed tail first (to me + my relay), flag it, then
+    // the direct body; the relay forwards after its own body so its egress
+    // carries part of the big owner's.
+    const uint32_t all = (nr >= 32) ? 0xffffffffu : ((1u << nr) - 1u);
+    int64_t direct = nvec;
+    if (a.relay_to >= 0) {
+      direct = nvec - a.relay_vecs;
+      ag_push<NR>(src, h2, direct, nvec, dst0, peer, nr,
+                  (1u << s.rank) | (1u << a.relay_to), src_vec);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        st_release_sys(slot(peer[a.relay_to], s.signal_off, a.channel, 2, blockIdx.x, s.rank),
+                       a.epoch);
+      }
+    }
+    ag_push<NR>(src, h2, 0, direct, dst0, peer, nr, all, src_vec);
+    if (a.relay_from >= 0) {
+      if (threadIdx.x == 0) {
+        const uint32_t* mine =
+            slot(peer[s.rank], s.signal_off, a.channel, 2, blockIdx.x, a.relay_from);
+        const uint64_t t0 = globaltimer_ns();
+        while (static_cast<int32_t>(ld_acquire_sys(mine) - a.epoch) < 0) {
+          if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
+            atomicExch(&g_symm_status, HET_SYMM_TIMEOUT);
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      const uint64_t fdst0 = a.data_off + static_cast<uint64_t>(a.from_offset) * 2;
+      int64_t fh1, fh2, fnvec;
+      ag_geometry(fdst0, a.from_count, &fh1, &fh2, &fnvec);
+      ag_forward<NR>(fh2, fnvec - a.from_vecs, fnvec, fdst0, peer, s.rank, nr,
+                     all & ~((1u << s.rank) | (1u << a.relay_from)));
+    }
+  } else
   for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
     uint4 w[kUnroll];
 #pragma unroll
@@ -448,6 +579,45 @@ bool pick_multicast(const het_symm_t* s, const int64_t* counts, int policy) {
   return total < push;
 }
 
+// Relay pairing for the peer all-gather (HET_SYMM_RELAY). Ranks sorted by
+// count, the i-th largest owner A pairs with the i-th smallest B (sB < sA).
+// A sends a fraction f of its body to B only and B forwards it to the other
+// N-2 ranks. Egress A = sA((N-1) - (N-2) f), egress B = sB(N-1) + (N-2) f sA;
+// equal at f = (sA - sB)(N-1) / (2 (N-2) sA). DESIGN.md §5.
+void relay_plan(const het_symm_t* s, const int64_t* counts, const int64_t* offsets,
+                uint64_t unit_off, Args* a) {
+  const int n = s->nranks;
+  if (n < 3) return;
+  int order[HET_MAX_RANKS];
+  for (int j = 0; j < n; ++j) order[j] = j;
+  for (int i = 1; i < n; ++i)   // stable insertion sort, count descending
+    for (int j = i; j > 0 && counts[order[j]] > counts[order[j - 1]]; --j) {
+      const int t = order[j];
+      order[j] = order[j - 1];
+      order[j - 1] = t;
+    }
+  for (int i = 0; i < n / 2; ++i) {
+    const int A = order[i], B = order[n - 1 - i];
+    const int64_t sa = counts[A], sb = counts[B];
+    if (sa <= sb) break;
+    const double f = static_cast<double>(sa - sb) * (n - 1) / (2.0 * (n - 2) * sa);
+    int64_t h1, h2, nvec;
+    ag_geometry(unit_off + static_cast<uint64_t>(offsets[A]) * 2, sa, &h1, &h2, &nvec);
+    const int64_t rv = static_cast<int64_t>(f * static_cast<double>(nvec));
+    if (rv <= 0) continue;
+    if (s->rank == A) {
+      a->relay_to = B;
+      a->relay_vecs = rv;
+    }
+    if (s->rank == B) {
+      a->relay_from = A;
+      a->from_count = sa;
+      a->from_offset = offsets[A];
+      a->from_vecs = rv;
+    }
+  }
+}
+
 int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offsets, int ctas) {
   if (!s || s->nranks < 1 || s->nranks > HET_MAX_RANKS || s->rank < 0 || s->rank >= s->nranks)
     return fail(HET_EARG, "het_symm: bad rank table");
@@ -469,7 +639,7 @@ int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offset
 extern "C" {
 
 int64_t het_symm_signal_bytes(void) {
-  return static_cast<int64_t>(HET_SYMM_CHANNELS) * 2 * kMaxCtas * HET_MAX_RANKS * 4;
+  return static_cast<int64_t>(HET_SYMM_CHANNELS) * 3 * kMaxCtas * HET_MAX_RANKS * 4;
 }
 
 int het_symm_status(int reset) {
@@ -491,9 +661,10 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
   if (counts[s->rank] > 0 && !src) return fail(HET_EARG, "het_symm_allgather_pack: null src");
   if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
-  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1};
+  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1, -1, -1, 0, 0, 0, 0};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool mc = pick_multicast(s, counts, policy);
+  const bool mc = policy == HET_SYMM_RELAY ? false : pick_multicast(s, counts, policy);
+  if (policy == HET_SYMM_RELAY) relay_plan(s, counts, offsets, unit_off, &a);
 #define HET_AG(MCV, NRV) symm_ag_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(src, a)
   HET_DISPATCH_NR(mc, s->nranks, HET_AG);
 #undef HET_AG

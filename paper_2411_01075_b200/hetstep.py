@@ -8,7 +8,7 @@ is not on a CUDA device, the call raises.
 from __future__ import annotations
 
 import ctypes
-from typing import Sequence
+from typing import Optional, Sequence
 
 import torch
 
@@ -24,7 +24,7 @@ ALGO_SYMM = 4            # fused kernels on a symmetric buffer (NVLS multicast /
 HET_MAX_RANKS = 8
 HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
-SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER = 0, 1, 2
+SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_RELAY = 0, 1, 2, 3
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
@@ -1050,6 +1050,32 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
     raise InputError(f"unknown collective {op!r}")
 
 
+def ag_symm_policy(counts: Sequence[int], nranks: int) -> int:
+    """Route policy for a fused all-gather: SYMM_RELAY when the relay's link
+    model beats the better of multicast and plain peer push by >10%, else
+    SYMM_AUTO. Mirrors relay_plan() in csrc/hetstep_symm.cu: the i-th largest
+    owner A pairs with the i-th smallest B, and the balanced pair egress is
+    (N-1)(sA+sB)/2; the ingress bound S - min s is unchanged. Measured at N=4,
+    1 GB (profiles/r1_final/relay_n4_c*.jsonl): 2:1 563-589 vs 485 GB/s, planner
+    643-676 vs 538; geometric (model margin 7%) stays on multicast (532 vs 465)."""
+    if nranks < 3:
+        return SYMM_AUTO
+    c = sorted((int(x) for x in counts), reverse=True)
+    total, mn = sum(c), c[-1]
+    if total <= 0:
+        return SYMM_AUTO
+    peer = max((nranks - 1) * c[0], total - mn)
+    best = min(peer, total)                 # multicast moves S on every link
+    relay = total - mn
+    for i in range(nranks):
+        j = nranks - 1 - i
+        if i < j and c[i] > c[j]:
+            relay = max(relay, (nranks - 1) * (c[i] + c[j]) / 2)
+        elif i <= j:                          # unpaired: plain push
+            relay = max(relay, (nranks - 1) * c[i])
+    return SYMM_RELAY if relay < 0.9 * best else SYMM_AUTO
+
+
 # ---------------------------------------------------------------------------
 # symmetric workspace + fused collectives
 
@@ -1108,14 +1134,17 @@ class SymmWorkspace:
         return self.views[name]
 
     def allgather_pack(self, src_f32: torch.Tensor, region: str, elem_off: int,
-                       counts: Sequence[int], offsets: Sequence[int], stream=None) -> None:
-        """bf16 unit at `region`[elem_off:] <- every rank's fp32 range (fused pack+AG)."""
+                       counts: Sequence[int], offsets: Sequence[int], stream=None,
+                       policy: Optional[int] = None) -> None:
+        """bf16 unit at `region`[elem_off:] <- every rank's fp32 range (fused pack+AG).
+        `policy` overrides the workspace's route policy for this call."""
         self.epoch[0] += 1
         src = _cuda(src_f32, torch.float32, "src") if src_f32.numel() else None
         byte_off = self.offsets[region] + 2 * elem_off
         _check(load().het_symm_allgather_pack(ctypes.byref(self.desc), src, byte_off,
                                               _i64(counts), _i64(offsets), self.epoch[0], 0,
-                                              self.policy, self.ctas, _stream(stream)),
+                                              self.policy if policy is None else int(policy),
+                                              self.ctas, _stream(stream)),
                "het_symm_allgather_pack")
 
     def reduce_scatter(self, region: str, elem_off: int, out: torch.Tensor,

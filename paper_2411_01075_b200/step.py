@@ -263,6 +263,9 @@ class UnevenFSDPTrainer:
         units = range(self.L.blocks + 1)
         self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
         self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
+        # fused AG units on skewed shards at N >= 3: relay policy (hetstep.ag_symm_policy)
+        self.ag_policy = [K.ag_symm_policy(self.L.counts[u], self.N)
+                          if self.ag_route[u] == "symm" else None for u in units]
         # a fused RS whose successor (RS order: L-1..0, root) is not fused must end with a
         # cross-rank barrier: nothing later proves that peers finished reading its acc
         order = list(range(self.L.blocks - 1, -1, -1)) + [self.L.root]
@@ -309,7 +312,8 @@ class UnevenFSDPTrainer:
             lo, cnt = offsets[self.rank], counts[self.rank]
             if ag:
                 src = pattern(torch.arange(lo, lo + cnt, device=dev), 0)
-                self.symm.allgather_pack(src, ub, 0, counts, offsets, stream=self._current())
+                self.symm.allgather_pack(src, ub, 0, counts, offsets, stream=self._current(),
+                                         policy=self.ag_policy[u])
                 want = pattern(torch.arange(size, device=dev), 0).to(torch.bfloat16)
                 bad += int(not torch.equal(self.symm[ub][:size], want))
                 checked += 1
@@ -488,7 +492,8 @@ class UnevenFSDPTrainer:
     def _ag_issue(self, u: int, dst: torch.Tensor) -> None:
         if self.ag_route[u] == "symm":   # fused pack + NVLS/peer all-gather from fp32 master
             self.symm.allgather_pack(self._local(self.p32, u), self._region(dst), 0,
-                                     self.L.counts[u], self.L.offsets[u], stream=self.ag_stream)
+                                     self.L.counts[u], self.L.offsets[u], stream=self.ag_stream,
+                                     policy=self.ag_policy[u])
             self.launches += 1
         else:
             K.allgather_uneven(self._local(self.p16, u), dst, self.L.counts[u],

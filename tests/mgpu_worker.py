@@ -82,7 +82,8 @@ def main(out_dir: str) -> None:
 
         # fused symmetric-memory collectives (NVLS multicast when available, then peer)
         maxu = max(sum(c) for c in shard_cases(world)) + 64
-        for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO)):
+        for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO),
+                               (False, K.SYMM_RELAY)):
             ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32),
                                   ("g16", maxu, torch.bfloat16)],
                                  dist.group.WORLD.group_name, dev, rank, world,

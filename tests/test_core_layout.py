@@ -125,3 +125,43 @@ def test_header_symbols_are_exported():
         assert hasattr(lib, sym), sym
     lib.het_version.restype = ctypes.c_char_p
     assert lib.het_version().decode().startswith("hetstep")
+
+
+def _relay_link_bytes(counts):
+    """Per-rank (egress, ingress) of the relay all-gather as relay_plan() in
+    csrc/hetstep_symm.cu schedules it: pair i-th largest A with i-th smallest
+    B, A hands f of its range to B only, B forwards it to the other N-2."""
+    n = len(counts)
+    eg = [(n - 1) * c for c in counts]
+    order = sorted(range(n), key=lambda j: -counts[j])
+    for i in range(n // 2):
+        a, b = order[i], order[n - 1 - i]
+        if counts[a] <= counts[b]:
+            break
+        f = (counts[a] - counts[b]) * (n - 1) / (2.0 * (n - 2) * counts[a])
+        eg[a] -= (n - 2) * f * counts[a]
+        eg[b] += (n - 2) * f * counts[a]
+    total = sum(counts)
+    return eg, [total - c for c in counts]
+
+
+def test_ag_relay_policy_link_model():
+    from paper_2411_01075_b200 import hetstep as K
+    T = 6 * 10**8
+    # 2:1 at N=4: balanced egress 3S/4, bound moves to the small owners' ingress 5S/6
+    c = [2 * T, T, 2 * T, T]
+    eg, ing = _relay_link_bytes(c)
+    S = sum(c)
+    assert max(eg) == pytest.approx(0.75 * S)
+    assert max(max(eg), max(ing)) == pytest.approx(5 * S / 6)
+    assert K.ag_symm_policy(c, 4) == K.SYMM_RELAY
+    # no gain: even shards, N=2, geometric (7% model margin), zero-count ranks
+    assert K.ag_symm_policy([T] * 4, 4) == K.SYMM_AUTO
+    assert K.ag_symm_policy([2 * T, T], 2) == K.SYMM_AUTO
+    assert K.ag_symm_policy([T >> i for i in range(4)], 4) == K.SYMM_AUTO
+    assert K.ag_symm_policy([T, 0, T, 0], 4) == K.SYMM_AUTO
+    assert K.ag_symm_policy([0, 0, 0, 0], 4) == K.SYMM_AUTO
+    # the relay never raises any rank's egress above the plain push maximum
+    for c in ([5, 1, 1, 1], [9, 4, 2, 1], [3, 3, 1, 1, 2, 2, 1, 1], [7, 0, 0, 0]):
+        eg, _ = _relay_link_bytes(c)
+        assert max(eg) <= (len(c) - 1) * max(c) + 1e-9
