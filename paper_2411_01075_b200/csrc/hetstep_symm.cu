@@ -27,6 +27,7 @@
 #include <stdint.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include "hetstep.h"
 #include "hetstep_internal.cuh"
@@ -588,6 +589,14 @@ void relay_plan(const het_symm_t* s, const int64_t* counts, const int64_t* offse
                 uint64_t unit_off, Args* a) {
   const int n = s->nranks;
   if (n < 3) return;
+  // f is scaled by 1.25 past the egress balance: B's link idles until A's
+  // first relay vectors land, so a slightly larger share evens the finish.
+  // Sweep 0.5-1.5 at N=4, 1 GB (profiles/r1_final/relay_fscale_n4.jsonl):
+  // 2:1 589 -> 616 GB/s, planner 674 -> 686. HET_RELAY_FSCALE overrides.
+  static const double fscale = [] {
+    const char* e = getenv("HET_RELAY_FSCALE");
+    return e ? atof(e) : 1.25;
+  }();
   int order[HET_MAX_RANKS];
   for (int j = 0; j < n; ++j) order[j] = j;
   for (int i = 1; i < n; ++i)   // stable insertion sort, count descending
@@ -600,7 +609,8 @@ void relay_plan(const het_symm_t* s, const int64_t* counts, const int64_t* offse
     const int A = order[i], B = order[n - 1 - i];
     const int64_t sa = counts[A], sb = counts[B];
     if (sa <= sb) break;
-    const double f = static_cast<double>(sa - sb) * (n - 1) / (2.0 * (n - 2) * sa);
+    double f = fscale * static_cast<double>(sa - sb) * (n - 1) / (2.0 * (n - 2) * sa);
+    if (f > 1.0) f = 1.0;
     int64_t h1, h2, nvec;
     ag_geometry(unit_off + static_cast<uint64_t>(offsets[A]) * 2, sa, &h1, &h2, &nvec);
     const int64_t rv = static_cast<int64_t>(f * static_cast<double>(nvec));

@@ -1056,8 +1056,8 @@ def ag_symm_policy(counts: Sequence[int], nranks: int) -> int:
     SYMM_AUTO. Mirrors relay_plan() in csrc/hetstep_symm.cu: the i-th largest
     owner A pairs with the i-th smallest B, and the balanced pair egress is
     (N-1)(sA+sB)/2; the ingress bound S - min s is unchanged. Measured at N=4,
-    1 GB (profiles/r1_final/relay_n4_c*.jsonl): 2:1 563-589 vs 485 GB/s, planner
-    643-676 vs 538; geometric (model margin 7%) stays on multicast (532 vs 465)."""
+    1 GB (profiles/r1_final/relay_n4_c*.jsonl, relay_fscale_n4.jsonl): 2:1 616 vs
+    485 GB/s, planner 686 vs 538; geometric (model margin 7%) stays on multicast (532 vs 465)."""
     if nranks < 3 or nranks > 4:   # relay measured at N=4 only; N=8 keeps AUTO until run
         return SYMM_AUTO
     c = sorted((int(x) for x in counts), reverse=True)
