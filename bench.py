@@ -382,6 +382,7 @@ def main() -> None:
             marks.append(ev)
         t1.record(comp)
         barrier()
+    tr.check_faults()           # a fused-collective barrier timeout voids the run (raises)
     launches = K.LAUNCHES - launches0
     retries_timed = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0
     ms = max_over_ranks(t0.elapsed_time(t1)) / args.steps
@@ -406,6 +407,7 @@ def main() -> None:
         loss_val = float(tr.step(x))          # D2H read of the step's loss
     e1.record(comp)
     barrier()
+    tr.check_faults()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     trace_report = None
     if args.trace_dir:

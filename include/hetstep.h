@@ -233,7 +233,20 @@ int het_lt_matmul(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, con
   * ((threads, loads in flight) = (256,4) (256,2) (256,1) (512,2) (512,1) (128,4));
  * default 4, measured fastest on B200 (tools/acc_bench.cu). */
 #define HET_TUNE_ACC_VARIANT 1
+/* HET_TUNE_SM_BUDGET: SMs the persistent grids (accumulate, AdamW, pack, fill)
+ * are sized for: a rank whose compute stream lives in a green-context
+ * partition of nsm SMs sets nsm, so one wave fills its partition instead of
+ * 148 x k CTAs queueing behind it. 0 = the whole device (default). */
+#define HET_TUNE_SM_BUDGET 2
+/* HET_TUNE_SYMM_TIMEOUT_MS: spin limit of the fused collectives' cross-rank
+ * barriers (default 10000 ms); after it the kernel records HET_SYMM_TIMEOUT. */
+#define HET_TUNE_SYMM_TIMEOUT_MS 3
 int het_tune(int key, int value);
+
+/* Emulation diagnostic: `ctas` CTAs each write the %smid they ran on to
+ * out[blockIdx]; launched on a green-context stream, the distinct values are
+ * the SMs of its partition (tests/test_emulation_gpu.py). */
+int het_probe_smid(int32_t* out, int ctas, void* stream);
 
 /* fill / zero helpers used by the step driver (idle ranks, pads) */
 int het_fill_f32(float* dst, float value, int64_t n, void* stream);
@@ -302,8 +315,14 @@ typedef struct {
 } het_symm_t;
 
 int64_t het_symm_signal_bytes(void);
-/* Sticky device status of the symmetric kernels (0 or HET_SYMM_TIMEOUT). */
+/* Sticky device status of the symmetric kernels (0 or HET_SYMM_TIMEOUT).
+ * Synchronous (device-wide copy); reset=1 clears it. */
 int het_symm_status(int reset);
+/* The same status written to *dst by a one-thread kernel on `stream`, after
+ * everything queued before it: dst may be pinned host memory (device-mapped
+ * under UVA), so the step driver checks it from an event, without a device
+ * sync, and raises instead of training on unsynchronised gradients. */
+int het_symm_status_async(int32_t* dst, void* stream);
 
 /* (1)+(2) fused: rank r rounds its fp32 master range src[0:counts[r]] to bf16
  * and stores it at unit_off + 2*offsets[r] on EVERY rank with one multicast

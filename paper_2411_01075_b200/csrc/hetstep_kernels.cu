@@ -39,14 +39,21 @@ int check_launch(const char* what) {
   return HET_OK;
 }
 
-int grid_for(int64_t work_items, int threads) {
-  static int sms = 0;
-  if (sms == 0) {
+int g_sm_budget = 0;   // het_tune(HET_TUNE_SM_BUDGET); 0 = the whole device
+
+int sm_count() {
+  static int dev_sms = 0;
+  if (dev_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev_sms <= 0) dev_sms = 148;
   }
+  return g_sm_budget > 0 && g_sm_budget < dev_sms ? g_sm_budget : dev_sms;
+}
+
+int grid_for(int64_t work_items, int threads) {
+  const int sms = sm_count();
   int64_t need = (work_items + threads - 1) / threads;
   int64_t cap = static_cast<int64_t>(sms) * 8;  // 8 x 256-thread CTAs resident per SM
   if (need < 1) need = 1;
@@ -528,6 +535,23 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 }  // namespace
 
+namespace {
+// Diagnostic for the heterogeneity emulation: each CTA records the SM it ran
+// on (%smid), so a test can prove a green-context stream stays in its partition.
+__global__ void probe_smid_kernel(int32_t* out) {
+  if (threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    // keep the CTA resident a little so the launch spreads over the partition
+    const long long t0 = clock64();
+    while (clock64() - t0 < 20000) {
+    }
+    out[blockIdx.x] = static_cast<int32_t>(sm);
+  }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* het_version(void) { return "hetstep 0.1.0 sm_100a"; }
@@ -570,20 +594,19 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
   if (blocks == 0) return HET_OK;
   if (blocks > 0x7fffffff) return fail(HET_EARG, "het_accumulate: too large");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // persistent: at most the resident CTAs of the variant (occupancy, cached per variant)
+  // persistent: at most the resident CTAs of the variant (occupancy per SM cached per
+  // variant) on the SMs this rank may use (green-context budget, het::sm_count)
   static int resident[8][2] = {};
 #define HET_ACC_LAUNCH(T, I)                                                              \
   do {                                                                                    \
     auto kf = mode == HET_ACC_FIRST ? accumulate_kernel<HET_ACC_FIRST, T, I>              \
                                     : accumulate_kernel<HET_ACC_ADD, T, I>;               \
-    int& r = resident[g_acc_variant][mode == HET_ACC_FIRST];                              \
-    if (r == 0) {                                                                         \
-      int per_sm = 0, dev = 0, sms = 0;                                                   \
+    int& per_sm = resident[g_acc_variant][mode == HET_ACC_FIRST];                         \
+    if (per_sm == 0) {                                                                    \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, T, 0);                   \
-      cudaGetDevice(&dev);                                                                \
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                  \
-      r = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);                              \
+      if (per_sm <= 0) per_sm = 1;                                                        \
     }                                                                                     \
+    const int64_t r = static_cast<int64_t>(per_sm) * het::sm_count();                     \
     const dim3 grid(static_cast<unsigned>(blocks < r ? blocks : r));                      \
     kf<<<grid, T, 0, st>>>(acc, t, scale);                                                \
   } while (0)
@@ -630,15 +653,13 @@ int het_accumulate_multi(float* acc, const het_seg_t* segs, int nseg, int nsrc, 
   if (blocks == 0) return HET_OK;
   if (blocks > 0x7fffffff) return fail(HET_EARG, "het_accumulate_multi: too large");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static int resident = 0;
-  if (resident == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+  static int per_sm = 0;
+  if (per_sm == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
                                                   accumulate_multi_kernel<HET_ACC_ADD, 4>, 512, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    if (per_sm <= 0) per_sm = 1;
   }
+  const int64_t resident = static_cast<int64_t>(per_sm) * het::sm_count();
   const dim3 grid(static_cast<unsigned>(blocks < resident ? blocks : resident));
 #define HET_ACCM(M, K) accumulate_multi_kernel<M, K><<<grid, 512, 0, st>>>(acc, t, ms, scale)
   if (mode == HET_ACC_FIRST) {
@@ -675,14 +696,12 @@ int het_gather_bf16(void* dst, const het_seg_t* segs, int nseg, void* stream) {
   }
   for (int s = nseg; s <= HET_MAX_SEGS; ++s) t.first_block[s] = blocks;
   if (blocks == 0) return HET_OK;
-  static int resident = 0;
-  if (resident == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+  static int per_sm = 0;
+  if (per_sm == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_bf16_kernel, 512, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    if (per_sm <= 0) per_sm = 1;
   }
+  const int64_t resident = static_cast<int64_t>(per_sm) * het::sm_count();
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   gather_bf16_kernel<<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<__nv_bfloat16*>(dst), t);
@@ -802,6 +821,12 @@ int het_embedding_grad_dev(float* acc, int64_t wte_off, int64_t wpe_off, const v
 }
 
 int het_tune(int key, int value) {
+  if (key == HET_TUNE_SM_BUDGET) {
+    if (value < 0) return fail(HET_EARG, "het_tune: SM budget must be >= 0");
+    het::g_sm_budget = value;
+    return HET_OK;
+  }
+  if (key == HET_TUNE_SYMM_TIMEOUT_MS) return het::set_symm_timeout_ms(value);
   if (key == HET_TUNE_ACC_VARIANT) {
     if (value < 0 || value >= static_cast<int>(sizeof(kAccShapes) / sizeof(kAccShapes[0])))
       return fail(HET_EARG, "het_tune: accumulate variant %d out of range", value);
@@ -809,6 +834,12 @@ int het_tune(int key, int value) {
     return HET_OK;
   }
   return fail(HET_EARG, "het_tune: unknown key %d", key);
+}
+
+int het_probe_smid(int32_t* out, int ctas, void* stream) {
+  if (!out || ctas < 1) return fail(HET_EARG, "het_probe_smid: bad args");
+  probe_smid_kernel<<<ctas, 128, 0, static_cast<cudaStream_t>(stream)>>>(out);
+  return het::check_launch("het_probe_smid");
 }
 
 int het_fill_f32(float* dst, float value, int64_t n, void* stream) {

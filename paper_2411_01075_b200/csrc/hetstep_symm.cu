@@ -39,9 +39,16 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kUnroll = 8;                   // independent 16-byte remote ops per thread
 constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
-constexpr uint64_t kSpinTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s wall clock
+// Barrier spin limit (wall clock); het_tune(HET_TUNE_SYMM_TIMEOUT_MS) overrides it
+// so a fault-injection test need not wait the full 10 s.
+uint64_t g_spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
 
 __device__ int g_symm_status = 0;
+
+// het_symm_status_async: the sticky status copied to `dst` (device memory or
+// pinned host memory, which is device-mapped under UVA) stream-ordered after
+// the step's collectives, so the host can check it without a device sync.
+__global__ void status_copy_kernel(int32_t* dst) { *dst = *(volatile int*)&g_symm_status; }
 
 struct Args {
   het_symm_t s;
@@ -57,6 +64,7 @@ struct Args {
   // from_offset). -1 / 0 = none.
   int relay_to = -1, relay_from = -1;
   int64_t relay_vecs = 0, from_count = 0, from_offset = 0, from_vecs = 0;
+  uint64_t timeout_ns = 0;    // barrier spin limit (g_spin_timeout_ns at launch)
 };
 
 __device__ __forceinline__ uint32_t* slot(uint64_t owner_base, uint64_t signal_off, int channel,
@@ -94,8 +102,20 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 // Scalar view of het_symm_t held in registers (the peer table lives in smem).
 struct Sym {
   int nranks, rank;
-  uint64_t mc_base, signal_off;
+  uint64_t mc_base, signal_off, timeout_ns;
 };
+
+// Spin until the slot reaches `epoch`; on timeout record HET_SYMM_TIMEOUT
+// (read back by het_symm_status / het_symm_status_async) and give up.
+__device__ __forceinline__ void wait_epoch(const uint32_t* p, uint32_t epoch, uint64_t timeout_ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (static_cast<int32_t>(ld_acquire_sys(p) - epoch) < 0) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(&g_symm_status, HET_SYMM_TIMEOUT);
+      break;
+    }
+  }
+}
 
 // `peer` is the CTA's shared copy of the peer base table.
 __device__ void cross_barrier(const Sym& s, const uint64_t* peer, int channel, int kind,
@@ -105,14 +125,8 @@ __device__ void cross_barrier(const Sym& s, const uint64_t* peer, int channel, i
   if (t < s.nranks) {
     __threadfence_system();
     st_release_sys(slot(peer[t], s.signal_off, channel, kind, blockIdx.x, s.rank), epoch);
-    const uint32_t* mine = slot(peer[s.rank], s.signal_off, channel, kind, blockIdx.x, t);
-    const uint64_t t0 = globaltimer_ns();
-    while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
-      if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
-        atomicExch(&g_symm_status, HET_SYMM_TIMEOUT);
-        break;
-      }
-    }
+    wait_epoch(slot(peer[s.rank], s.signal_off, channel, kind, blockIdx.x, t), epoch,
+               s.timeout_ns);
   }
   __syncthreads();
 }
@@ -244,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
                                                            const __grid_constant__ Args a) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
-  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off};
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
   cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank released its copy of the unit
   const int64_t n = a.count;
   const uint64_t dst0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;  // byte offset
@@ -281,15 +295,8 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
     ag_push<NR>(src, h2, 0, direct, dst0, peer, nr, all, src_vec);
     if (a.relay_from >= 0) {
       if (threadIdx.x == 0) {
-        const uint32_t* mine =
-            slot(peer[s.rank], s.signal_off, a.channel, 2, blockIdx.x, a.relay_from);
-        const uint64_t t0 = globaltimer_ns();
-        while (static_cast<int32_t>(ld_acquire_sys(mine) - a.epoch) < 0) {
-          if (globaltimer_ns() - t0 > kSpinTimeoutNs) {
-            atomicExch(&g_symm_status, HET_SYMM_TIMEOUT);
-            break;
-          }
-        }
+        wait_epoch(slot(peer[s.rank], s.signal_off, a.channel, 2, blockIdx.x, a.relay_from),
+                   a.epoch, s.timeout_ns);
       }
       __syncthreads();
       const uint64_t fdst0 = a.data_off + static_cast<uint64_t>(a.from_offset) * 2;
@@ -377,7 +384,7 @@ template <bool MC, int NR>
 __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const __grid_constant__ Args a) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
-  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off};
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
   cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's accumulator is final
   const int64_t n = a.count;
   const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 4;
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restric
                                                                 const __grid_constant__ Weights wt) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
-  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off};
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
   cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's gradient is staged
   const int64_t n = a.count;
   const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;
@@ -646,6 +653,14 @@ int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offset
 
 }  // namespace
 
+namespace het {
+int set_symm_timeout_ms(int ms) {
+  if (ms < 1) return fail(HET_EARG, "het_tune: symmetric barrier timeout must be >= 1 ms");
+  g_spin_timeout_ns = static_cast<uint64_t>(ms) * 1000ull * 1000ull;
+  return HET_OK;
+}
+}  // namespace het
+
 extern "C" {
 
 int64_t het_symm_signal_bytes(void) {
@@ -663,6 +678,12 @@ int het_symm_status(int reset) {
   return v;
 }
 
+int het_symm_status_async(int32_t* dst, void* stream) {
+  if (!dst) return fail(HET_EARG, "het_symm_status_async: null dst");
+  status_copy_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(dst);
+  return het::check_launch("het_symm_status_async");
+}
+
 int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit_off,
                             const int64_t* counts, const int64_t* offsets, uint32_t epoch,
                             int channel, int policy, int ctas, void* stream) {
@@ -671,7 +692,8 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
   if (counts[s->rank] > 0 && !src) return fail(HET_EARG, "het_symm_allgather_pack: null src");
   if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
-  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1, -1, -1, 0, 0, 0, 0};
+  Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1, -1, -1, 0, 0, 0, 0,
+         g_spin_timeout_ns};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool mc = policy == HET_SYMM_RELAY ? false : pick_multicast(s, counts, policy);
   if (policy == HET_SYMM_RELAY) relay_plan(s, counts, offsets, unit_off, &a);
@@ -690,6 +712,7 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter: null out");
   if (acc_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter: acc offset not 16B aligned");
   Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
+  a.timeout_ns = g_spin_timeout_ns;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool mc = pick_multicast(s, counts, policy);
 #define HET_RS(MCV, NRV) symm_rs_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(out, a)
@@ -709,6 +732,7 @@ int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* 
   if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: null out");
   if (grad_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: grad offset not 16B aligned");
   Args a{*s, grad_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
+  a.timeout_ns = g_spin_timeout_ns;
   Weights wt{};
   for (int j = 0; j < s->nranks; ++j) wt.w[j] = weights[j];
   cudaStream_t st = static_cast<cudaStream_t>(stream);

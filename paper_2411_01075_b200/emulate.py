@@ -64,4 +64,8 @@ def emulate_tier(cluster: ClusterSpec, rank: int, device: torch.device, *,
         raw = green.Stream()
         stream = raw if isinstance(raw, torch.cuda.Stream) else torch.cuda.Stream(
             stream_id=raw.stream_id, device_index=raw.device_index, device_type=raw.device_type)
+        # persistent grids of the owned kernels sized for the partition (one wave
+        # fills nsm SMs instead of 148 x k CTAs queueing in it)
+        from . import hetstep as K
+        K.set_sm_budget(nsm)
     return TierEmulation(gpu.profile_key, frac, nsm, cap, stream, green)

@@ -37,7 +37,8 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
            "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi",
-           "het_embedding_grad_dev", "het_adamw_coef", "het_adamw_devcoef")
+           "het_embedding_grad_dev", "het_adamw_coef", "het_adamw_devcoef",
+           "het_symm_status_async", "het_probe_smid")
 
 
 class HetSeg(ctypes.Structure):
@@ -110,6 +111,8 @@ def load(build: bool = False) -> ctypes.CDLL:
                                        i32, vp, vp], i32),
         "het_symm_signal_bytes": ([], i64),
         "het_symm_status": ([i32], i32),
+        "het_symm_status_async": ([vp, vp], i32),
+        "het_probe_smid": ([vp, i32, vp], i32),
         "het_symm_allgather_pack": ([ctypes.POINTER(HetSymm), vp, ctypes.c_uint64,
                                      ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
                                      i32, i32, i32, vp], i32),
@@ -379,6 +382,8 @@ def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: tor
 
 
 HET_TUNE_ACC_VARIANT = 1
+HET_TUNE_SM_BUDGET = 2
+HET_TUNE_SYMM_TIMEOUT_MS = 3
 LN_DIMS = (256, 768, 1024)
 
 
@@ -949,6 +954,23 @@ def layer_norm(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, eps: float = 1
     return LayerNormFn.apply(x, w, b, eps)
 
 
+def probe_smid(ctas: int, stream=None) -> torch.Tensor:
+    """SM id each of `ctas` CTAs ran on (emulation diagnostic)."""
+    out = torch.full((ctas,), -1, dtype=torch.int32, device=torch.cuda.current_device())
+    _check(load().het_probe_smid(out.data_ptr(), int(ctas), _stream(stream)), "het_probe_smid")
+    return out
+
+
+def set_sm_budget(nsm: int) -> None:
+    """Persistent grids sized for `nsm` SMs (a green-context partition); 0 = all."""
+    tune(HET_TUNE_SM_BUDGET, int(nsm))
+
+
+def set_symm_timeout_ms(ms: int) -> None:
+    """Spin limit of the fused collectives' cross-rank barriers (default 10 s)."""
+    tune(HET_TUNE_SYMM_TIMEOUT_MS, int(ms))
+
+
 def tune(key: int, value: int) -> None:
     _check(load().het_tune(int(key), int(value)), "het_tune")
 
@@ -1178,3 +1200,59 @@ class SymmWorkspace:
     @staticmethod
     def status(reset: bool = False) -> int:
         return int(load().het_symm_status(int(reset)))
+
+
+class CollectiveFault(RuntimeError):
+    """A fused collective's cross-rank barrier timed out: the kernel went on
+    without its peers, so the buffers it produced (gathered parameters,
+    reduced gradient shards) are not valid."""
+
+
+class StatusWatch:
+    """Asynchronous check of the fused collectives' sticky device status.
+
+    ``record(stream, tag)`` queues het_symm_status_async on `stream` (after the
+    step's collectives) into a slot of a small pinned host ring and an event;
+    ``poll()`` checks every slot whose event has completed and ``check()``
+    waits for all of them. A non-zero status raises CollectiveFault naming
+    the tag (the step) it was first seen after. No device-wide sync: the
+    step driver polls the previous steps' slots at the start of each step."""
+
+    def __init__(self, slots: int = 4):
+        self.host = torch.zeros(slots, dtype=torch.int32).pin_memory()
+        self.ev: list = [None] * slots
+        self.tag: list = [None] * slots
+        self.next = 0
+
+    def record(self, stream, tag) -> None:
+        k = self.next % len(self.ev)
+        if self.ev[k] is not None:          # slot still pending: settle it first
+            self._settle(k, block=True)
+        _check(load().het_symm_status_async(self.host[k:].data_ptr(), _stream(stream)),
+               "het_symm_status_async", "het_probe_smid")
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.ev[k], self.tag[k] = ev, tag
+        self.next += 1
+
+    def _settle(self, k: int, block: bool) -> None:
+        ev = self.ev[k]
+        if ev is None:
+            return
+        if not block and not ev.query():
+            return
+        ev.synchronize()
+        v, tag = int(self.host[k]), self.tag[k]
+        self.ev[k] = self.tag[k] = None
+        if v != 0:
+            raise CollectiveFault(
+                f"fused collective barrier timed out (status {v}) by {tag}: the gathered "
+                f"parameters / reduced gradients of that step are invalid")
+
+    def poll(self) -> None:
+        for k in range(len(self.ev)):
+            self._settle(k, block=False)
+
+    def check(self) -> None:
+        for k in range(len(self.ev)):
+            self._settle(k, block=True)

@@ -202,6 +202,10 @@ class UnevenFSDPTrainer:
         self.rank_weights = [a.microbatch / plan.total_batch for a in plan.assignments]
         self._set_routes(self.symm is not None)
         self.route_check = None
+        # fused-collective fault check: the sticky barrier status is copied to pinned
+        # host memory after every step's collectives (no device sync) and polled at
+        # the start of the next step; a timeout raises K.CollectiveFault
+        self._watch = K.StatusWatch() if self.symm is not None else None
         if self.symm is not None and check_routes:
             self.route_check = self._check_symm_routes()
             if not self.route_check["ok"]:       # every rank agrees: all-NCCL routes
@@ -697,6 +701,8 @@ class UnevenFSDPTrainer:
         if self.m > 0 and (tok.shape[0] != self.m * self.l or tok.shape[1] != arch.seq + 1):
             raise InputError(f"rank {self.rank} expects tokens [{self.m * self.l}, {arch.seq + 1}]")
         multi = self.N > 1
+        if self._watch is not None:
+            self._watch.poll()           # earlier steps' collectives: raise on a timeout
         unit_names = [nm for nm, _ in arch.unit_layout()]
         root_names = [nm for nm, _ in arch.root_layout()]
         loss = torch.zeros((), dtype=torch.float32, device=self.device)
@@ -909,6 +915,8 @@ class UnevenFSDPTrainer:
         if multi:
             rs_ev[root] = self._rs(root, racc, self._event(comp))
             comp.wait_event(rs_ev[root])            # RS stream is in order: all shards ready
+            if self._watch is not None:
+                self._watch.record(comp, f"step {self.steps + 1} on rank {self.rank}")
 
         # ---- optimizer -------------------------------------------------------
         self.steps += 1
@@ -928,6 +936,12 @@ class UnevenFSDPTrainer:
             b.record()
         self.launches += 1
         return loss
+
+    def check_faults(self) -> None:
+        """Wait for every step issued so far and raise K.CollectiveFault if any
+        fused collective's cross-rank barrier timed out (its outputs are invalid)."""
+        if self._watch is not None:
+            self._watch.check()
 
     # ------------------------------------------------------------------ views for tests
     def full_units(self, which: str = "p32") -> list[torch.Tensor]:

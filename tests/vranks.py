@@ -1,0 +1,124 @@
+"""Virtual-rank harness: N ranks of the fused symmetric collectives on ONE GPU.
+
+The fused kernels (csrc/hetstep_symm.cu) address every rank's copy of the
+symmetric buffer through ``het_symm_t.peer_base[j]``; they never ask where
+that memory lives. Here one allocation holds N equal copies (rank j's copy at
+``base + j * stride``), N descriptors differ only in ``rank``, and rank r's
+kernel is launched on its own stream. The N launches run concurrently, meet
+at the same in-kernel CTA-pairwise barriers as on N GPUs (peer stores and
+loads are plain HBM accesses here), and produce the same bytes, so the
+driver's 1-GPU test run exercises the NR = 2 / 4 / 8 specialisations, the
+peer and relay all-gathers and both reduce-scatters against the oracle.
+
+Co-residency: every barrier needs CTA b of all N launches resident at once.
+``ctas * N`` is kept below one CTA per SM (148), so they always are, and the
+barriers cannot time out unless a rank is deliberately left out.
+
+This is test infrastructure (it measures nothing: a "link" is local HBM).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from paper_2411_01075_b200 import hetstep as K
+
+ALIGN = 256
+
+
+class VirtualGroup:
+    def __init__(self, n: int, regions: Sequence[tuple[str, int, torch.dtype]],
+                 device: torch.device, ctas: int | None = None):
+        if not 1 <= n <= K.HET_MAX_RANKS:
+            raise ValueError("1..8 virtual ranks")
+        lib = K.load()
+        self.n, self.device = n, device
+        self.offsets, pos = {}, 0
+        self.regions = list(regions)
+        for name, numel, dtype in regions:
+            self.offsets[name] = pos
+            esz = torch.tensor([], dtype=dtype).element_size()
+            pos += (numel * esz + ALIGN - 1) // ALIGN * ALIGN
+        self.signal_off = pos
+        per_rank = pos + int(lib.het_symm_signal_bytes())
+        self.stride = (per_rank + 4095) // 4096 * 4096
+        self.raw = torch.zeros(n * self.stride, dtype=torch.uint8, device=device)
+        base = self.raw.data_ptr()
+        self.desc = []
+        for r in range(n):
+            d = K.HetSymm()
+            d.nranks, d.rank = n, r
+            for j in range(n):
+                d.peer_base[j] = base + j * self.stride
+            d.mc_base = 0                       # one GPU: no NVLS multicast object
+            d.signal_off = self.signal_off
+            self.desc.append(d)
+        # one CTA per SM at most across all virtual ranks (co-residency of every barrier)
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        self.ctas = ctas if ctas is not None else max(1, min(32, (sms - 4) // n))
+        if self.ctas * n > sms:
+            raise ValueError("ctas * n exceeds one CTA per SM: barriers could deadlock")
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(n)]
+        self.epoch = [0, 0]
+        torch.cuda.synchronize(device)
+
+    def view(self, r: int, name: str) -> torch.Tensor:
+        for nm, numel, dtype in self.regions:
+            if nm == name:
+                o = r * self.stride + self.offsets[name]
+                esz = torch.tensor([], dtype=dtype).element_size()
+                return self.raw[o:o + numel * esz].view(dtype)
+        raise KeyError(name)
+
+    def _launch(self, fn, ranks) -> None:
+        torch.cuda.synchronize(self.device)     # inputs written on the default stream
+        for r in ranks:
+            fn(r, self.streams[r].cuda_stream)
+        torch.cuda.synchronize(self.device)
+
+    def allgather_pack(self, srcs: Sequence[torch.Tensor], region: str, elem_off: int,
+                       counts: Sequence[int], offsets: Sequence[int], policy: int = K.SYMM_AUTO,
+                       ranks: Sequence[int] | None = None) -> None:
+        self.epoch[0] += 1
+        lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
+        byte_off = self.offsets[region] + 2 * elem_off
+
+        def go(r, st):
+            src = srcs[r].data_ptr() if srcs[r].numel() else None
+            K._check(lib.het_symm_allgather_pack(ctypes.byref(self.desc[r]), src, byte_off, c, o,
+                                                 self.epoch[0], 0, policy, self.ctas, st),
+                     "het_symm_allgather_pack")
+        self._launch(go, range(self.n) if ranks is None else ranks)
+
+    def reduce_scatter(self, region: str, elem_off: int, outs: Sequence[torch.Tensor],
+                       counts: Sequence[int], offsets: Sequence[int], end_barrier: bool = True,
+                       policy: int = K.SYMM_AUTO) -> None:
+        self.epoch[1] += 1
+        lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
+        byte_off = self.offsets[region] + 4 * elem_off
+
+        def go(r, st):
+            out = outs[r].data_ptr() if outs[r].numel() else None
+            K._check(lib.het_symm_reduce_scatter(ctypes.byref(self.desc[r]), byte_off, out, c, o,
+                                                 self.epoch[1], 1, int(end_barrier), policy,
+                                                 self.ctas, st),
+                     "het_symm_reduce_scatter")
+        self._launch(go, range(self.n))
+
+    def reduce_scatter_bf16(self, region: str, elem_off: int, outs: Sequence[torch.Tensor],
+                            counts: Sequence[int], offsets: Sequence[int],
+                            weights: Sequence[float], end_barrier: bool = True) -> None:
+        self.epoch[1] += 1
+        lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
+        byte_off = self.offsets[region] + 2 * elem_off
+        w = (ctypes.c_float * len(weights))(*[float(x) for x in weights])
+
+        def go(r, st):
+            out = outs[r].data_ptr() if outs[r].numel() else None
+            K._check(lib.het_symm_reduce_scatter_bf16(ctypes.byref(self.desc[r]), byte_off, out,
+                                                      c, o, w, self.epoch[1], 1,
+                                                      int(end_barrier), self.ctas, st),
+                     "het_symm_reduce_scatter_bf16")
+        self._launch(go, range(self.n))
