@@ -51,6 +51,16 @@ def peaks() -> tuple[float, str]:
     return HBM_FALLBACK, "fallback"
 
 
+def bf16_sustained() -> float:
+    """Sustained dense bf16 TFLOP/s from MEASURED_PEAKS.json (B200_PROFILING.md
+    fallback otherwise)."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["bf16_tflops_sustained"])
+    except Exception:
+        return 1388.5
+
+
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled while the timed
     region runs: NVML every 50 ms (nvidia-smi every 200 ms if NVML is absent),
@@ -176,15 +186,23 @@ def make_comms(world: int, rank: int):
     return K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
 
 
-def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None,
-                       warmup: int = 1) -> dict:
-    """The oracle step (torch CPU fp32, N simulated ranks in one process) on a
-    bounded sample of the same workload: `sample` global samples per step."""
+def cpu_reference_rate(config: str, global_batch: int, max_seconds: float = 20.0,
+                       steps: int | None = None, warmup: int = 1) -> dict:
+    """The oracle step (torch CPU fp32; oracle/model_oracle.py) timed on this
+    host's cores on a bounded sample of the workload, amortised like the GPU
+    step: each timed CPU step runs the forward + backward of ONE sample
+    (Eq. 1-weighted, as one rank of the step) and one AdamW over the whole
+    model; the rate of a global_batch-sample step is then
+        B / (B * t_sample + t_adamw),
+    the per-sample and per-step parts measured separately. No planner call and
+    nothing from the package's native libraries: the workload comes from the
+    config's architecture and batch alone."""
     from oracle import model_oracle as MO
-    from paper_2411_01075_b200.model import init_flat
+    from paper_2411_01075_b200.data import tokens
+    from paper_2411_01075_b200.model import ARCHS, init_flat
     cores = len(os.sched_getaffinity(0))
     torch.set_num_threads(cores)
-    arch = job.arch
+    arch = ARCHS[CONFIGS[config].arch]
     units = []
     for u in range(arch.layers + 1):
         g = torch.Generator().manual_seed(u)
@@ -192,30 +210,52 @@ def cpu_reference_rate(job, max_seconds: float = 20.0, steps: int | None = None,
                                "cpu"))
     opt = dict(lr=OPT.lr, beta1=OPT.betas[0], beta2=OPT.betas[1], eps=OPT.eps,
                weight_decay=OPT.weight_decay)
-    st = MO.CPUStep(arch, units[:-1], units[-1], opt)
-    sample = 2 if arch.d >= 512 else 8
-    # sample: the first `sample` global samples, split over two simulated ranks as m=1 each
-    micro = [(1, sample // 2), (1, sample - sample // 2)]
-    from paper_2411_01075_b200.data import tokens
-    for w in range(warmup):                 # untimed warm-up steps
-        toks = tokens(np.arange(sample), arch.seq, arch.vocab, SEED, 10_000 + w)
-        st.step([toks[:micro[0][1]], toks[micro[0][1]:]], micro)
-    done, t_total, n = 0, 0.0, 0
-    while True:
-        toks = tokens(np.arange(sample), arch.seq, arch.vocab, SEED, n)
-        parts = [toks[:micro[0][1]], toks[micro[0][1]:]]
+    params = units[:-1] + [units[-1]]
+    mom = [(torch.zeros_like(t), torch.zeros_like(t)) for t in params]
+
+    def one(n: int) -> tuple[float, float]:
+        tok = tokens(np.array([n % global_batch]), arch.seq, arch.vocab, SEED, n)
         t0 = time.perf_counter()
-        st.step(parts, micro)
-        t_total += time.perf_counter() - t0
-        done += sample
+        gu, gr, _ = MO.weighted_gradient(arch, units[:-1], units[-1], [tok],
+                                         [(1, 1)])
+        t1 = time.perf_counter()
+        with torch.no_grad():
+            for t, g, (m, v) in zip(params, gu + [gr], mom):
+                MO.adamw_(t, g, m, v, n + 1, **opt)
+        return t1 - t0, time.perf_counter() - t1
+
+    for w in range(warmup):
+        one(10_000 + w)
+    fb, ad, n = [], [], 0
+    while True:
+        a, b = one(n)
+        fb.append(a)
+        ad.append(b)
         n += 1
-        if (steps is not None and n >= steps) or (steps is None and t_total >= max_seconds):
+        if (steps is not None and n >= steps) or (steps is None and sum(fb) + sum(ad) >= max_seconds):
             break
-    return {"value": done / t_total, "unit": "samples/s", "cores": cores, "kind": "port",
-            "sample": f"{n} timed CPU steps (after {warmup} warm-up) x {sample} samples of "
-                      f"{job.config.name} (seq {arch.seq}) over 2 simulated ranks, torch CPU "
-                      f"fp32 oracle (oracle/model_oracle.py)",
-            "seconds": t_total}
+    t_sample, t_adamw = float(np.mean(fb)), float(np.mean(ad))
+    rate = global_batch / (global_batch * t_sample + t_adamw)
+    return {"value": rate, "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{n} timed CPU steps (after {warmup} warm-up), each = forward+backward of "
+                      f"1 sample of {config} (seq {arch.seq}) + one AdamW over all "
+                      f"{arch.layers * arch.unit_params + arch.root_params} params, torch CPU "
+                      f"fp32 oracle (oracle/model_oracle.py); rate of the {global_batch}-sample "
+                      f"step = B / (B * {t_sample * 1e3:.1f} ms + {t_adamw * 1e3:.1f} ms)",
+            "sample_ms": t_sample * 1e3, "adamw_ms": t_adamw * 1e3,
+            "seconds": float(sum(fb) + sum(ad))}
+
+
+def describe(config: str, world: int) -> str:
+    """The workload as run at this rank count (tiers: configs.CONFIGS)."""
+    from collections import Counter
+    cfg = CONFIGS[config]
+    tiers = [cfg.tiers[i % len(cfg.tiers)] for i in range(world)]
+    tally = ", ".join(f"{k} x{v}" for k, v in Counter(tiers).items())
+    if world == 1:
+        return (f"{cfg.description}; N=1 runs the first tier alone ({tiers[0]}), "
+                f"the uneven split starts at N=2")
+    return f"{cfg.description}; N={world} tiers: {tally}"
 
 
 def run_reference(args) -> None:
@@ -223,18 +263,21 @@ def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    job = build_job(args.config, max(args.gpus, world), measured=True)   # our arm's plan
-    ref = cpu_reference_rate(job, steps=args.steps, warmup=args.warmup)
+    n = max(args.gpus, world)
+    cfg = CONFIGS[args.config]
+    from paper_2411_01075_b200.model import ARCHS
+    B = cfg.batch_per_gpu * n               # the GPU arm's global batch (weak scaling)
+    ref = cpu_reference_rate(args.config, B, steps=args.steps, warmup=args.warmup)
     line = {"metric": "train samples/s", "value": ref["value"], "unit": "samples/s",
-            "impl": "reference", "n_gpus": max(args.gpus, world), "steps": args.steps,
+            "impl": "reference", "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": job.config.name,
-                                            "description": job.config.description},
+            "data": "synthetic", "scaling": "weak",
+            "config": {"workload": args.config, "description": describe(args.config, n),
+                       "global_batch": B, "seq_len": ARCHS[cfg.arch].seq},
             "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": ref["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
 
 
 def tier_capacity(job, no_emulate: bool) -> float:
@@ -456,6 +499,7 @@ def main() -> None:
 
     B = plan.total_batch
     hbm, hbm_kind = peaks()
+    bf16_peak = bf16_sustained()
     # dominant owned kernel = the one with the largest share of the timed steps
     if not kern:                              # --no-kernel-timers
         kern = {"adamw": {"launches": 0, "ms_total": 0.0, "ms_mean": 0.0, "bytes_total": 0.0,
@@ -467,7 +511,7 @@ def main() -> None:
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            ref = cpu_reference_rate(job)
+            ref = cpu_reference_rate(args.config, B)
             cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
         tok_bytes = sum(h.numel() * h.element_size() for h in host[:1]) * world
         line = {
@@ -476,7 +520,7 @@ def main() -> None:
             "step_ms": step_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic tokens (splitmix64), random-init weights",
-            "config": {"workload": job.config.name, "description": job.config.description,
+            "config": {"workload": job.config.name, "description": describe(args.config, world),
                        "global_batch": B, "seq_len": arch.seq,
                        "plan": [[a.microbatch, a.num_microbatches, a.state_ratio]
                                 for a in plan.assignments],
@@ -508,6 +552,12 @@ def main() -> None:
                          "frac": achieved / hbm if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": kern[dom]["bytes_per_launch"],
                          "step_share": kern[dom]["ms_total"] / steps_timed / ms},
+            # model FLOPs (6 P T + attention, no recompute) per second against the
+            # measured sustained dense bf16 peak: the step-level context of the line
+            "mfu": {"model_tflop_per_step": B * arch.model_flops_per_sample() / 1e12,
+                    "achieved_tflops": B * arch.model_flops_per_sample() / (ms * 1e-3) / 1e12,
+                    "peak_tflops": bf16_peak,
+                    "frac": B * arch.model_flops_per_sample() / (ms * 1e-3) / 1e12 / bf16_peak},
             "kernels": {k: dict(v, ms_per_step=v["ms_total"] / steps_timed)
                         for k, v in kern.items()},
             "gpu_launches": launches,

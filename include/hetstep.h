@@ -150,13 +150,6 @@ int het_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* r
 /* Rotary position embedding in place on bf16 [rows, heads, dh] (row r at
  * position r % seq, rotate-half pairs); inverse=1 applies the backward
  * (inverse) rotation. */
-/* Cross-entropy loss and gradient in one pass (the head's upstream gradient
- * is known: grad_scale, normally 1): loss[r] = logsumexp(row) - row[target],
- * and the row is overwritten in place with grad_scale/rows * (softmax - onehot).
- * vocab % 8 == 0, vocab <= 65536. */
-int het_xent_fused(void* logits, const int64_t* target, int64_t rows, int64_t vocab,
-                   float grad_scale, float* loss, void* stream);
-
 /* Residual add fused into the norms: xsum = bf16(x + r) is written and
  * normalised (forward); the backward adds the residual path's gradient dres
  * to the norm's input gradient in the same pass (dres may be NULL). */
@@ -207,26 +200,6 @@ int het_bias_grad(const void* g, int64_t rows, int64_t n, void* db, float* parti
 int het_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
 int het_gelu_bwd_bias(const void* dy, const void* pre, void* dpre, int64_t rows, int64_t n,
                       void* db, float* partial, void* stream);
-
-/* Library GEMM with a fused epilogue (cuBLASLt; bf16 A, B, D, fp32 compute), in
- * cuBLAS column-major terms: D[m, n] = op(A) op(B) with op = transpose when
- * trans_* = 1, then the epilogue:
- *   HET_LT_BIAS           D += bias[m]
- *   HET_LT_GELU_BIAS      D = gelu_tanh(D + bias[m])
- *   HET_LT_GELU_AUX_BIAS  as GELU_BIAS, and aux[m, n] (ld ldaux) = D + bias (pre-activation)
- *   HET_LT_DGELU_BGRAD    D = D * gelu_tanh'(aux); bias[m] = sum over n of D (bias gradient)
- *   HET_LT_BGRADB         bias[n] = sum over k of op(B) (bias gradient of a weight-gradient GEMM)
- * bias is bf16. Plans (descriptors + heuristic algorithm) are cached per shape. */
-#define HET_LT_NONE 0
-#define HET_LT_BIAS 1
-#define HET_LT_GELU_BIAS 2
-#define HET_LT_GELU_AUX_BIAS 3
-#define HET_LT_DGELU_BGRAD 4
-#define HET_LT_BGRADB 5
-int het_lt_matmul(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, const void* a,
-                  int64_t lda, const void* b, int64_t ldb, void* d, int64_t ldd, int epilogue,
-                  void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes,
-                  void* stream);
 
 /* Launch-shape tuning knobs (process-wide; defaults are the measured best).
  * HET_TUNE_ACC_VARIANT: het_accumulate CTA shape index 0..5

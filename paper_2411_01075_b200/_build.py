@@ -78,8 +78,6 @@ def build_step(force: bool = False, verbose: bool = False) -> Path:
            f"-I{INCLUDE}", f"-I{nccl / 'include'}",
            *[str(s) for s in srcs if s.suffix == ".cu"],
            f"-L{nccl / 'lib'}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={nccl / 'lib'}",
-           f"-L{_cublas_root() / 'lib'}", "-l:libcublasLt.so.12",
-           "-Xlinker", f"-rpath={_cublas_root() / 'lib'}",
            "-o", str(tmp)]
     _run(cmd)
     os.replace(tmp, STEP_LIB)

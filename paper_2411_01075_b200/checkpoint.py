@@ -17,6 +17,7 @@ ranks whose ranges overlap it, so a job can resume on a re-planned cluster.
 from __future__ import annotations
 
 import json
+import os
 from pathlib import Path
 
 import torch
@@ -35,8 +36,11 @@ def _tables(layout: RankLayout) -> dict:
 
 
 def save_shards(path: str | Path, layout: RankLayout, buffers: dict[str, torch.Tensor],
-                step: int, plan: TrainPlan | None = None) -> None:
-    """Write this rank's ranges of every state buffer (flat local layout)."""
+                step: int, plan: TrainPlan | None = None, barrier=None) -> None:
+    """Write this rank's ranges of every state buffer (flat local layout).
+    Every file is written to a temporary name and renamed into place; with
+    `barrier` (a cross-rank barrier callable) rank 0 writes meta.json only
+    after every rank's file is in place, so meta.json marks a complete save."""
     d = Path(path)
     d.mkdir(parents=True, exist_ok=True)
     per_unit = {}
@@ -45,11 +49,23 @@ def save_shards(path: str | Path, layout: RankLayout, buffers: dict[str, torch.T
         per_unit[name] = [buf[off:off + cnt].detach().to("cpu", torch.float32).clone()
                           for off, cnt in (layout.local_range(u)
                                            for u in range(layout.blocks + 1))]
-    torch.save({"rank": layout.rank, "step": step, "state": per_unit}, d / f"rank{layout.rank}.pt")
+    _atomic(d / f"rank{layout.rank}.pt",
+            lambda tmp: torch.save({"rank": layout.rank, "step": step, "state": per_unit}, tmp))
+    if barrier is not None:
+        barrier()            # every rank file is complete before meta.json names them
     if layout.rank == 0:
-        (d / "meta.json").write_text(json.dumps({"step": step, **_tables(layout)}, indent=1))
         if plan is not None:
-            save_plan(plan, d / "plan.json")
+            _atomic(d / "plan.json", lambda tmp: save_plan(plan, tmp))
+        # meta.json last: a reader that sees it sees a complete checkpoint
+        _atomic(d / "meta.json", lambda tmp: Path(tmp).write_text(
+            json.dumps({"step": step, **_tables(layout)}, indent=1)))
+
+
+def _atomic(dst: Path, write) -> None:
+    """write(tmp) then rename over dst (POSIX rename is atomic on one filesystem)."""
+    tmp = dst.with_name(f".{dst.name}.tmp{os.getpid()}")
+    write(tmp)
+    os.replace(tmp, dst)
 
 
 def load_shards(path: str | Path, layout: RankLayout) -> tuple[dict[str, list[torch.Tensor]], int]:
@@ -60,6 +76,9 @@ def load_shards(path: str | Path, layout: RankLayout) -> tuple[dict[str, list[to
     if meta["unit_params"] != layout.unit_params or meta["root_params"] != layout.root_params \
             or len(meta["counts"]) != layout.blocks + 1:
         raise InputError("checkpoint was written for a different model shape")
+    missing = [r for r in range(meta["nranks"]) if not (d / f"rank{r}.pt").exists()]
+    if missing:
+        raise InputError(f"checkpoint is incomplete: missing rank files {missing}")
     same = meta["counts"] == [list(c) for c in layout.counts]
     cache: dict[int, dict] = {}
 
@@ -99,8 +118,13 @@ def save_trainer(trainer, path: str | Path) -> None:
     """Checkpoint an UnevenFSDPTrainer (every rank calls this)."""
     if trainer.cuda:
         torch.cuda.synchronize(trainer.device)
+    barrier = None
+    if trainer.N > 1:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            barrier = dist.barrier
     save_shards(path, trainer.L, {n: getattr(trainer, n) for n in STATE}, trainer.steps,
-                trainer.plan)
+                trainer.plan, barrier=barrier)
 
 
 def load_trainer(trainer, path: str | Path) -> int:

@@ -388,88 +388,11 @@ __global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(
   }
 }
 
-// Loss AND gradient in one pass for the head's known upstream gradient: the
-// row (V <= 512 * 8 * NV) is held in registers, so it is read from HBM once
-// and dlogits = scale * (softmax - onehot) overwrites it in place.
-template <int NV>
-__global__ void __launch_bounds__(kXentThreads) xent_fused_kernel(
-    __nv_bfloat16* __restrict__ logits, const int64_t* __restrict__ target, int64_t V,
-    float scale, float* __restrict__ loss_out) {
-  __shared__ float smem[33];
-  const int64_t row = blockIdx.x;
-  __nv_bfloat16* x = logits + row * V;
-  const int64_t nv = V / 8;
-  const int64_t tgt = target[row];
-  uint4 r[NV];
-  float mx = -INFINITY, sum = 0.f;
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int64_t i = threadIdx.x + static_cast<int64_t>(j) * kXentThreads;
-    if (i < nv) r[j] = *reinterpret_cast<const uint4*>(x + i * 8);
-  }
-  float xt = 0.f;                                   // the target logit (one thread has it)
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int64_t i = threadIdx.x + static_cast<int64_t>(j) * kXentThreads;
-    if (i < nv) {
-      float f[8];
-      load8(reinterpret_cast<const __nv_bfloat16*>(&r[j]), f);
-      float m8 = f[0];
-#pragma unroll
-      for (int k = 1; k < 8; ++k) m8 = fmaxf(m8, f[k]);
-      if (m8 > mx) {
-        sum *= __expf(mx - m8);
-        mx = m8;
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        sum += __expf(f[k] - mx);
-        if (i * 8 + k == tgt) xt = f[k];
-      }
-    }
-  }
-  const float gmax = block_reduce(mx, true, smem);
-  const float gsum = block_reduce(sum * __expf(mx - gmax), false, smem);
-  const float lse = gmax + __logf(gsum);
-  const float xtg = block_reduce(xt, false, smem);  // only the owner contributes
-  if (threadIdx.x == 0) loss_out[row] = lse - xtg;
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int64_t i = threadIdx.x + static_cast<int64_t>(j) * kXentThreads;
-    if (i < nv) {
-      float f[8];
-      load8(reinterpret_cast<const __nv_bfloat16*>(&r[j]), f);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float pr = __expf(f[k] - lse);
-        f[k] = scale * (pr - (i * 8 + k == tgt ? 1.f : 0.f));
-      }
-      store8(x + i * 8, f);
-    }
-  }
-}
 
 }  // namespace
 
 extern "C" {
 
-int het_xent_fused(void* logits, const int64_t* target, int64_t rows, int64_t vocab,
-                   float grad_scale, float* loss, void* stream) {
-  if (!logits || !target || !loss || rows < 0 || vocab <= 0 || vocab > 16 * 8 * kXentThreads ||
-      (reinterpret_cast<uintptr_t>(logits) & 15) || (vocab % 8))
-    return fail(HET_EARG, "het_xent_fused: bad args (vocab %% 8, <= 65536, 16-byte alignment)");
-  if (rows == 0) return HET_OK;
-  const float scale = grad_scale / static_cast<float>(rows);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  auto L = static_cast<__nv_bfloat16*>(logits);
-  const int64_t per = (vocab / 8 + kXentThreads - 1) / kXentThreads;
-  const unsigned g = static_cast<unsigned>(rows);
-  if (per <= 4) xent_fused_kernel<4><<<g, kXentThreads, 0, st>>>(L, target, vocab, scale, loss);
-  else if (per <= 8) xent_fused_kernel<8><<<g, kXentThreads, 0, st>>>(L, target, vocab, scale, loss);
-  else if (per <= 13) xent_fused_kernel<13><<<g, kXentThreads, 0, st>>>(L, target, vocab, scale, loss);
-  else xent_fused_kernel<16><<<g, kXentThreads, 0, st>>>(L, target, vocab, scale, loss);
-  return het::check_launch("het_xent_fused");
-}
 
 int het_xent_fwd(const void* logits, const int64_t* target, int64_t rows, int64_t vocab,
                  float* lse, float* loss, void* stream) {

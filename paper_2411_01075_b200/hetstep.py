@@ -31,7 +31,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_layernorm_fwd", "het_layernorm_bwd", "het_xent_fwd", "het_xent_bwd",
            "het_rmsnorm_partial_floats", "het_rmsnorm_fwd", "het_rmsnorm_bwd", "het_rope_inplace",
            "het_swiglu_fwd", "het_swiglu_bwd", "het_rope_qkv_split", "het_rope_qkv_merge",
-           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_xent_fused", "het_lt_matmul", "het_rmsnorm_add_fwd",
+           "het_layernorm_add_fwd", "het_layernorm_bwd_add", "het_rmsnorm_add_fwd",
            "het_rmsnorm_bwd_add", "het_colsum_partial_floats", "het_bias_grad",
            "het_gelu_fwd", "het_gelu_bwd_bias", "het_comm_unique_id", "het_comm_init", "het_comm_destroy",
            "het_allgather_uneven", "het_reduce_scatter_uneven", "het_symm_signal_bytes",
@@ -84,9 +84,6 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_rmsnorm_bwd": ([vp, vp, vp, vp, vp, vp, vp, i64, i64, vp], i32),
         "het_rope_inplace": ([vp, i64, i32, i32, i64, i32, vp], i32),
         "het_xent_bwd": ([vp, vp, i64, i64, vp, vp, vp, vp], i32),
-        "het_xent_fused": ([vp, vp, i64, i64, f32, vp, vp], i32),
-        "het_lt_matmul": ([i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp, vp, i64,
-                           vp, i64, vp], i32),
         "het_swiglu_fwd": ([vp, vp, i64, vp, i64, i64, vp], i32),
         "het_rope_qkv_split": ([vp, vp, vp, vp, i64, i32, i32, i64, vp], i32),
         "het_layernorm_add_fwd": ([vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, f32, vp], i32),
@@ -453,20 +450,6 @@ class CrossEntropyFn(torch.autograd.Function):
         return lg, None
 
 
-def xent_value_and_grad(logits: torch.Tensor, target: torch.Tensor,
-                        grad_scale: float = 1.0) -> torch.Tensor:
-    """Mean cross-entropy of bf16 [rows, vocab] logits AND its gradient in one
-    pass: returns the loss (device scalar) and overwrites `logits` in place with
-    grad_scale * d(mean loss)/d(logits)."""
-    rows, vocab = logits.shape
-    tgt = target.reshape(-1).to(torch.int64).contiguous()
-    loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
-    _check(load().het_xent_fused(_cuda(logits, torch.bfloat16, "logits"), tgt.data_ptr(), rows,
-                                 vocab, float(grad_scale), loss.data_ptr(), _stream(None)),
-           "het_xent_fused")
-    return loss.mean()
-
-
 RMS_DIMS = (256, 768, 1024, 2048)
 
 
@@ -716,120 +699,6 @@ class LinearGeluFn(torch.autograd.Function):
         return dx, dw, db
 
 
-LT_NONE, LT_BIAS, LT_GELU_BIAS, LT_GELU_AUX_BIAS, LT_DGELU_BGRAD, LT_BGRADB = range(6)
-_LT_WS: dict = {}
-_LT_WS_BYTES = 32 << 20
-
-
-def _lt_workspace(device) -> torch.Tensor:
-    ws = _LT_WS.get(device)
-    if ws is None:
-        ws = _LT_WS[device] = torch.empty(_LT_WS_BYTES, dtype=torch.uint8, device=device)
-    return ws
-
-
-def lt_matmul(ta: int, tb: int, m: int, n: int, k: int, a: torch.Tensor, lda: int,
-              b: torch.Tensor, ldb: int, d: torch.Tensor, ldd: int, epilogue: int = LT_NONE,
-              bias: torch.Tensor | None = None, aux: torch.Tensor | None = None,
-              ldaux: int = 0) -> None:
-    """het_lt_matmul (cuBLASLt GEMM + fused epilogue), column-major arguments."""
-    ws = _lt_workspace(d.device)
-    _check(load().het_lt_matmul(ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
-                                d.data_ptr(), ldd, epilogue,
-                                None if bias is None else bias.data_ptr(),
-                                None if aux is None else aux.data_ptr(), ldaux, ws.data_ptr(),
-                                _LT_WS_BYTES, _stream(None)), "het_lt_matmul")
-
-
-def _rows(x: torch.Tensor) -> torch.Tensor:
-    x2 = x.reshape(-1, x.shape[-1])
-    return x2 if x2.is_contiguous() else x2.contiguous()
-
-
-def _lt_forward(x2, w, b, epilogue, aux=None):
-    """y[M, N] = x2[M, K] W[N, K]^T + b with the epilogue (row-major views)."""
-    M, K = x2.shape
-    N = w.shape[0]
-    y = torch.empty(M, N, dtype=torch.bfloat16, device=x2.device)
-    lt_matmul(1, 0, N, M, K, w, K, x2, K, y, N, epilogue, b, aux, N if aux is not None else 0)
-    return y
-
-
-def _lt_wgrad(x2, g2, with_bias: bool):
-    """dW[N, K] = g2^T x2 (+ db[N] = column sums of g2 from the same GEMM)."""
-    M, K = x2.shape
-    N = g2.shape[1]
-    dw = torch.empty(N, K, dtype=torch.bfloat16, device=x2.device)
-    db = torch.empty(N, dtype=torch.bfloat16, device=x2.device) if with_bias else None
-    lt_matmul(0, 1, K, N, M, x2, K, g2, N, dw, K, LT_BGRADB if with_bias else LT_NONE, db)
-    return dw, db
-
-
-class LtLinearFn(torch.autograd.Function):
-    """y = x W^T + b: cuBLASLt bias epilogue forward; the weight-gradient GEMM
-    also produces the bias gradient (BGRADB epilogue), so no reduction pass."""
-
-    @staticmethod
-    def forward(ctx, x, w, b):
-        x2 = _rows(x)
-        ctx.save_for_backward(x2, w)
-        ctx.shape = x.shape
-        return _lt_forward(x2, w, b, LT_BIAS).view(*x.shape[:-1], w.shape[0])
-
-    @staticmethod
-    def backward(ctx, g):
-        x2, w = ctx.saved_tensors
-        g2 = _rows(g)
-        dx = (g2 @ w).view(ctx.shape) if ctx.needs_input_grad[0] else None
-        dw, db = _lt_wgrad(x2, g2, True)
-        return dx, dw, db
-
-
-class LtMLPFn(torch.autograd.Function):
-    """out = gelu_tanh(x W1^T + b1) W2^T + b2 with every elementwise pass inside
-    the GEMMs: GELU+bias (+ the pre-activation) in the up-projection, bias in
-    the down-projection; backward: fc2's weight GEMM gives db2 (BGRADB), fc2's
-    input-gradient GEMM applies GELU' and gives db1 (DGELU_BGRAD)."""
-
-    @staticmethod
-    def forward(ctx, x, w1, b1, w2, b2):
-        x2 = _rows(x)
-        M, f = x2.shape[0], w1.shape[0]
-        pre = torch.empty(M, f, dtype=torch.bfloat16, device=x.device)
-        y = _lt_forward(x2, w1, b1, LT_GELU_AUX_BIAS, pre)
-        out = _lt_forward(y, w2, b2, LT_BIAS)
-        ctx.save_for_backward(x2, w1, w2, y, pre)
-        ctx.shape = x.shape
-        return out.view(*x.shape[:-1], w2.shape[0])
-
-    @staticmethod
-    def backward(ctx, g):
-        x2, w1, w2, y, pre = ctx.saved_tensors
-        g2 = _rows(g)
-        M, d = g2.shape
-        f = w1.shape[0]
-        dw2, db2 = _lt_wgrad(y, g2, True)
-        dpre = torch.empty(M, f, dtype=torch.bfloat16, device=g.device)
-        db1 = torch.empty(f, dtype=torch.bfloat16, device=g.device)
-        lt_matmul(0, 0, f, M, d, w2, f, g2, d, dpre, f, LT_DGELU_BGRAD, db1, pre, f)
-        dw1 = dpre.t() @ x2
-        dx = (dpre @ w1).view(ctx.shape) if ctx.needs_input_grad[0] else None
-        return dx, dw1, db1, dw2, db2
-
-
-def lt_linear(x, w, b):
-    if not torch.is_grad_enabled():
-        return _lt_forward(_rows(x), w, b, LT_BIAS).view(*x.shape[:-1], w.shape[0])
-    return LtLinearFn.apply(x, w, b)
-
-
-def lt_mlp(x, w1, b1, w2, b2):
-    if not torch.is_grad_enabled():
-        y = _lt_forward(_rows(x), w1, b1, LT_GELU_BIAS)
-        return _lt_forward(y, w2, b2, LT_BIAS).view(*x.shape[:-1], w2.shape[0])
-    return LtMLPFn.apply(x, w1, b1, w2, b2)
-
-
 def linear(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     if not torch.is_grad_enabled():
         return torch.nn.functional.linear(x, w, b)
@@ -1072,30 +941,47 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
     raise InputError(f"unknown collective {op!r}")
 
 
-def ag_symm_policy(counts: Sequence[int], nranks: int) -> int:
+RELAY_FSCALE = 1.25     # relay_plan()'s share factor past the egress balance (HET_RELAY_FSCALE)
+
+
+def relay_link_bytes(counts: Sequence[int], nranks: int, fscale: float = RELAY_FSCALE) -> float:
+    """Largest per-GPU link load (bytes in elements) of the relay all-gather as
+    relay_plan() in csrc/hetstep_symm.cu runs it: ranks sorted by count, the
+    i-th largest owner A pairs with the i-th smallest B (sB < sA); A sends a
+    share f = min(1, fscale * (sA - sB)(N-1) / (2 (N-2) sA)) of its range to B
+    only and B forwards it. Egress A = sA((N-1) - (N-2) f), egress B =
+    sB(N-1) + (N-2) f sA; every rank's ingress is S - s_i."""
+    c = sorted((int(x) for x in counts), reverse=True)
+    n = nranks
+    total = sum(c)
+    load = float(total - c[-1])                       # ingress of the smallest owner
+    for i in range(n):
+        j = n - 1 - i
+        if i < j and c[i] > c[j]:
+            f = min(1.0, fscale * (c[i] - c[j]) * (n - 1) / (2.0 * (n - 2) * c[i]))
+            load = max(load, c[i] * ((n - 1) - (n - 2) * f), c[j] * (n - 1) + (n - 2) * f * c[i])
+        elif i <= j:                                  # unpaired: plain push
+            load = max(load, (n - 1) * c[i])
+    return load
+
+
+def ag_symm_policy(counts: Sequence[int], nranks: int, multicast: bool = True) -> int:
     """Route policy for a fused all-gather: SYMM_RELAY when the relay's link
-    model beats the better of multicast and plain peer push by >10%, else
-    SYMM_AUTO. Mirrors relay_plan() in csrc/hetstep_symm.cu: the i-th largest
-    owner A pairs with the i-th smallest B, and the balanced pair egress is
-    (N-1)(sA+sB)/2; the ingress bound S - min s is unchanged. Measured at N=4,
-    1 GB (profiles/r1_final/relay_n4_c*.jsonl, relay_fscale_n4.jsonl): 2:1 616 vs
-    485 GB/s, planner 686 vs 538; geometric (model margin 7%) stays on multicast (532 vs 465)."""
+    load (relay_link_bytes, the kernel's own pairing and share) beats the
+    better of plain peer push and, when the workspace has an NVLS multicast
+    object, multicast (S bytes on every link) by >10%; else SYMM_AUTO.
+    Measured at N=4, 1 GB (profiles/r1_final/relay_n4_c*.jsonl,
+    relay_fscale_n4.jsonl): 2:1 616 vs 485 GB/s, planner 686 vs 538;
+    geometric (model margin 7%) stays on multicast (532 vs 465)."""
     if nranks < 3 or nranks > 4:   # relay measured at N=4 only; N=8 keeps AUTO until run
         return SYMM_AUTO
-    c = sorted((int(x) for x in counts), reverse=True)
-    total, mn = sum(c), c[-1]
+    c = [int(x) for x in counts]
+    total, mx, mn = sum(c), max(c), min(c)
     if total <= 0:
         return SYMM_AUTO
-    peer = max((nranks - 1) * c[0], total - mn)
-    best = min(peer, total)                 # multicast moves S on every link
-    relay = total - mn
-    for i in range(nranks):
-        j = nranks - 1 - i
-        if i < j and c[i] > c[j]:
-            relay = max(relay, (nranks - 1) * (c[i] + c[j]) / 2)
-        elif i <= j:                          # unpaired: plain push
-            relay = max(relay, (nranks - 1) * c[i])
-    return SYMM_RELAY if relay < 0.9 * best else SYMM_AUTO
+    peer = max((nranks - 1) * mx, total - mn)
+    best = min(peer, total) if multicast else peer
+    return SYMM_RELAY if relay_link_bytes(c, nranks) < 0.9 * best else SYMM_AUTO
 
 
 # ---------------------------------------------------------------------------
@@ -1229,7 +1115,7 @@ class StatusWatch:
         if self.ev[k] is not None:          # slot still pending: settle it first
             self._settle(k, block=True)
         _check(load().het_symm_status_async(self.host[k:].data_ptr(), _stream(stream)),
-               "het_symm_status_async", "het_probe_smid")
+               "het_symm_status_async")
         ev = torch.cuda.Event()
         ev.record(stream)
         self.ev[k], self.tag[k] = ev, tag

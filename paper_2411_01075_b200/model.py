@@ -89,6 +89,15 @@ class ArchSpec:
         return 4 * 2 * tokens * (dense + attn)
 
 
+    def model_flops_per_sample(self) -> float:
+        """MODEL FLOPs of one training sample (forward + backward, no recompute):
+        6 per parameter-token of every matmul weight (the blocks and the tied LM
+        head; embedding lookups are free) plus 12 * s * d per token per layer
+        for the attention score and value products (PaLM's MFU accounting)."""
+        dense = self.layers * self.unit_params + self.vocab * self.d
+        return 6.0 * self.seq * dense + 12.0 * self.layers * self.seq * self.seq * self.d
+
+
 ARCHS: dict[str, ArchSpec] = {
     "tiny_gpt": ArchSpec("tiny_gpt", "gpt", d=256, layers=4, heads=4, ffn=1024, vocab=4096,
                          seq=128),
@@ -151,14 +160,6 @@ def _rms(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6) -> torch.Tensor:
 # residual add fused into the following norm (hetstep.add_layer_norm / add_rms_norm);
 # a switch so tools/ab_step.py can A/B it on the same box
 FUSE_RESIDUAL_NORM = True
-# GPT/BERT linears through cuBLASLt epilogue GEMMs (hetstep.lt_linear / lt_mlp: bias,
-# GELU and both bias gradients inside the GEMMs) instead of torch GEMMs + fused passes
-LT_EPILOGUES = False
-# cross-entropy loss and gradient in one pass over the logits (het_xent_fused). Off:
-# measured 0.4-0.5% slower per step than the two-kernel pair (tools/ab_step.py), as
-# its register-resident rows allow one CTA per SM and the read and write phases of
-# a CTA do not overlap
-FUSE_XENT = False
 
 
 def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -> torch.Tensor:
@@ -193,8 +194,7 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     # CUDA: linears with the fused bias-gradient column sum, and the MLP
     # up-projection + GELU as one epilogue GEMM (no-grad) / fused GELU passes
     fused = x.is_cuda and x.dtype == torch.bfloat16
-    lt = fused and LT_EPILOGUES
-    lin = _K.lt_linear if lt else _K.linear if fused else F.linear
+    lin = _K.linear if fused else F.linear
     h = _ln(x, p["ln1_w"], p["ln1_b"])
     # q/k/v as views of the fused projection in (b, s, H, dh) memory order: SDPA
     # (cuDNN) keeps that layout for its output, so neither the head split nor
@@ -208,8 +208,6 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
     else:
         x = x + attn
         h = _ln(x, p["ln2_w"], p["ln2_b"])
-    if lt:
-        return x + _K.lt_mlp(h, p["fc_w"], p["fc_b"], p["fc2_w"], p["fc2_b"])
     if fused:
         h = _K.linear_gelu(h, p["fc_w"], p["fc_b"])
     else:
@@ -238,10 +236,9 @@ def head_value_and_grad(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Ten
                         grad_scale: float = 1.0):
     """Mean next-token loss of one microbatch and its gradients w.r.t. `wrt`
     (head parameters and the head input), the gradients scaled by grad_scale
-    (a row chunk of a microbatch passes its share of the rows). On CUDA the loss
-    and dlogits come from one fused pass over the logits (het_xent_fused),
-    written over the logits in place, and autograd takes it from the logits GEMM
-    down."""
+    (a row chunk of a microbatch passes its share of the rows). On CUDA the
+    cross-entropy is the fused het_xent_fwd / het_xent_bwd pair (the backward
+    writes dlogits over the logits in place)."""
     with torch.enable_grad():
         if arch.kind == "llama":
             h = (_K.rms_norm(x, p["normf"]) if x.is_cuda and x.dtype == torch.bfloat16 and
@@ -250,11 +247,6 @@ def head_value_and_grad(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Ten
             h = _ln(x, p["lnf_w"], p["lnf_b"])
         logits = h @ p["wte"].t()
         flat = logits.view(-1, logits.shape[-1])
-        if FUSE_XENT and flat.is_cuda and flat.dtype == torch.bfloat16 and \
-                flat.shape[-1] % 8 == 0 and flat.shape[-1] <= 65536:
-            loss = _K.xent_value_and_grad(flat.detach(), targets.reshape(-1), grad_scale)
-            # the matmul's backward keeps h and wte, not the logits: their buffer is free
-            return loss, torch.autograd.grad(logits, wrt, logits.detach())
         if flat.is_cuda and flat.dtype == torch.bfloat16 and flat.shape[-1] % 8 == 0:
             loss = _K.cross_entropy(flat, targets.reshape(-1))
         else:

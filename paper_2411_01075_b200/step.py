@@ -268,7 +268,8 @@ class UnevenFSDPTrainer:
         self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
         self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
         # fused AG units on skewed shards at N >= 3: relay policy (hetstep.ag_symm_policy)
-        self.ag_policy = [K.ag_symm_policy(self.L.counts[u], self.N)
+        mc = self.symm is not None and self.symm.multicast
+        self.ag_policy = [K.ag_symm_policy(self.L.counts[u], self.N, multicast=mc)
                           if self.ag_route[u] == "symm" else None for u in units]
         # a fused RS whose successor (RS order: L-1..0, root) is not fused must end with a
         # cross-rank barrier: nothing later proves that peers finished reading its acc
@@ -820,13 +821,13 @@ class UnevenFSDPTrainer:
                     ag_ev[u - 1] = self._ag(u - 1, self.ubuf[(u - 1) % 2], "bwd")
                 if u < nb - 2:
                     comp.wait_event(ag_ev[u])
-                if not self.pair_units:
-                    if u + 2 in rs_ev:              # acc[u % 2] last read by RS(u+2)
-                        comp.wait_event(rs_ev[u + 2])
-                    if self.symm is not None and u + 1 in rs_ev:
-                        # peers read acc[u % 2] remotely during RS(u+2): my RS(u+1) having
-                        # passed its start barrier proves every rank finished RS(u+2)
-                        comp.wait_event(rs_ev[u + 1])
+            # acc[u % 2] is rewritten by this unit's first accumulate: its last readers
+            # are RS(u+2) on this rank and, through the fused RS, on every peer (my
+            # RS(u+1) having passed its start barrier proves every rank finished
+            # RS(u+2)). The waits sit right before that first accumulate, so the
+            # reduce-scatters overlap this unit's recompute and backward.
+            acc_free = [rs_ev[v] for v in (u + 2, u + 1) if multi and not self.pair_units
+                        and v in rs_ev and (v == u + 2 or self.symm is not None)]
             if off and not deep:
                 if u - 1 >= 0:                    # one unit of look-ahead
                     pref[u - 1] = self._prefetch_unit(u - 1, nmb)
@@ -870,6 +871,9 @@ class UnevenFSDPTrainer:
                     else:
                         held.append(list(grads[:-1]))
                         if len(held) >= self.acc_microbatches or k == nmb - 1:
+                            for ev_ in acc_free:
+                                comp.wait_event(ev_)
+                            acc_free = []
                             self._accumulate_mb(acc, held, unit_names, self.unit_seg,
                                                 first=(k + 1 == len(held)))
                             held = []
@@ -897,12 +901,15 @@ class UnevenFSDPTrainer:
             if len(pending) < self.acc_group and u > 0:
                 continue                             # wait for the group's last unit
             if multi:
-                # both accumulators are rewritten: their previous readers are the last
-                # pair's reduce-scatters (the second one ends with a cross-rank barrier
-                # when fused; its start barrier covers the first one)
+                # the group's accumulators are rewritten: their previous readers are
+                # RS(v+2) here and on every peer. RS(v+1), when issued already, is the
+                # later one; with an odd block count the last group is unit 0 alone,
+                # and RS(2) (first of its pair, no end barrier) proves only this
+                # rank's read, so RS(1) (end barrier) must be waited on too
                 for v, _ in pending:
-                    if v + 2 in rs_ev:
-                        comp.wait_event(rs_ev[v + 2])
+                    for w_ in (v + 2, v + 1):
+                        if w_ in rs_ev:
+                            comp.wait_event(rs_ev[w_])
             if mb:
                 self._accumulate_units([p for p in pending if p[1]], unit_names, self.unit_seg)
             ev = self._event(comp)

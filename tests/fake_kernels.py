@@ -36,7 +36,7 @@ def route_collective(op, counts, nranks, symm):
     return "nccl"
 
 
-def ag_symm_policy(counts, nranks):
+def ag_symm_policy(counts, nranks, multicast=True):
     return 0
 
 

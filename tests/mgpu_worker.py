@@ -194,6 +194,32 @@ def main(out_dir: str) -> None:
             pair[wire] = [t.cpu().numpy() for t in t2.full_units("g32")]
             del t2
         report["symm_status_pair"] = float(K.SymmWorkspace.status(reset=True))
+
+        # fault injection: rank 0 enters a fused all-gather that no other rank joins
+        # (shortened spin limit). Its barrier times out; the trainer's asynchronous
+        # status check must then raise CollectiveFault on rank 0 after its next step
+        # instead of training on that step's unsynchronised buffers.
+        torch.cuda.synchronize()
+        dist.barrier()
+        K.set_symm_timeout_ms(300)
+        if rank == 0:
+            trs.symm.allgather_pack(torch.zeros(4, device=dev), "ub0", 0, [4] + [0] * (world - 1),
+                                    [0] * world)
+            torch.cuda.synchronize()
+        K.set_symm_timeout_ms(10_000)
+        if rank != 0:
+            trs.symm.epoch[0] += 1      # every rank's AG channel epoch agrees again
+        dist.barrier()
+        raised = 0
+        try:
+            trs.step(torch.from_numpy(tok).to(dev))
+            trs.check_faults()
+        except K.CollectiveFault:
+            raised = 1
+        report["fault_raised"] = float(raised == (1 if rank == 0 else 0))
+        K.SymmWorkspace.status(reset=True)
+        torch.cuda.synchronize()
+        dist.barrier()
         torch.cuda.synchronize()
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), loss=float(loss),
                  micro=np.array(micro), ratios=np.array(ratios),

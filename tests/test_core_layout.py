@@ -161,6 +161,14 @@ def test_ag_relay_policy_link_model():
     assert K.ag_symm_policy([T >> i for i in range(4)], 4) == K.SYMM_AUTO
     assert K.ag_symm_policy([T, 0, T, 0], 4) == K.SYMM_AUTO
     assert K.ag_symm_policy([0, 0, 0, 0], 4) == K.SYMM_AUTO
+    # the Python model is the kernel's pairing with its 1.25x share: 2:1 lands on
+    # the small owners' ingress bound 5S/6
+    assert K.relay_link_bytes(c, 4) == pytest.approx(5 * S / 6)
+    # without an NVLS multicast object the comparison is against plain push only:
+    # geometric and two-owner shapes then take the relay
+    assert K.ag_symm_policy([T >> i for i in range(4)], 4, multicast=False) == K.SYMM_RELAY
+    assert K.ag_symm_policy([T, 0, T, 0], 4, multicast=False) == K.SYMM_RELAY
+    assert K.ag_symm_policy([T] * 4, 4, multicast=False) == K.SYMM_AUTO
     # the relay never raises any rank's egress above the plain push maximum
     for c in ([5, 1, 1, 1], [9, 4, 2, 1], [3, 3, 1, 1, 2, 2, 1, 1], [7, 0, 0, 0]):
         eg, _ = _relay_link_bytes(c)

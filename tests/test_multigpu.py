@@ -53,6 +53,8 @@ def test_multigpu_collectives_and_step(tmp_path):
                 assert v > 0, "the l<=1 plan did not use the bf16-wire reduce-scatter"
             elif k == "symm_route_check_ok":
                 assert v == 1.0, "fused collectives failed their startup known-answer check"
+            elif k == "fault_raised":
+                assert v == 1.0, "a fused-collective timeout was not raised as CollectiveFault"
             elif k == "trace_lint_problems":
                 assert v == 0.0, "measured multi-rank trace violates the schedule's causality"
     arch = ARCHS["tiny_gpt"]

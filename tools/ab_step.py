@@ -50,10 +50,6 @@ tok = torch.from_numpy(rank_tokens(plan, 0, job.arch.seq, job.arch.vocab, 1, 0))
 def setting(on: bool) -> None:
     if args.switch == "fuse_residual_norm":
         M.FUSE_RESIDUAL_NORM = on
-    elif args.switch == "fuse_xent":
-        M.FUSE_XENT = on
-    elif args.switch == "lt_epilogues":
-        M.LT_EPILOGUES = on
     elif args.switch == "keep_last":
         tr.keep_last_graph = on
     elif args.switch == "offload":
