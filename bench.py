@@ -500,6 +500,8 @@ def main() -> None:
     B = plan.total_batch
     hbm, hbm_kind = peaks()
     bf16_peak = bf16_sustained()
+    from paper_2411_01075_b200.planner import crosscheck_measured
+    xc = crosscheck_measured(plan, ms)
     # dominant owned kernel = the one with the largest share of the timed steps
     if not kern:                              # --no-kernel-timers
         kern = {"adamw": {"launches": 0, "ms_total": 0.0, "ms_mean": 0.0, "bytes_total": 0.0,
@@ -538,6 +540,10 @@ def main() -> None:
                        "profiles": ("measured" if any(d.get("profile_key") for d in job.profile_docs)
                                     and not args.analytic_profiles else "analytic"),
                        "planner_predicted_iteration_ms": plan.predicted_iteration_ms,
+                       # the reference's crosscheck_optimizer (sim.py:445-452) against the
+                       # measured step instead of the simulator
+                       "crosscheck": {"predicted_ms": xc.predicted_ms, "measured_ms": xc.measured_ms,
+                                      "rel_error": xc.rel_error},
                        "parallelism": f"uneven-fsdp{world}",
                        "emulation_rank0": emu.describe(),
                        # sum over ranks of the emulated tiers' SM fractions (N=1: 1.0);

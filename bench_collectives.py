@@ -32,10 +32,11 @@ from paper_2411_01075_b200.configs import build_job  # noqa: E402
 
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
          "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route",
-         "symm_relay": "symm_relay",
-         "symm_bf16wire": "symm_bf16wire"}
+         "symm_relay": "symm_relay", "symm_helpers": "symm_helpers",
+         "symm_bf16wire": "symm_bf16wire", "symm_bf16wire_helpers": "symm_bf16wire_helpers"}
 SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
-        "symm_peer": (False, K.SYMM_PEER), "symm_relay": (False, K.SYMM_RELAY)}
+        "symm_peer": (False, K.SYMM_PEER), "symm_relay": (False, K.SYMM_RELAY),
+        "symm_helpers": (False, K.SYMM_HELPERS)}
 
 
 def skew_counts(skew: str, total: int, n: int) -> list[int]:
@@ -111,12 +112,13 @@ def main() -> None:
     maxel = int(max(args.sizes_mb) * (1 << 20)) // 2 + 64
     ws = {}
     for an, (mc, policy) in SYMM.items():
-        if an in args.algos or (an in ("symm", "symm_relay") and world > 2 and
+        if an in args.algos or (an == "symm_helpers" and "symm_bf16wire_helpers" in args.algos) \
+                or (an in ("symm", "symm_relay", "symm_helpers") and world > 2 and
                                 "route" in args.algos) or (an == "symm" and (
                                     "route" in args.algos or "symm_bf16wire" in args.algos)):
-            ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel // 2 + 64,
+            ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel + 64,
                                                                          torch.float32),
-                                      ("g16", maxel // 2 + 64, torch.bfloat16)],
+                                      ("g16", maxel + 64, torch.bfloat16)],
                                      dist.group.WORLD.group_name, dev, rank, world,
                                      ctas=args.ctas, use_multicast=mc, policy=policy)
             if rank == 0:
@@ -144,14 +146,18 @@ def main() -> None:
                             if (algo == "symm" and op == "allgather" and
                                     K.ag_symm_policy(c, world) == K.SYMM_RELAY):
                                 algo = "symm_relay"
-                        if algo == "symm_bf16wire":
+                        if algo in ("symm_bf16wire", "symm_bf16wire_helpers"):
                             if op != "reduce_scatter":
                                 continue
-                            w = ws["symm"]
+                            hel = algo == "symm_bf16wire_helpers"
+                            w = ws["symm_helpers" if hel else "symm"]
                             w["g16"][:total].normal_()
                             out = torch.empty(c[rank], device=dev)
                             wts = [1.0 / world] * world
-                            fn = lambda: w.reduce_scatter_bf16("g16", 0, out, c, o, wts)  # noqa: E731
+                            pol = K.SYMM_HELPERS if hel else K.SYMM_AUTO
+                            st_ = "acc" if hel else None
+                            fn = lambda: w.reduce_scatter_bf16("g16", 0, out, c, o, wts,  # noqa: E731
+                                                               policy=pol, stage=st_)
                         elif isinstance(algo, str):
                             w = ws[algo]
                             if op == "allgather":

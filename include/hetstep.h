@@ -274,6 +274,20 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
  * each big owner hands a share of its range to a small owner, which forwards
  * it, balancing link egress on skewed shard vectors (N >= 3). */
 #define HET_SYMM_RELAY 3
+/* All-gather and both reduce-scatters: heavy owners hand pieces of their range
+ * to light ranks ("helpers"). AG: the owner pushes a piece to its helper only
+ * and the helper forwards it to the other N-2 ranks. RS: the helper reduces
+ * the piece over all ranks into a staging copy in its own buffer and the owner
+ * pulls the reduced piece. Pieces stream in grid-stride iterations with
+ * CTA-pairwise progress flags, so forwarding / pulling overlaps production.
+ * A single owner then moves S (not (N-1) S) over its link; the plan
+ * (het_symm_helper_plan) balances every link's load. N >= 3. */
+#define HET_SYMM_HELPERS 4
+
+/* Ops of het_symm_helper_plan */
+#define HET_OP_AG 0
+#define HET_OP_RS 1
+#define HET_OP_RS_BF16 2
 
 /* A buffer allocated at the same byte layout on every rank (torch symmetric
  * memory is the plumbing): peer_base[j] = its address on rank j mapped into
@@ -323,7 +337,21 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
 int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* out,
                                  const int64_t* counts, const int64_t* offsets,
                                  const float* weights, uint32_t epoch, int channel,
-                                 int end_barrier, int ctas, void* stream);
+                                 int end_barrier, int policy, uint64_t stage_off, int ctas,
+                                 void* stream);
+/* policy: HET_SYMM_AUTO / HET_SYMM_PEER (peer pull) or HET_SYMM_HELPERS, whose
+ * helpers write fp32 partial results at stage_off (an fp32 unit-sized region of
+ * the symmetric buffer, 16-byte aligned; unused otherwise). The helper routes
+ * always end with the cross-rank barrier (owners have read the staging). */
+
+/* The helper plan the kernels use for `op` (HET_OP_*) on this shard table:
+ * direct body vectors per rank (out_direct[nranks]), (owner, helper) pairs of
+ * the pieces (out_pieces[2 * max_pieces]) and the per-rank link load in bytes
+ * (link_load[nranks]: AG egress, RS ingress). Host only. Returns the number
+ * of pieces, or -HET_EARG. */
+int het_symm_helper_plan(int op, int nranks, const int64_t* counts, const int64_t* offsets,
+                         uint64_t off, int64_t* out_direct, int32_t* out_pieces, int max_pieces,
+                         double* link_load);
 
 /* bf16 gradient segments copied (unscaled) into one bf16 unit buffer:
  * dst[segs[i].dst_off : +n] = segs[i].src. The l_i = 1 staging of the bf16-wire

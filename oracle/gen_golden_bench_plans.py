@@ -35,7 +35,8 @@ def main() -> None:
     sys.path.insert(0, str(ROOT))
     import hetplan as R
     import numpy as np
-    from paper_2411_01075_b200.configs import CONFIGS, cluster_doc, measured_profiles, tier_profile
+    from paper_2411_01075_b200.configs import (CONFIGS, cluster_doc, measured_profiles,
+                                               planner_model, tier_profile)
     from paper_2411_01075_b200.model import ARCHS
     meta = {"reference": "hetplan " + R.__version__, "numpy": np.__version__,
             "generated": time.strftime("%Y-%m-%d"), "script": "oracle/gen_golden_bench_plans.py"}
@@ -56,14 +57,16 @@ def main() -> None:
             inst = {"name": f"{name}@{n}",
                     "profiles": docs,
                     "cluster": cluster_doc(arch, tiers, memory_gib=dict(cfg.memory_gib)),
-                    "model": {"layers": arch.layers, "params_per_layer": arch.unit_params,
-                              "global_batch": cfg.batch_per_gpu * n},
+                    "model": planner_model(arch, cfg.batch_per_gpu * n),
                     "allow_idle": False}
             inst["dp"] = run_planner(R, inst)
             if "plan" in inst["dp"]:
+                # the flat layout shards the real units (U params), with the plan's ratios
                 sp = R.assign_unit_shards(
                     [a["state_ratio"] for a in inst["dp"]["plan"]["assignments"]],
-                    R.model_from_dict(inst["model"]))
+                    R.model_from_dict({"layers": arch.layers,
+                                       "params_per_layer": arch.unit_params,
+                                       "global_batch": cfg.batch_per_gpu * n}))
                 inst["shards"] = {"shards": [list(v) for v in sp.shards],
                                   "offsets": [list(v) for v in sp.offsets],
                                   "uneven_units": sp.uneven_units}

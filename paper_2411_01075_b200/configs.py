@@ -11,6 +11,7 @@ in the same schema. The planner consumes either unchanged.
 """
 from __future__ import annotations
 
+import dataclasses
 import json
 from dataclasses import dataclass
 from pathlib import Path
@@ -19,6 +20,7 @@ from .core import ClusterSpec, ModelSpec, TrainPlan, cluster_from_dict, model_fr
 from .model import ARCHS, ArchSpec
 from .perf import ClusterPerf, FitError, fit_perf_model
 from .planner import dp_optimize
+from .sharding import assign_unit_shards
 
 GIB = 1 << 30
 SUSTAINED_TFLOPS = 500.0      # assumed achieved bf16 rate of the model GEMMs on a full B200
@@ -133,6 +135,16 @@ def measured_profiles(name: str) -> dict[str, dict] | None:
     return {d["profile_key"]: d for d in json.loads(p.read_text())["profiles"]}
 
 
+def planner_model(arch: ArchSpec, global_batch: int) -> dict:
+    """Model JSON (core.py:344-355) the planner sees: the root unit's
+    parameters (embeddings, final norm, tied head: 31% of GPT-2 small) are
+    amortised into params_per_layer, as the reference fixtures do
+    (fixtures/model_bert_large.json), so state_bytes = 16 (L U + E)
+    (core.py:151-154) covers the whole training state the ranks hold."""
+    ppl = -(-(arch.layers * arch.unit_params + arch.root_params) // arch.layers)
+    return {"layers": arch.layers, "params_per_layer": ppl, "global_batch": global_batch}
+
+
 def build_job(name: str, n_gpus: int, global_batch: int | None = None,
               measured: bool = False) -> Job:
     """Cluster, model, fitted perf models and the planner's plan for a config.
@@ -152,8 +164,11 @@ def build_job(name: str, n_gpus: int, global_batch: int | None = None,
             docs = tuple(tier_profile(arch, t) for t in sorted(set(tiers)))
     cluster = cluster_from_dict(cluster_doc(arch, tiers, memory_gib=dict(cfg.memory_gib)))
     batch = global_batch if global_batch is not None else cfg.batch_per_gpu * n_gpus
-    model = model_from_dict({"layers": arch.layers, "params_per_layer": arch.unit_params,
-                             "global_batch": batch})
+    model = model_from_dict(planner_model(arch, batch))
     perf = perf_from_docs(docs)
     plan = dp_optimize(cluster, model, perf)
+    # the flat layout shards the real units (U params each; the root unit gets the
+    # same ratios in layout.root_shard_plan), not the amortised planning unit
+    plan = dataclasses.replace(plan, unit_shards=assign_unit_shards(
+        [a.state_ratio for a in plan.assignments], arch.model_spec(batch)))
     return Job(cfg, arch, cluster, model, perf, plan, docs)

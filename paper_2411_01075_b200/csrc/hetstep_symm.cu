@@ -28,6 +28,7 @@
 
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 
 #include "hetstep.h"
 #include "hetstep_internal.cuh"
@@ -39,6 +40,8 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kUnroll = 8;                   // independent 16-byte remote ops per thread
 constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
+// signal slot kinds: 0 start barrier, 1 end barrier, 2 pair-relay flag, 3 helper progress
+constexpr int kKinds = 4;
 // Barrier spin limit (wall clock); het_tune(HET_TUNE_SYMM_TIMEOUT_MS) overrides it
 // so a fault-injection test need not wait the full 10 s.
 uint64_t g_spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
@@ -70,7 +73,7 @@ struct Args {
 __device__ __forceinline__ uint32_t* slot(uint64_t owner_base, uint64_t signal_off, int channel,
                                           int kind, int cta, int src) {
   const uint64_t idx =
-      ((static_cast<uint64_t>(channel) * 3 + kind) * kMaxCtas + cta) * HET_MAX_RANKS + src;
+      ((static_cast<uint64_t>(channel) * kKinds + kind) * kMaxCtas + cta) * HET_MAX_RANKS + src;
   return reinterpret_cast<uint32_t*>(owner_base + signal_off + idx * 4);
 }
 
@@ -554,6 +557,322 @@ __global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restric
   if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading mine
 }
 
+
+// ---------------------------------------------------------------- helper relay
+//
+// HET_SYMM_HELPERS: a heavy owner hands pieces of its range to light ranks
+// ("helpers"), which finish the collective for those pieces:
+//   all-gather:      the owner pushes a piece to its helper only; the helper
+//                    forwards it to the other N-2 ranks.
+//   reduce-scatter:  the helper reduces the piece over all N ranks (pull) into
+//                    a staging copy in its own buffer; the owner pulls the
+//                    reduced piece instead of N-1 raw ones.
+// A single owner at N ranks thus moves S bytes over its link instead of
+// (N-1) S (plain push / pull) and every helper link carries about S as well
+// (helper_plan). Pieces are ranges of the owner's body vectors and are
+// streamed in grid-stride iterations; after iteration k of a piece the
+// producing CTA b release-stores a progress count into slot (kind 3, cta b)
+// of the consumer, whose CTA b acquires it before consuming iteration k: the
+// same vector -> CTA mapping on both sides, so only CTA b's own progress is
+// awaited (a pipelined, CTA-pairwise handoff).
+
+struct HArgs {
+  int64_t direct;                        // my body vectors [0, direct) go the plain way
+  int n_own, n_help;
+  int own_peer[HET_MAX_RANKS];           // my pieces: helper rank, body vector range
+  int64_t own_lo[HET_MAX_RANKS], own_hi[HET_MAX_RANKS];
+  int help_peer[HET_MAX_RANKS];          // pieces I help with: owner rank, range,
+  int64_t help_lo[HET_MAX_RANKS], help_hi[HET_MAX_RANKS];   // owner's count / offset
+  int64_t help_count[HET_MAX_RANKS], help_offset[HET_MAX_RANKS];
+  int gran;                              // iterations per progress signal
+  uint64_t stage_off;                    // RS: fp32 staging region (in place for fp32)
+};
+
+__device__ __forceinline__ int64_t iters_of(int64_t lo, int64_t hi, int64_t per_iter) {
+  return hi > lo ? (hi - lo + per_iter - 1) / per_iter : 0;
+}
+
+// progress value after iteration k (signalled when (k+1) % gran == 0 or k is last)
+__device__ __forceinline__ uint32_t progress(uint32_t epoch, int64_t k, int gran) {
+  return epoch * 4096u + static_cast<uint32_t>(k / gran + 1);
+}
+
+__device__ __forceinline__ void signal_progress(uint64_t owner_base, const Sym& s, int channel,
+                                                uint32_t v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(slot(owner_base, s.signal_off, channel, 3, blockIdx.x, s.rank), v);
+  }
+}
+
+__device__ __forceinline__ void await_progress(const uint64_t* peer, const Sym& s, int channel,
+                                               int src, uint32_t v) {
+  if (threadIdx.x == 0)
+    wait_epoch(slot(peer[s.rank], s.signal_off, channel, 3, blockIdx.x, src), v, s.timeout_ns);
+  __syncthreads();
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads) symm_ag_help_kernel(const float* __restrict__ src,
+                                                                const __grid_constant__ Args a,
+                                                                const __grid_constant__ HArgs h) {
+  __shared__ uint64_t peer[HET_MAX_RANKS];
+  HET_STAGE_PEERS(a, peer);
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
+  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank released its copy of the unit
+  const int nr = NR > 0 ? NR : s.nranks;
+  const uint32_t all = (nr >= 32) ? 0xffffffffu : ((1u << nr) - 1u);
+  const int me = s.rank;
+  const int64_t n = a.count;
+  const uint64_t dst0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;
+  int64_t h1, h2, nvec;
+  ag_geometry(dst0, n, &h1, &h2, &nvec);
+  const bool src_vec = ((reinterpret_cast<uintptr_t>(src + h2)) & 15) == 0;
+  const int64_t per_iter = static_cast<int64_t>(gridDim.x) * blockDim.x * kUnroll;
+  // 1) my pieces to their helpers only (interleaved, so every helper starts early)
+  int64_t kmax = 0;
+  for (int p = 0; p < h.n_own; ++p) {
+    const int64_t k = iters_of(h.own_lo[p], h.own_hi[p], per_iter);
+    kmax = k > kmax ? k : kmax;
+  }
+  for (int64_t k = 0; k < kmax; ++k) {
+    for (int p = 0; p < h.n_own; ++p) {
+      const int64_t kp = iters_of(h.own_lo[p], h.own_hi[p], per_iter);
+      if (k >= kp) continue;
+      const int64_t lo = h.own_lo[p] + k * per_iter;
+      const int64_t hi = lo + per_iter < h.own_hi[p] ? lo + per_iter : h.own_hi[p];
+      ag_push<NR>(src, h2, lo, hi, dst0, peer, nr, (1u << me) | (1u << h.own_peer[p]), src_vec);
+      if ((k + 1) % h.gran == 0 || k + 1 == kp)
+        signal_progress(peer[h.own_peer[p]], s, a.channel, progress(a.epoch, k, h.gran));
+    }
+  }
+  // 2) my direct body vectors to every rank
+  ag_push<NR>(src, h2, 0, h.direct, dst0, peer, nr, all, src_vec);
+  // 3) forward the pieces I help with (they landed in my copy of the unit)
+  kmax = 0;
+  for (int q = 0; q < h.n_help; ++q) {
+    const int64_t k = iters_of(h.help_lo[q], h.help_hi[q], per_iter);
+    kmax = k > kmax ? k : kmax;
+  }
+  for (int64_t k = 0; k < kmax; ++k) {
+    for (int q = 0; q < h.n_help; ++q) {
+      const int64_t kq = iters_of(h.help_lo[q], h.help_hi[q], per_iter);
+      if (k >= kq) continue;
+      const int owner = h.help_peer[q];
+      await_progress(peer, s, a.channel, owner, progress(a.epoch, k, h.gran));
+      const uint64_t fdst0 = a.data_off + static_cast<uint64_t>(h.help_offset[q]) * 2;
+      int64_t fh1, fh2, fnvec;
+      ag_geometry(fdst0, h.help_count[q], &fh1, &fh2, &fnvec);
+      const int64_t lo = h.help_lo[q] + k * per_iter;
+      const int64_t hi = lo + per_iter < h.help_hi[q] ? lo + per_iter : h.help_hi[q];
+      ag_forward<NR>(fh2, lo, hi, fdst0, peer, me, nr, all & ~((1u << me) | (1u << owner)));
+    }
+  }
+  // 4) edges of my range (CTA 0), straight to every rank
+  if (blockIdx.x == 0) {
+    const int64_t body_end = h2 + nvec * 8;
+    auto pair = [&](int64_t e) {
+      const uint32_t w = pack_bf16x2(src[e], src[e + 1]);
+      for (int p = 0; p < nr; ++p)
+        *reinterpret_cast<uint32_t*>(peer[p] + dst0 + static_cast<uint64_t>(e) * 2) = w;
+    };
+    auto single = [&](int64_t e) {
+      const __nv_bfloat16 v = __float2bfloat16_rn(src[e]);
+      for (int p = 0; p < nr; ++p)
+        *reinterpret_cast<__nv_bfloat16*>(peer[p] + dst0 + static_cast<uint64_t>(e) * 2) = v;
+    };
+    const int t = threadIdx.x;
+    if (t == 0 && h1 == 1) single(0);
+    for (int64_t e = h1 + 2 * t; e + 1 < h2; e += 2 * blockDim.x) pair(e);
+    if (t == 0 && (h2 - h1) % 2 == 1) single(h2 - 1);
+    for (int64_t e = body_end + 2 * t; e + 1 < n; e += 2 * blockDim.x) pair(e);
+    if (t == 0 && (n - body_end) % 2 == 1) single(n - 1);
+  }
+  cross_barrier(s, peer, a.channel, 1, a.epoch);   // every rank's stores have landed
+}
+
+// Reduce-scatter element geometry of a rank's range: 16-byte vectors of VE
+// elements (4 fp32 or 8 bf16) after a head of unaligned elements.
+template <bool BF16>
+__device__ __forceinline__ void rs_geometry(uint64_t data_off, int64_t offset, int64_t n,
+                                            int64_t* head, int64_t* nvec) {
+  constexpr int ES = BF16 ? 2 : 4, VE = 16 / ES;
+  const uint64_t src0 = data_off + static_cast<uint64_t>(offset) * ES;
+  int64_t hd = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / ES);
+  if (hd > n) hd = n;
+  *head = hd;
+  *nvec = (n - hd) / VE;
+}
+
+// One vector (VE elements at element e of the unit) reduced over all ranks in
+// rank order with explicit rounding: fp32 sum, or sum of fl(w_j * g_j).
+template <int NR, bool BF16>
+struct RsVec {
+  static constexpr int VE = BF16 ? 8 : 4;
+  float r[VE];
+  __device__ __forceinline__ void reduce(const uint64_t* peer, int nr, uint64_t byte_off,
+                                         const Weights& wt) {
+    constexpr int kMaxR = NR > 0 ? NR : HET_MAX_RANKS;
+    uint4 x[kMaxR];
+#pragma unroll
+    for (int p = 0; p < kMaxR; ++p)
+      if (p < nr && (!BF16 || wt.w[p] != 0.f))
+        x[p] = __ldcg(reinterpret_cast<const uint4*>(peer[p] + byte_off));
+#pragma unroll
+    for (int i = 0; i < VE; ++i) r[i] = 0.f;
+    bool first = true;
+#pragma unroll
+    for (int p = 0; p < kMaxR; ++p) {
+      if (p >= nr) continue;
+      if (BF16) {
+        if (wt.w[p] == 0.f) continue;
+        float f[8];
+        bf8_to_f(x[p], f);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) r[i] = __fadd_rn(r[i], __fmul_rn(wt.w[p], f[i]));
+      } else {
+        const float f[4] = {__uint_as_float(x[p].x), __uint_as_float(x[p].y),
+                            __uint_as_float(x[p].z), __uint_as_float(x[p].w)};
+#pragma unroll
+        for (int i = 0; i < VE; ++i) r[i] = first ? f[i] : __fadd_rn(r[i], f[i]);
+        first = false;
+      }
+    }
+  }
+};
+
+template <int NR, bool BF16>
+__global__ void __launch_bounds__(kThreads) symm_rs_help_kernel(float* __restrict__ out,
+                                                                const __grid_constant__ Args a,
+                                                                const __grid_constant__ HArgs h,
+                                                                const __grid_constant__ Weights wt) {
+  __shared__ uint64_t peer[HET_MAX_RANKS];
+  HET_STAGE_PEERS(a, peer);
+  const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
+  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's input is final
+  const int nr = NR > 0 ? NR : s.nranks;
+  constexpr int ES = BF16 ? 2 : 4, VE = 16 / ES;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t per_iter = gsz * kUnroll;
+  // 1) helper: reduce the owners' pieces into my staging copy, signal each iteration
+  int64_t kmax = 0;
+  for (int q = 0; q < h.n_help; ++q) {
+    const int64_t k = iters_of(h.help_lo[q], h.help_hi[q], per_iter);
+    kmax = k > kmax ? k : kmax;
+  }
+  for (int64_t k = 0; k < kmax; ++k) {
+    for (int q = 0; q < h.n_help; ++q) {
+      const int64_t kq = iters_of(h.help_lo[q], h.help_hi[q], per_iter);
+      if (k >= kq) continue;
+      int64_t head, nv;
+      rs_geometry<BF16>(a.data_off, h.help_offset[q], h.help_count[q], &head, &nv);
+      const int64_t lo = h.help_lo[q] + k * per_iter;
+      const int64_t hi = lo + per_iter < h.help_hi[q] ? lo + per_iter : h.help_hi[q];
+      for (int64_t v = lo + gtid; v < hi; v += gsz) {
+        const int64_t e = h.help_offset[q] + head + v * VE;      // unit element
+        RsVec<NR, BF16> rv;
+        rv.reduce(peer, nr, a.data_off + static_cast<uint64_t>(e) * ES, wt);
+        float4* st = reinterpret_cast<float4*>(peer[s.rank] + h.stage_off +
+                                               static_cast<uint64_t>(e) * 4);
+        __stcg(st, make_float4(rv.r[0], rv.r[1], rv.r[2], rv.r[3]));
+        if (BF16) __stcg(st + 1, make_float4(rv.r[4 % VE], rv.r[5 % VE], rv.r[6 % VE], rv.r[7 % VE]));
+      }
+      if ((k + 1) % h.gran == 0 || k + 1 == kq)
+        signal_progress(peer[h.help_peer[q]], s, a.channel, progress(a.epoch, k, h.gran));
+    }
+  }
+  // 2) my direct vectors: reduce over all ranks straight into my shard
+  const int64_t n = a.count;
+  int64_t head, nvec;
+  rs_geometry<BF16>(a.data_off, a.offset, n, &head, &nvec);
+  const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
+  auto put = [&](int64_t le, const float* r) {   // le: element of my range
+    if (out_vec) {
+      __stcs(reinterpret_cast<float4*>(out + le), make_float4(r[0], r[1], r[2], r[3]));
+      if (BF16) __stcs(reinterpret_cast<float4*>(out + le + 4),
+                       make_float4(r[4 % VE], r[5 % VE], r[6 % VE], r[7 % VE]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < VE; ++i) out[le + i] = r[i];
+    }
+  };
+  for (int64_t v = gtid; v < h.direct; v += gsz) {
+    RsVec<NR, BF16> rv;
+    rv.reduce(peer, nr, a.data_off + static_cast<uint64_t>(a.offset + head + v * VE) * ES, wt);
+    put(head + v * VE, rv.r);
+  }
+  // 3) owner: pull my pieces, reduced by their helpers, as they become ready
+  kmax = 0;
+  for (int p = 0; p < h.n_own; ++p) {
+    const int64_t k = iters_of(h.own_lo[p], h.own_hi[p], per_iter);
+    kmax = k > kmax ? k : kmax;
+  }
+  for (int64_t k = 0; k < kmax; ++k) {
+    for (int p = 0; p < h.n_own; ++p) {
+      const int64_t kp = iters_of(h.own_lo[p], h.own_hi[p], per_iter);
+      if (k >= kp) continue;
+      await_progress(peer, s, a.channel, h.own_peer[p], progress(a.epoch, k, h.gran));
+      const uint64_t base = peer[h.own_peer[p]] + h.stage_off;
+      const int64_t lo = h.own_lo[p] + k * per_iter;
+      const int64_t hi = lo + per_iter < h.own_hi[p] ? lo + per_iter : h.own_hi[p];
+      constexpr int kB = 4;                     // staged vectors in flight per thread
+      for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kB) {
+        float4 x[kB][VE / 4];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int64_t v = v0 + u * gsz;
+          if (v < hi) {
+            const float4* src4 = reinterpret_cast<const float4*>(
+                base + static_cast<uint64_t>(a.offset + head + v * VE) * 4);
+#pragma unroll
+            for (int j = 0; j < VE / 4; ++j) x[u][j] = __ldcg(src4 + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int64_t v = v0 + u * gsz;
+          if (v < hi) {
+            float r[VE];
+#pragma unroll
+            for (int j = 0; j < VE / 4; ++j) {
+              r[4 * j] = x[u][j].x; r[4 * j + 1] = x[u][j].y;
+              r[4 * j + 2] = x[u][j].z; r[4 * j + 3] = x[u][j].w;
+            }
+            put(head + v * VE, r);
+          }
+        }
+      }
+    }
+  }
+  // 4) head / tail elements of my range (CTA 0), reduced directly
+  if (blockIdx.x == 0) {
+    const int64_t body_end = head + nvec * VE;
+    auto one = [&](int64_t le) {
+      const uint64_t off = a.data_off + static_cast<uint64_t>(a.offset + le) * ES;
+      float r = 0.f;
+      bool first = true;
+      for (int p = 0; p < nr; ++p) {
+        if (BF16) {
+          if (wt.w[p] == 0.f) continue;
+          const float g = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(peer[p] + off));
+          r = __fadd_rn(r, __fmul_rn(wt.w[p], g));
+        } else {
+          const float g = *reinterpret_cast<const float*>(peer[p] + off);
+          r = first ? g : __fadd_rn(r, g);
+          first = false;
+        }
+      }
+      out[le] = r;
+    };
+    for (int64_t e = threadIdx.x; e < head; e += blockDim.x) one(e);
+    for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
+  }
+  // every owner finished pulling its helpers' staging (and every helper its inputs)
+  cross_barrier(s, peer, a.channel, 1, a.epoch);
+}
+
 // multicast kernels do not loop over ranks; peer kernels get the rank count
 // as a template constant for 2/4/8 ranks so their per-rank loops unroll
 #define HET_DISPATCH_NR(mc, n, LAUNCH) \
@@ -635,6 +954,176 @@ void relay_plan(const het_symm_t* s, const int64_t* counts, const int64_t* offse
   }
 }
 
+
+// Helper plan (HET_SYMM_HELPERS), computed identically on every rank from the
+// shard table. Link cost per element (bytes), for a rank's own range split
+// into a direct part d and helper pieces r = s - d:
+//   owner:  alpha * d + beta * r      (AG: (N-1) d + r egress;  RS fp32:
+//                                      (N-1) d + r ingress; RS bf16 wire:
+//                                      2(N-1) d + 4 r ingress)
+//   helper: alpha * s_h + gamma * a   (a = elements it relays; AG gamma = N-2
+//                                      forwards, RS gamma = (N-1) pulls x ES)
+// Binary search for the smallest per-link load T such that the heavy ranks'
+// excess fits into the light ranks' spare capacity, then fill: heavy owners in
+// count order (largest first), helpers lightest first. Pieces are in units of
+// the owner's body vectors (vnec[i] of them); the direct part takes the head.
+struct HelperPlan {
+  int npieces = 0;
+  int owner[2 * HET_MAX_RANKS], helper[2 * HET_MAX_RANKS];
+  int64_t lo[2 * HET_MAX_RANKS], hi[2 * HET_MAX_RANKS];
+  int64_t direct[HET_MAX_RANKS];
+};
+
+HelperPlan helper_plan(int n, const int64_t* counts, const int64_t* nvecs, double alpha,
+                       double beta, double gamma) {
+  HelperPlan hp;
+  for (int i = 0; i < n; ++i) hp.direct[i] = nvecs[i];
+  if (n < 3 || alpha <= beta) return hp;
+  double mx = 0;
+  for (int i = 0; i < n; ++i) mx = counts[i] > mx ? static_cast<double>(counts[i]) : mx;
+  auto excess = [&](double T, int i) {       // elements owner i must relay at load T
+    const double c = static_cast<double>(counts[i]);
+    if (alpha * c <= T) return 0.0;
+    double d = (T - beta * c) / (alpha - beta);
+    if (d < 0) d = 0;
+    return c - d;
+  };
+  auto spare = [&](double T, int j) {
+    const double c = static_cast<double>(counts[j]);
+    return alpha * c < T ? (T - alpha * c) / gamma : 0.0;
+  };
+  auto feasible = [&](double T) {
+    double need = 0, have = 0;
+    for (int i = 0; i < n; ++i) {
+      if (beta * counts[i] > T) return false;
+      need += excess(T, i);
+      have += spare(T, i);
+    }
+    return need <= have;
+  };
+  double lo = 0, hi = alpha * mx;
+  if (hi <= 0) return hp;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    (feasible(mid) ? hi : lo) = mid;
+  }
+  const double T = hi;
+  int order[HET_MAX_RANKS];
+  for (int j = 0; j < n; ++j) order[j] = j;
+  for (int i = 1; i < n; ++i)      // stable insertion sort, count descending
+    for (int j = i; j > 0 && counts[order[j]] > counts[order[j - 1]]; --j) {
+      const int t = order[j];
+      order[j] = order[j - 1];
+      order[j - 1] = t;
+    }
+  // helpers: ranks with spare capacity at T and nothing to relay, lightest first
+  int helpers[HET_MAX_RANKS], nh = 0;
+  double cap[HET_MAX_RANKS];
+  for (int oi = n - 1; oi >= 0; --oi) {
+    const int j = order[oi];
+    cap[j] = spare(T, j);
+    if (cap[j] > 0 && excess(T, j) <= 0) helpers[nh++] = j;
+  }
+  int hk = 0;
+  for (int oi = 0; oi < n; ++oi) {
+    const int i = order[oi];
+    const double ex = excess(T, i);
+    if (ex <= 0 || nvecs[i] <= 0 || hk >= nh) continue;
+    const double per_vec = static_cast<double>(counts[i]) / static_cast<double>(nvecs[i]);
+    int64_t rv = static_cast<int64_t>(ex / per_vec + 0.5);
+    if (rv > nvecs[i]) rv = nvecs[i];
+    if (rv <= 0) continue;
+    hp.direct[i] = nvecs[i] - rv;
+    int64_t pos = hp.direct[i];
+    int last = -1;
+    while (pos < nvecs[i] && hk < nh && hp.npieces < 2 * HET_MAX_RANKS) {
+      const int h = helpers[hk];
+      int64_t take = static_cast<int64_t>(cap[h] / per_vec + 0.5);
+      if (take < 1) take = 1;
+      if (take > nvecs[i] - pos || hk == nh - 1) take = nvecs[i] - pos;
+      last = hp.npieces++;
+      hp.owner[last] = i;
+      hp.helper[last] = h;
+      hp.lo[last] = pos;
+      hp.hi[last] = pos + take;
+      pos += take;
+      cap[h] -= static_cast<double>(take) * per_vec;
+      if (cap[h] <= 0.5 * per_vec) ++hk;
+    }
+    if (pos < nvecs[i]) {     // out of piece slots: the rest rides on the last piece
+      if (last >= 0) hp.hi[last] = nvecs[i];
+      else hp.direct[i] = nvecs[i];
+    }
+  }
+  return hp;
+}
+
+// Fill this rank's role tables from the plan.
+void fill_hargs(const HelperPlan& hp, int rank, const int64_t* counts, const int64_t* offsets,
+                int ctas, HArgs* h) {
+  std::memset(h, 0, sizeof(*h));
+  h->direct = hp.direct[rank];
+  int64_t kmax = 1;
+  const int64_t per_iter = static_cast<int64_t>(ctas) * kThreads * kUnroll;
+  for (int k = 0; k < hp.npieces; ++k) {
+    const int64_t it = (hp.hi[k] - hp.lo[k] + per_iter - 1) / per_iter;
+    kmax = it > kmax ? it : kmax;
+    if (hp.owner[k] == rank && h->n_own < HET_MAX_RANKS) {
+      const int j = h->n_own++;
+      h->own_peer[j] = hp.helper[k];
+      h->own_lo[j] = hp.lo[k];
+      h->own_hi[j] = hp.hi[k];
+    }
+    if (hp.helper[k] == rank && h->n_help < HET_MAX_RANKS) {
+      const int j = h->n_help++;
+      h->help_peer[j] = hp.owner[k];
+      h->help_lo[j] = hp.lo[k];
+      h->help_hi[j] = hp.hi[k];
+      h->help_count[j] = counts[hp.owner[k]];
+      h->help_offset[j] = offsets[hp.owner[k]];
+    }
+  }
+  h->gran = static_cast<int>((kmax + 3999) / 4000);
+}
+
+// Body-vector counts of every rank's range (AG: bf16 at unit_off; RS: fp32 or
+// bf16 at data_off), the geometry the kernels derive on the device.
+void body_vectors(int op, int n, const int64_t* counts, const int64_t* offsets, uint64_t off,
+                  int64_t* nvecs) {
+  for (int j = 0; j < n; ++j) {
+    if (op == HET_OP_AG) {
+      int64_t h1, h2, nv;
+      ag_geometry(off + static_cast<uint64_t>(offsets[j]) * 2, counts[j], &h1, &h2, &nv);
+      nvecs[j] = nv;
+    } else {
+      const int es = op == HET_OP_RS_BF16 ? 2 : 4;
+      const uint64_t src0 = off + static_cast<uint64_t>(offsets[j]) * es;
+      int64_t hd = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / es);
+      if (hd > counts[j]) hd = counts[j];
+      nvecs[j] = (counts[j] - hd) / (16 / es);
+    }
+  }
+}
+
+// Per-element link costs in bytes (alpha, beta, gamma) of helper_plan for an op at n ranks.
+void helper_costs(int op, int n, double* alpha, double* beta, double* gamma) {
+  if (op == HET_OP_AG) {
+    *alpha = 2.0 * (n - 1); *beta = 2; *gamma = 2.0 * (n - 2);
+  } else if (op == HET_OP_RS) {
+    *alpha = 4.0 * (n - 1); *beta = 4; *gamma = 4.0 * (n - 1);
+  } else {
+    *alpha = 2.0 * (n - 1); *beta = 4; *gamma = 2.0 * (n - 1);
+  }
+}
+
+HelperPlan plan_for(int op, int n, const int64_t* counts, const int64_t* offsets, uint64_t off) {
+  int64_t nv[HET_MAX_RANKS];
+  body_vectors(op, n, counts, offsets, off, nv);
+  double a, b, g;
+  helper_costs(op, n, &a, &b, &g);
+  return helper_plan(n, counts, nv, a, b, g);
+}
+
 int check_symm(const het_symm_t* s, const int64_t* counts, const int64_t* offsets, int ctas) {
   if (!s || s->nranks < 1 || s->nranks > HET_MAX_RANKS || s->rank < 0 || s->rank >= s->nranks)
     return fail(HET_EARG, "het_symm: bad rank table");
@@ -664,7 +1153,7 @@ int set_symm_timeout_ms(int ms) {
 extern "C" {
 
 int64_t het_symm_signal_bytes(void) {
-  return static_cast<int64_t>(HET_SYMM_CHANNELS) * 3 * kMaxCtas * HET_MAX_RANKS * 4;
+  return static_cast<int64_t>(HET_SYMM_CHANNELS) * kKinds * kMaxCtas * HET_MAX_RANKS * 4;
 }
 
 int het_symm_status(int reset) {
@@ -676,6 +1165,39 @@ int het_symm_status(int reset) {
     cudaMemcpyToSymbol(g_symm_status, &z, sizeof(int));
   }
   return v;
+}
+
+int het_symm_helper_plan(int op, int nranks, const int64_t* counts, const int64_t* offsets,
+                         uint64_t off, int64_t* out_direct, int32_t* out_pieces, int max_pieces,
+                         double* link_load) {
+  if (nranks < 1 || nranks > HET_MAX_RANKS || !counts || !offsets ||
+      (op != HET_OP_AG && op != HET_OP_RS && op != HET_OP_RS_BF16))
+    return -fail(HET_EARG, "het_symm_helper_plan: bad args");
+  const HelperPlan hp = plan_for(op, nranks, counts, offsets, off);
+  if (out_direct)
+    for (int j = 0; j < nranks; ++j) out_direct[j] = hp.direct[j];
+  if (out_pieces)
+    for (int k = 0; k < hp.npieces && k < max_pieces; ++k) {
+      out_pieces[2 * k] = hp.owner[k];
+      out_pieces[2 * k + 1] = hp.helper[k];
+    }
+  if (link_load) {       // per-rank link bytes of this plan (AG egress / RS ingress)
+    int64_t nv[HET_MAX_RANKS];
+    body_vectors(op, nranks, counts, offsets, off, nv);
+    double a, b, g;
+    helper_costs(op, nranks, &a, &b, &g);
+    for (int j = 0; j < nranks; ++j) {
+      const double per = nv[j] > 0 ? static_cast<double>(counts[j]) / nv[j] : 0.0;
+      link_load[j] = a * (counts[j] - (nv[j] - hp.direct[j]) * per);
+    }
+    for (int k = 0; k < hp.npieces; ++k) {
+      const int i = hp.owner[k], h = hp.helper[k];
+      const double el = static_cast<double>(hp.hi[k] - hp.lo[k]) * counts[i] / nv[i];
+      link_load[i] += b * el;
+      link_load[h] += g * el;
+    }
+  }
+  return hp.npieces;
 }
 
 int het_symm_status_async(int32_t* dst, void* stream) {
@@ -695,6 +1217,18 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1, -1, -1, 0, 0, 0, 0,
          g_spin_timeout_ns};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (policy == HET_SYMM_HELPERS) {
+    HArgs h;
+    fill_hargs(plan_for(HET_OP_AG, s->nranks, counts, offsets, unit_off), s->rank, counts,
+               offsets, ctas, &h);
+    switch (s->nranks) {
+      case 2: symm_ag_help_kernel<2><<<ctas, kThreads, 0, st>>>(src, a, h); break;
+      case 4: symm_ag_help_kernel<4><<<ctas, kThreads, 0, st>>>(src, a, h); break;
+      case 8: symm_ag_help_kernel<8><<<ctas, kThreads, 0, st>>>(src, a, h); break;
+      default: symm_ag_help_kernel<0><<<ctas, kThreads, 0, st>>>(src, a, h);
+    }
+    return het::check_launch("het_symm_allgather_pack");
+  }
   const bool mc = policy == HET_SYMM_RELAY ? false : pick_multicast(s, counts, policy);
   if (policy == HET_SYMM_RELAY) relay_plan(s, counts, offsets, unit_off, &a);
 #define HET_AG(MCV, NRV) symm_ag_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(src, a)
@@ -714,6 +1248,20 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
   a.timeout_ns = g_spin_timeout_ns;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (policy == HET_SYMM_HELPERS) {       // helpers reduce in place in their own acc
+    HArgs h;
+    fill_hargs(plan_for(HET_OP_RS, s->nranks, counts, offsets, acc_off), s->rank, counts,
+               offsets, ctas, &h);
+    h.stage_off = acc_off;
+    Weights wt{};
+    switch (s->nranks) {
+      case 2: symm_rs_help_kernel<2, false><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      case 4: symm_rs_help_kernel<4, false><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      case 8: symm_rs_help_kernel<8, false><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      default: symm_rs_help_kernel<0, false><<<ctas, kThreads, 0, st>>>(out, a, h, wt);
+    }
+    return het::check_launch("het_symm_reduce_scatter");
+  }
   const bool mc = pick_multicast(s, counts, policy);
 #define HET_RS(MCV, NRV) symm_rs_kernel<MCV, NRV><<<ctas, kThreads, 0, st>>>(out, a)
   HET_DISPATCH_NR(mc, s->nranks, HET_RS);
@@ -724,7 +1272,8 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
 int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* out,
                                  const int64_t* counts, const int64_t* offsets,
                                  const float* weights, uint32_t epoch, int channel,
-                                 int end_barrier, int ctas, void* stream) {
+                                 int end_barrier, int policy, uint64_t stage_off, int ctas,
+                                 void* stream) {
   int rc = check_symm(s, counts, offsets, ctas);
   if (rc != HET_OK) return rc;
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
@@ -736,6 +1285,21 @@ int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* 
   Weights wt{};
   for (int j = 0; j < s->nranks; ++j) wt.w[j] = weights[j];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (policy == HET_SYMM_HELPERS) {       // helpers stage fp32 sums at stage_off
+    if (stage_off & 15)
+      return fail(HET_EARG, "het_symm_reduce_scatter_bf16: stage offset not 16B aligned");
+    HArgs h;
+    fill_hargs(plan_for(HET_OP_RS_BF16, s->nranks, counts, offsets, grad_off), s->rank, counts,
+               offsets, ctas, &h);
+    h.stage_off = stage_off;
+    switch (s->nranks) {
+      case 2: symm_rs_help_kernel<2, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      case 4: symm_rs_help_kernel<4, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      case 8: symm_rs_help_kernel<8, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      default: symm_rs_help_kernel<0, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt);
+    }
+    return het::check_launch("het_symm_reduce_scatter_bf16");
+  }
   switch (s->nranks) {
     case 2: symm_rs_bf16_kernel<2><<<ctas, kThreads, 0, st>>>(out, a, wt); break;
     case 4: symm_rs_bf16_kernel<4><<<ctas, kThreads, 0, st>>>(out, a, wt); break;

@@ -24,7 +24,8 @@ ALGO_SYMM = 4            # fused kernels on a symmetric buffer (NVLS multicast /
 HET_MAX_RANKS = 8
 HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
-SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_RELAY = 0, 1, 2, 3
+SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_RELAY, SYMM_HELPERS = 0, 1, 2, 3, 4
+OP_AG, OP_RS, OP_RS_BF16 = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
@@ -38,7 +39,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
            "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi",
            "het_embedding_grad_dev", "het_adamw_coef", "het_adamw_devcoef",
-           "het_symm_status_async", "het_probe_smid")
+           "het_symm_status_async", "het_probe_smid", "het_symm_helper_plan")
 
 
 class HetSeg(ctypes.Structure):
@@ -119,7 +120,11 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_symm_reduce_scatter_bf16": ([ctypes.POINTER(HetSymm), ctypes.c_uint64, vp,
                                           ctypes.POINTER(i64), ctypes.POINTER(i64),
                                           ctypes.POINTER(f32), ctypes.c_uint32, i32, i32, i32,
-                                          vp], i32),
+                                          ctypes.c_uint64, i32, vp], i32),
+        "het_symm_helper_plan": ([i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                  ctypes.c_uint64, ctypes.POINTER(i64),
+                                  ctypes.POINTER(ctypes.c_int32), i32,
+                                  ctypes.POINTER(f64)], i32),
         "het_gather_bf16": ([vp, ctypes.POINTER(HetSeg), i32, vp], i32),
     }
     for name, (args, res) in sig.items():
@@ -136,6 +141,7 @@ def version() -> str:
 
 LAUNCHES = 0      # owned kernel launches issued by this process (incl. model-side kernels)
 _NOT_LAUNCHES = ("het_comm_unique_id", "het_comm_init", "het_comm_destroy", "het_tune",
+                 "het_symm_helper_plan",
                  "het_symm_status", "het_allgather_uneven", "het_reduce_scatter_uneven",  # NCCL
                  "het_adamw_coef")                                                 # host-only
 
@@ -941,6 +947,33 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
     raise InputError(f"unknown collective {op!r}")
 
 
+def helper_plan(op: int, counts: Sequence[int], offsets: Sequence[int], off: int = 0
+                ) -> dict:
+    """The HET_SYMM_HELPERS plan the kernels run for `op` (OP_AG / OP_RS /
+    OP_RS_BF16) on a shard table: direct body vectors per rank, the
+    (owner, helper) pieces and each rank's link bytes (AG egress, RS ingress)."""
+    n = len(counts)
+    direct = (ctypes.c_int64 * n)()
+    pieces = (ctypes.c_int32 * (4 * HET_MAX_RANKS))()
+    loads = (ctypes.c_double * n)()
+    k = load().het_symm_helper_plan(op, n, _i64(counts), _i64(offsets), int(off), direct, pieces,
+                                    2 * HET_MAX_RANKS, loads)
+    if k < 0:
+        raise InputError(load().het_last_error().decode())
+    return {"direct": list(direct), "pieces": [(pieces[2 * i], pieces[2 * i + 1])
+                                               for i in range(k)],
+            "link_bytes": list(loads)}
+
+
+def plain_link_bytes(op: int, counts: Sequence[int]) -> float:
+    """Largest per-rank link bytes of the plain peer route (no helpers):
+    AG push egress (N-1) max s (2 B), ingress S - min s; RS pull ingress
+    (N-1) max s (4 B fp32 / 2 B bf16 wire)."""
+    n, total = len(counts), sum(counts)
+    es = 2 if op in (OP_AG, OP_RS_BF16) else 4
+    return es * max((n - 1) * max(counts), total - min(counts))
+
+
 RELAY_FSCALE = 1.25     # relay_plan()'s share factor past the egress balance (HET_RELAY_FSCALE)
 
 
@@ -1057,30 +1090,41 @@ class SymmWorkspace:
 
     def reduce_scatter(self, region: str, elem_off: int, out: torch.Tensor,
                        counts: Sequence[int], offsets: Sequence[int], end_barrier: bool = False,
-                       stream=None) -> None:
-        """out <- sum over ranks of the fp32 accumulator at `region`[elem_off:] (my range)."""
+                       stream=None, policy: Optional[int] = None) -> None:
+        """out <- sum over ranks of the fp32 accumulator at `region`[elem_off:] (my range).
+        `policy` overrides the workspace's route policy for this call (SYMM_HELPERS:
+        helpers reduce pieces in place in their own accumulator)."""
         self.epoch[1] += 1
         o = _cuda(out, torch.float32, "out") if out.numel() else None
         byte_off = self.offsets[region] + 4 * elem_off
+        pol = self.policy if policy is None else int(policy)
+        if pol == SYMM_RELAY:          # all-gather only
+            pol = SYMM_AUTO
         _check(load().het_symm_reduce_scatter(ctypes.byref(self.desc), byte_off, o, _i64(counts),
                                               _i64(offsets), self.epoch[1], 1, int(end_barrier),
-                                              self.policy, self.ctas, _stream(stream)),
+                                              pol, self.ctas, _stream(stream)),
                "het_symm_reduce_scatter")
 
     def reduce_scatter_bf16(self, region: str, elem_off: int, out: torch.Tensor,
                             counts: Sequence[int], offsets: Sequence[int],
                             weights: Sequence[float], end_barrier: bool = False,
-                            stream=None) -> None:
+                            stream=None, policy: int = SYMM_AUTO,
+                            stage: str | None = None) -> None:
         """out <- sum_j weights[j] * bf16 gradient of rank j at `region`[elem_off:]
-        (my range), in fp32: Eq. 1 weighting and the cast inside the RS."""
+        (my range), in fp32: Eq. 1 weighting and the cast inside the RS.
+        policy=SYMM_HELPERS stages the helpers' fp32 sums in the fp32 region
+        `stage` (same element offsets)."""
         self.epoch[1] += 1
         o = _cuda(out, torch.float32, "out") if out.numel() else None
         byte_off = self.offsets[region] + 2 * elem_off
+        stage_off = self.offsets[stage] + 4 * elem_off if stage is not None else 0
+        if policy == SYMM_HELPERS and stage is None:
+            raise InputError("reduce_scatter_bf16: the helper route needs an fp32 stage region")
         w = (ctypes.c_float * len(weights))(*[float(x) for x in weights])
         _check(load().het_symm_reduce_scatter_bf16(ctypes.byref(self.desc), byte_off, o,
                                                    _i64(counts), _i64(offsets), w, self.epoch[1],
-                                                   1, int(end_barrier), self.ctas,
-                                                   _stream(stream)),
+                                                   1, int(end_barrier), int(policy), stage_off,
+                                                   self.ctas, _stream(stream)),
                "het_symm_reduce_scatter_bf16")
 
     @staticmethod

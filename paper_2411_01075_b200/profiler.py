@@ -6,8 +6,12 @@ from 1 to B, fitting linear models").
 For an emulated tier (SM fraction via a green context, configs.TIERS) and
 microbatch sizes m = 1..max_m it measures, on one GPU:
   fwd_ms[m]  one transformer unit's forward on [m, seq, d] bf16 activations
-  bwd_ms[m]  that unit's backward alone (the planner adds the checkpoint
-             recompute as recompute_multiplier * fwd, planner.py:132)
+  bwd_ms[m]  step-calibrated backward: the measured whole 1-GPU step at
+             microbatch m over L, minus the unit's forward and its
+             recompute (calibrate_bwd), so head / embedding / AdamW time is
+             in the planner's per-layer model; calibrate=False keeps the
+             unit's backward alone (the planner adds the recompute as
+             recompute_multiplier * fwd, planner.py:132)
   compute_mem_gib[m]  peak allocator bytes of a full 1-GPU train step with
              microbatch m minus the sharded training state (16 B/param +
              the 2 B bf16 shadow) — the paper's M_compute = M - M_state
@@ -101,6 +105,48 @@ def unit_latencies(arch: ArchSpec, tier: str, ms: list[int], device: torch.devic
     return fwd, bwd
 
 
+def step_latencies(arch: ArchSpec, tier: str, ms: list[int], device: torch.device,
+                   reps: int = 5) -> list[float]:
+    """Device time of one whole 1-GPU train step (eager, as multi-rank steps
+    run: embedding, every unit's forward / recompute / backward, the head,
+    accumulate, AdamW) at microbatch m, l = 1, on the tier's SM partition."""
+    from .data import rank_tokens
+    from .step import UnevenFSDPTrainer
+    stream, green = _tier_stream(tier, device)
+    out = []
+    with torch.cuda.stream(stream):
+        for m in ms:
+            model = ModelSpec(arch.layers, arch.unit_params, m)
+            plan = TrainPlan((GpuAssignment("prof", m, 1, m, 1.0, 0.0,
+                                            float(model.state_bytes)),),
+                             1.0, 1.0, 2.0 * arch.layers, False, assign_unit_shards([1.0], model))
+            tr = UnevenFSDPTrainer(arch, plan, 0, device=device)
+            tr.init_params(0)
+            tok = torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, 0, 0)).to(device)
+            out.append(_time(lambda: tr.step(tok), stream, reps))
+            del tr, tok
+    torch.cuda.synchronize(device)
+    del green
+    return out
+
+
+def calibrate_bwd(arch: ArchSpec, fwd: list[float], step: list[float],
+                  recompute_multiplier: float = 1.0) -> list[float]:
+    """Per-layer backward entries that make the planner's latency model
+    (planner.per_gpu_layer_latency, Eqs. 2-3: L * (l F + l (B + rec F)))
+    reproduce the measured whole step at l = 1:
+        B'(m) = step(m) / L - (1 + rec) F(m).
+    The head, the embedding backward, the accumulate and AdamW, which the
+    reference's per-layer model has no term for, are thereby amortised over
+    the L units exactly as the reference fixtures amortise the embedding
+    parameters into params_per_layer (fixtures/model_bert_large.json)."""
+    L = arch.layers
+    out = []
+    for f, st in zip(fwd, step):
+        out.append(max(st / L - (1.0 + recompute_multiplier) * f, 1e-3))
+    return out
+
+
 def compute_memory(arch: ArchSpec, ms: list[int], device: torch.device) -> list[float]:
     """Peak allocator bytes of one real 1-GPU step per microbatch size, minus
     the sharded state; GiB."""
@@ -130,9 +176,14 @@ def compute_memory(arch: ArchSpec, ms: list[int], device: torch.device) -> list[
 
 
 def profile_tier(arch: ArchSpec, tier: str, device: torch.device, max_m: int = 8,
-                 mem: list[float] | None = None) -> dict:
+                 mem: list[float] | None = None, calibrate: bool = True) -> dict:
+    """Profile entry of one tier. calibrate=True (the bench's profiles): the
+    backward entries are step-calibrated (calibrate_bwd) so the planner's
+    predicted iteration matches the measured whole step."""
     ms = list(range(1, max_m + 1))
     fwd, bwd = unit_latencies(arch, tier, ms, device)
+    if calibrate:
+        bwd = calibrate_bwd(arch, fwd, step_latencies(arch, tier, ms, device))
     if mem is None:
         mem = compute_memory(arch, ms, device)
     # the schema requires strictly increasing memory in m (core.py:200-203)

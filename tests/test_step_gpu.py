@@ -219,3 +219,29 @@ def test_head_row_chunks_on_gpu(cuda):
         del tr
     assert abs(out[1][0] - out[None][0]) <= 1e-5 * abs(out[None][0])
     assert float((out[1][1] - out[None][1]).norm() / out[None][1].norm()) <= 2e-2
+
+
+def test_offload_residency_contract(cuda):
+    """The reference's residency contract on a MEASURED step (sim.py ledger rules,
+    trace.boundary_residency; test_acceptance.py:157-186): with l = 4 the
+    schedule keeps l + 1 = 5 boundary items resident without offload and 2 with
+    the reference offload schedule."""
+    from paper_2411_01075_b200.trace import StepTracer, boundary_residency, lint_measured_trace
+    arch = ARCHS["gpt2_small"]
+    plan = one_gpu_plan(arch, 4, 4)
+    tok = torch.from_numpy(rank_tokens(plan, 0, arch.seq, arch.vocab, seed=5, step=0)).to(cuda)
+    peaks = {}
+    for off in (False, True):
+        tr = UnevenFSDPTrainer(arch, plan, 0, opt=OPT, device=cuda, offload_activations=off,
+                               offload_schedule="reference")
+        tr.init_params(seed=1)
+        tr.keep_last_graph = False
+        tr.step(tok)
+        tr.tracer = StepTracer("g0")
+        tr.step(tok)
+        ev = tr.tracer.collect()
+        assert lint_measured_trace(ev, arch.layers) == []
+        peaks[off] = boundary_residency(ev, arch.layers)["g0"]
+        del tr
+    assert peaks[False] == 4 + 1, peaks
+    assert peaks[True] == 2, peaks

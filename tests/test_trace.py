@@ -111,3 +111,37 @@ def test_real_step_trace_is_causal(cuda, tmp_path):
     fwd, bwd = per_layer_metrics(ev, arch.layers)
     assert fwd > 0 and bwd > 0
     trace_to_jsonl(ev, tmp_path / "step.jsonl")
+
+
+def test_boundary_residency_ledger_rules():
+    """trace.boundary_residency follows the reference ledger (sim.py:226-322):
+    a unit-major schedule of L units x l microbatches holds l + 1 boundary
+    items without offload; with the simulator's offload hand-off (prefetch
+    lands as the previous offload drains) it holds 2."""
+    from paper_2411_01075_b200.trace import TraceEvent, boundary_residency
+    L, l = 3, 4
+    ev, t = [], 0.0
+    for u in range(1, L + 1):
+        for j in range(1, l + 1):
+            ev.append(TraceEvent("g", "fwd_compute", u, j, "fwd", t, t + 1.0))
+            t += 1.0
+    for u in range(L, 0, -1):
+        for j in range(1, l + 1):
+            ev.append(TraceEvent("g", "recompute", u, j, "bwd", t, t + 1.0))
+            ev.append(TraceEvent("g", "bwd_compute", u, j, "bwd", t + 1.0, t + 3.0))
+            t += 3.0
+    assert boundary_residency(ev, L)["g"] == l + 1
+    # offload: every forward/backward item prefetched during the previous compute,
+    # outputs drained during the next one (transfer time = compute time / 2)
+    off = [e for e in ev]
+    for e in ev:
+        if e.kind == "fwd_compute":
+            off.append(TraceEvent("g", "offload_act", e.unit, e.microbatch, "fwd", e.end_ms,
+                                  e.end_ms + 0.5))
+            if e.unit > 1:
+                off.append(TraceEvent("g", "prefetch_act", e.unit, e.microbatch, "fwd",
+                                      e.start_ms - 0.5, e.start_ms))
+        if e.kind == "bwd_compute" and e.unit > 1:
+            off.append(TraceEvent("g", "prefetch_act", e.unit, e.microbatch, "bwd",
+                                  e.start_ms - 1.5, e.start_ms - 1.0))
+    assert boundary_residency(off, L)["g"] == 2

@@ -14,6 +14,10 @@ against the oracle, on:
     planner's gpt2_small / bert_large / llama_1b3 bench plans at N = 8
     (reference sharding.py:89-95 offsets, gradcheck.py:30-46 weights).
 
+Every route runs: AUTO / PEER (plain push / pull), RELAY (pair relay
+all-gather) and HELPERS (light ranks relay or reduce pieces of the heavy
+owners' ranges, hetstep_symm.cu helper_plan) for all three collectives.
+
 Bars: all-gather bit-exact vs oracle.allgather of the packed ranges; fp32
 reduce-scatter bit-exact vs the rank-ordered fp32 sum (the peer route's
 order) and within 1e-5 of oracle.reduce_scatter (fp64 sum); bf16-wire
@@ -88,13 +92,13 @@ def check_allgather(vg: VirtualGroup, counts, offs, policy, shift, seed):
             f"AG n={n} policy={policy} shift={shift} rank {r} counts={counts}"
 
 
-def check_reduce_scatter(vg: VirtualGroup, counts, offs, shift, seed):
+def check_reduce_scatter(vg: VirtualGroup, counts, offs, shift, seed, policy=K.SYMM_AUTO):
     n, total, dev = vg.n, sum(counts), vg.device
     srcs = _rank_srcs(total, n, seed)
     for r in range(n):
         vg.view(r, "acc")[4 * shift:4 * shift + total].copy_(torch.from_numpy(srcs[r]))
     outs = [torch.full((counts[r],), float("nan"), device=dev) for r in range(n)]
-    vg.reduce_scatter("acc", 4 * shift, outs, counts, offs)
+    vg.reduce_scatter("acc", 4 * shift, outs, counts, offs, policy=policy)
     ordered = srcs[0].copy()
     for r in range(1, n):
         ordered = ordered + srcs[r]          # fp32, rank order (the peer route)
@@ -103,23 +107,25 @@ def check_reduce_scatter(vg: VirtualGroup, counts, offs, shift, seed):
         got = outs[r].cpu().numpy()
         lo = offs[r]
         assert np.array_equal(got, ordered[lo:lo + counts[r]]), \
-            f"RS n={n} shift={shift} rank {r} not the rank-ordered fp32 sum"
+            f"RS n={n} shift={shift} policy={policy} rank {r} not the rank-ordered fp32 sum"
         if counts[r]:
             assert max_rel(got, want[r]) <= FP32_RTOL
 
 
-def check_reduce_scatter_bf16(vg: VirtualGroup, counts, offs, shift, seed, weights):
+def check_reduce_scatter_bf16(vg: VirtualGroup, counts, offs, shift, seed, weights,
+                              policy=K.SYMM_AUTO):
     n, total, dev = vg.n, sum(counts), vg.device
     bits = [O.pack(s) for s in _rank_srcs(total, n, seed)]
     for r in range(n):
         vg.view(r, "g16")[8 * shift:8 * shift + total].copy_(
             torch.from_numpy(bits[r].view(np.int16)).view(torch.bfloat16))
     outs = [torch.full((counts[r],), float("nan"), device=dev) for r in range(n)]
-    vg.reduce_scatter_bf16("g16", 8 * shift, outs, counts, offs, weights)
+    vg.reduce_scatter_bf16("g16", 8 * shift, outs, counts, offs, weights, policy=policy,
+                           stage="acc" if policy == K.SYMM_HELPERS else None)
     want = O.reduce_scatter_bf16(bits, weights, counts, offs)
     for r in range(n):
         assert np.array_equal(outs[r].cpu().numpy(), want[r]), \
-            f"bf16-wire RS n={n} shift={shift} rank {r} counts={counts}"
+            f"bf16-wire RS n={n} shift={shift} policy={policy} rank {r} counts={counts}"
 
 
 def _weights(n: int) -> list[float]:
@@ -146,10 +152,11 @@ def test_virtual_ranks_shard_cases(cuda, n):
     for ci, counts in enumerate(cases):
         offs = _offsets(counts)
         for shift in (0, 3):
-            for policy in (K.SYMM_AUTO, K.SYMM_PEER, K.SYMM_RELAY):
+            for policy in (K.SYMM_AUTO, K.SYMM_PEER, K.SYMM_RELAY, K.SYMM_HELPERS):
                 check_allgather(vg, counts, offs, policy, shift, seed=ci)
-            check_reduce_scatter(vg, counts, offs, shift, seed=100 + ci)
-            check_reduce_scatter_bf16(vg, counts, offs, shift, 200 + ci, _weights(n))
+            for policy in (K.SYMM_AUTO, K.SYMM_HELPERS):
+                check_reduce_scatter(vg, counts, offs, shift, 100 + ci, policy)
+                check_reduce_scatter_bf16(vg, counts, offs, shift, 200 + ci, _weights(n), policy)
 
 
 @pytest.mark.parametrize("name", ["gpt2_small", "bert_large", "llama_1b3"])
@@ -159,12 +166,13 @@ def test_virtual_ranks_planner_shapes_n8(cuda, name):
     maxu = max(sum(c) for c, _ in shapes) + 64
     vg = VirtualGroup(n, [("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32),
                           ("g16", maxu, torch.bfloat16)], cuda)
-    policies = {K.SYMM_AUTO, K.SYMM_RELAY, K.ag_symm_policy(shapes[0][0], n)}
+    policies = {K.SYMM_AUTO, K.SYMM_RELAY, K.SYMM_HELPERS, K.ag_symm_policy(shapes[0][0], n)}
     for si, (counts, offs) in enumerate(shapes):
         for policy in sorted(policies):
             check_allgather(vg, counts, offs, policy, 0, seed=si)
-        check_reduce_scatter(vg, counts, offs, 0, seed=300 + si)
-        check_reduce_scatter_bf16(vg, counts, offs, 0, 400 + si, _weights(n))
+        for policy in (K.SYMM_AUTO, K.SYMM_HELPERS):
+            check_reduce_scatter(vg, counts, offs, 0, 300 + si, policy)
+            check_reduce_scatter_bf16(vg, counts, offs, 0, 400 + si, _weights(n), policy)
 
 
 def test_missing_rank_times_out_and_is_reported(cuda):

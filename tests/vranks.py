@@ -109,16 +109,19 @@ class VirtualGroup:
 
     def reduce_scatter_bf16(self, region: str, elem_off: int, outs: Sequence[torch.Tensor],
                             counts: Sequence[int], offsets: Sequence[int],
-                            weights: Sequence[float], end_barrier: bool = True) -> None:
+                            weights: Sequence[float], end_barrier: bool = True,
+                            policy: int = K.SYMM_AUTO, stage: str | None = None) -> None:
         self.epoch[1] += 1
         lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
         byte_off = self.offsets[region] + 2 * elem_off
+        stage_off = self.offsets[stage] + 4 * elem_off if stage is not None else 0
         w = (ctypes.c_float * len(weights))(*[float(x) for x in weights])
 
         def go(r, st):
             out = outs[r].data_ptr() if outs[r].numel() else None
             K._check(lib.het_symm_reduce_scatter_bf16(ctypes.byref(self.desc[r]), byte_off, out,
                                                       c, o, w, self.epoch[1], 1,
-                                                      int(end_barrier), self.ctas, st),
+                                                      int(end_barrier), policy, stage_off,
+                                                      self.ctas, st),
                      "het_symm_reduce_scatter_bf16")
         self._launch(go, range(self.n))
