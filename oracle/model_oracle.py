@@ -50,7 +50,7 @@ def _attention(q, k, v, causal):
     s = q.shape[-2]
     att = (q @ k.transpose(-1, -2)) / math.sqrt(q.shape[-1])
     if causal:
-        mask = torch.ones(s, s, dtype=torch.bool).triu(1)
+        mask = torch.ones(s, s, dtype=torch.bool, device=q.device).triu(1)
         att = att.masked_fill(mask, float("-inf"))
     return att.softmax(-1) @ v
 
@@ -58,9 +58,9 @@ def _attention(q, k, v, causal):
 def _rotary(x):
     s, dh = x.shape[-2], x.shape[-1]
     half = dh // 2
-    freq = 1.0 / (10000.0 ** (torch.arange(half, dtype=torch.float32) / half))
-    ang = torch.arange(s, dtype=torch.float32)[:, None] * freq[None, :]
-    c, sn = torch.cos(ang), torch.sin(ang)
+    freq = 1.0 / (10000.0 ** (torch.arange(half, dtype=torch.float32, device=x.device) / half))
+    ang = torch.arange(s, dtype=torch.float32, device=x.device)[:, None] * freq[None, :]
+    c, sn = torch.cos(ang).to(x.dtype), torch.sin(ang).to(x.dtype)
     a, b = x[..., :half], x[..., half:]
     return torch.cat([a * c - b * sn, a * sn + b * c], -1)
 
@@ -111,10 +111,11 @@ def weighted_gradient(arch, units: Sequence[torch.Tensor], root: torch.Tensor,
     B = sum(m * l for m, l in micro)
     params = [u.detach().clone().requires_grad_(True) for u in units]
     rootp = root.detach().clone().requires_grad_(True)
-    total = torch.zeros(())
+    total = torch.zeros((), device=rootp.device)
     for tok, (m, l) in zip(rank_tokens, micro):
         for k in range(l):
-            lk = microbatch_loss(arch, params, rootp, torch.from_numpy(tok[k * m:(k + 1) * m]))
+            lk = microbatch_loss(arch, params, rootp,
+                                 torch.from_numpy(tok[k * m:(k + 1) * m]).to(rootp.device))
             total = total + lk * (m / B)
     total.backward()
     return [p.grad for p in params], rootp.grad, float(total.detach())

@@ -106,7 +106,7 @@ def unit_latencies(arch: ArchSpec, tier: str, ms: list[int], device: torch.devic
 
 
 def step_latencies(arch: ArchSpec, tier: str, ms: list[int], device: torch.device,
-                   reps: int = 5) -> list[float]:
+                   reps: int = 3) -> list[float]:
     """Device time of one whole 1-GPU train step (eager, as multi-rank steps
     run: embedding, every unit's forward / recompute / backward, the head,
     accumulate, AdamW) at microbatch m, l = 1, on the tier's SM partition."""

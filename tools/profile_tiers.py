@@ -22,20 +22,30 @@ from paper_2411_01075_b200.profiler import compute_memory, profile_tier  # noqa:
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", nargs="*", default=sorted(CONFIGS))
-ap.add_argument("--max-m", type=int, default=16)
+ap.add_argument("--max-m", type=int, default=0,
+                help="profile m = 1..max_m (0: per config, past the largest microbatch the "
+                     "bench plans use at N = 1..8)")
+ap.add_argument("--out-dir", default=os.path.join(ROOT, "paper_2411_01075_b200", "profiles_b200"))
+ap.add_argument("--no-calibrate", action="store_true",
+                help="per-unit backward only (no whole-step calibration)")
 a = ap.parse_args()
+MAX_M = {"tiny_gpt": 8, "gpt2_small": 96, "bert_large": 80, "llama_1b3": 32}
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
 for name in a.configs:
     cfg = CONFIGS[name]
     arch = ARCHS[cfg.arch]
     t0 = time.time()
-    mem = compute_memory(arch, list(range(1, a.max_m + 1)), dev)
-    docs = [profile_tier(arch, tier, dev, a.max_m, mem=list(mem)) for tier in sorted(set(cfg.tiers))]
-    out = os.path.join(ROOT, "paper_2411_01075_b200", "profiles_b200", f"{name}.json")
+    max_m = a.max_m or MAX_M.get(name, 16)
+    mem = compute_memory(arch, list(range(1, max_m + 1)), dev)
+    docs = [profile_tier(arch, tier, dev, max_m, mem=list(mem), calibrate=not a.no_calibrate)
+            for tier in sorted(set(cfg.tiers))]
+    os.makedirs(a.out_dir, exist_ok=True)
+    out = os.path.join(a.out_dir, f"{name}.json")
     with open(out, "w") as fh:
         json.dump({"meta": {"gpu": torch.cuda.get_device_name(dev), "torch": torch.__version__,
-                            "seconds": time.time() - t0, "tool": "tools/profile_tiers.py"},
+                            "seconds": time.time() - t0, "tool": "tools/profile_tiers.py",
+                            "calibrated": not a.no_calibrate},
                    "profiles": docs}, fh, indent=1)
     print(name, f"{time.time() - t0:.1f}s", [(d["profile_key"], d["fwd_ms"][0][1], d["fwd_ms"][-1][1],
                                               d["compute_mem_gib"][-1][1]) for d in docs], flush=True)
