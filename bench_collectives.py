@@ -143,9 +143,11 @@ def main() -> None:
                             pick = K.route_collective("ag" if op == "allgather" else "rs", c,
                                                       world, "symm" in ws)
                             algo = "symm" if pick == "symm" else K.ALGO_AUTO
-                            if (algo == "symm" and op == "allgather" and
-                                    K.ag_symm_policy(c, world) == K.SYMM_RELAY):
-                                algo = "symm_relay"
+                            if algo == "symm":
+                                pol = K.symm_policy("ag" if op == "allgather" else "rs", c,
+                                                    world, multicast=ws["symm"].multicast)
+                                algo = {K.SYMM_RELAY: "symm_relay",
+                                        K.SYMM_HELPERS: "symm_helpers"}.get(pol, "symm")
                         if algo in ("symm_bf16wire", "symm_bf16wire_helpers"):
                             if op != "reduce_scatter":
                                 continue

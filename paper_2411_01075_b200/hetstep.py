@@ -923,10 +923,78 @@ def reduce_scatter_uneven(src: torch.Tensor, shard: torch.Tensor, counts: Sequen
 # ---------------------------------------------------------------------------
 # route table
 
+# HET_SYMM_HELPERS routes for skewed units at N >= 3 (off: HET_HELPERS=0, which
+# restores the round-1 table: NCCL for near-single-owner units at N >= 4)
+import os as _os
+HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "1") != "0"
+# NVLS multicast stores / ld_reduce reach a smaller share of the link than peer
+# stores / loads: single-owner AG at N=4, 1 GB, round 1: multicast 554 GB/s against
+# 660-700 for the peer-class routes (profiles/r1_collectives_n4*.jsonl)
+MC_EFF = 0.83
+
+
+def symm_link_bytes(op: str, counts: Sequence[int], nranks: int, policy: int,
+                    multicast: bool = False) -> float:
+    """Largest per-GPU link bytes (ingress or egress) of one fused collective
+    under `policy`: "ag" (bf16), "rs" (fp32 accumulators) or "rs16" (bf16 wire).
+    The model the route choice uses; measured against it in
+    profiles/r2_collectives_*.jsonl."""
+    c = [int(x) for x in counts]
+    n, total, mx, mn = nranks, sum(c), max(c), min(c)
+    if op == "ag":
+        ingress = 2 * (total - mn)
+        if policy == SYMM_MULTICAST:
+            return 2.0 * total / MC_EFF
+        if policy == SYMM_RELAY:
+            return 2.0 * relay_link_bytes(c, n)
+        if policy == SYMM_HELPERS:
+            return max(max(helper_plan(OP_AG, c, _prefix(c))["link_bytes"]), ingress)
+        return float(max(2 * (n - 1) * mx, ingress))
+    es = 4 if op == "rs" else 2
+    egress = es * (total - mn)            # every rank's inputs read by the others
+    if policy == SYMM_MULTICAST and op == "rs":
+        return 4.0 * total / MC_EFF
+    if policy == SYMM_HELPERS:
+        plan = helper_plan(OP_RS if op == "rs" else OP_RS_BF16, c, _prefix(c))
+        return max(max(plan["link_bytes"]), egress)
+    return float(max(es * (n - 1) * mx, egress))
+
+
+def _prefix(c: Sequence[int]) -> list[int]:
+    out, pos = [], 0
+    for x in c:
+        out.append(pos)
+        pos += x
+    return out
+
+
+def symm_policy(op: str, counts: Sequence[int], nranks: int, multicast: bool = False) -> int:
+    """Policy of a fused collective: the one with the smallest largest-link load
+    (symm_link_bytes) among plain AUTO (peer push / pull, or multicast when the
+    workspace has it), RELAY (all-gather) and HELPERS; a non-AUTO policy must
+    win by > 10%. Relay: measured at N = 4 only (N = 3..4)."""
+    c = [int(x) for x in counts]
+    if sum(c) <= 0:
+        return SYMM_AUTO
+    auto = symm_link_bytes(op, c, nranks, SYMM_AUTO)
+    if multicast and op != "rs16":
+        auto = min(auto, symm_link_bytes(op, c, nranks, SYMM_MULTICAST))
+    best, pol = auto, SYMM_AUTO
+    if op == "ag" and ag_symm_policy(c, nranks, multicast) == SYMM_RELAY:
+        best, pol = min(best, 0.9 * auto), SYMM_RELAY
+    if HELPERS_ROUTE and nranks >= 3:
+        hb = symm_link_bytes(op, c, nranks, SYMM_HELPERS)
+        if hb < 0.9 * best and hb < 0.9 * auto:
+            best, pol = hb, SYMM_HELPERS
+    return pol
+
+
 def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) -> str:
     """'symm' (fused kernels on the symmetric workspace) or 'nccl' for one
-    unit's all-gather ("ag", bf16) / reduce-scatter ("rs", fp32), from the
-    measured sweeps (profiles/r1_collectives_n2.jsonl, r1_collectives_n4*.jsonl):
+    unit's all-gather ("ag", bf16) / reduce-scatter ("rs", fp32). With the
+    helper routes (HELPERS_ROUTE) every unit at N >= 3 is fused and
+    symm_policy picks the kernel route. Without them, the round-1 table from
+    the measured sweeps (profiles/r1_collectives_n2.jsonl, r1_collectives_n4*.jsonl):
       * AG: the fused kernel wins every shape except near-single-owner units at
         N >= 4, where NCCL's pipelined ring broadcast keeps the owner's link
         busier than the NVLS multicast store does;
@@ -938,6 +1006,10 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
         return "nccl"
     total, mx, mn = sum(counts), max(counts), min(counts)
     owner_like = nranks >= 4 and mx >= 0.75 * total
+    if HELPERS_ROUTE and nranks >= 3 and total > 0:
+        # the helper routes move S (not (N-1) S) over the owner's link: fused for
+        # every shape (the reduce-scatter of very large skewed units included)
+        return "symm"
     if op == "ag":
         return "nccl" if owner_like else "symm"
     if op == "rs":

@@ -110,17 +110,21 @@ class _NoStream:
         pass
 
 
-def _sum_ranks(value: int, dev: torch.device) -> int:
-    """Sum of an integer over the default process group (CPU tensor under gloo)."""
-    import torch.distributed as dist
-    on_cpu = dist.get_backend() == "gloo"
-    t = torch.tensor([int(value)], dtype=torch.int32, device="cpu" if on_cpu else dev)
-    dist.all_reduce(t)
-    return int(t.item())
+class DistGroup:
+    """Host-side agreement between the ranks of one step (torch.distributed
+    default group: plumbing). A test may pass any object with the same
+    `sum_ranks` to drive several ranks from one process (tests/vranks.py)."""
 
+    def __init__(self, dev: torch.device):
+        self.dev = dev
 
-def _any_rank(flag: bool, dev: torch.device) -> bool:
-    return _sum_ranks(int(flag), dev) > 0
+    def sum_ranks(self, value: int) -> int:
+        """Sum of an integer over the default process group (CPU tensor under gloo)."""
+        import torch.distributed as dist
+        on_cpu = dist.get_backend() == "gloo"
+        t = torch.tensor([int(value)], dtype=torch.int32, device="cpu" if on_cpu else self.dev)
+        dist.all_reduce(t)
+        return int(t.item())
 
 
 class UnevenFSDPTrainer:
@@ -132,7 +136,10 @@ class UnevenFSDPTrainer:
                  algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64,
                  offload_activations: bool = False, offload_schedule: str = "reference",
                  check_routes: bool = True,
-                 bf16_wire: bool = True):
+                 bf16_wire: bool = True, group=None, symm_workspace=None):
+        """group: host-side rank agreement (default DistGroup over torch.distributed);
+        symm_workspace: a pre-built symmetric workspace with this trainer's regions
+        (default: allocated through torch symmetric memory when algo = ALGO_SYMM)."""
         if plan.unit_shards is None or plan.unit_shards.units != arch.layers:
             raise InputError("plan unit_shards must have one row per transformer block")
         self.arch, self.plan, self.rank, self.opt, self.algo = arch, plan, rank, opt, algo
@@ -142,8 +149,10 @@ class UnevenFSDPTrainer:
             K.load()
         self.L = RankLayout.from_plan(plan, arch.unit_params, arch.root_params, rank)
         self.N = self.L.nranks
-        if self.N > 1 and (comm_ag is None or comm_rs is None):
+        if self.N > 1 and (comm_ag is None or comm_rs is None) and symm_workspace is None:
             raise InputError("multi-rank plan needs the AG and RS communicators")
+        self._group = group if group is not None else (DistGroup(self.device)
+                                                      if self.N > 1 else None)
         self.comm_ag, self.comm_rs = comm_ag, comm_rs
         a = plan.assignments[rank]
         self.m, self.l = a.microbatch, a.num_microbatches
@@ -158,23 +167,21 @@ class UnevenFSDPTrainer:
         U, E = arch.unit_params, arch.root_params
         self.symm = None
         self.symm_error = None
-        if self.N > 1 and algo == K.ALGO_SYMM:
+        if self.N > 1 and symm_workspace is not None:
+            self.symm = symm_workspace
+        elif self.N > 1 and algo == K.ALGO_SYMM:
             # fused NVLS collectives: unit buffers and accumulators live in one
             # symmetric allocation; the AG reads the fp32 master directly
             import torch.distributed as dist
             gname = group_name or dist.group.WORLD.group_name
             err = None
             try:
-                self.symm = K.SymmWorkspace(
-                    [("ub0", U, torch.bfloat16), ("ub1", U, torch.bfloat16),
-                     ("rbuf", E, torch.bfloat16), ("acc0", U, torch.float32),
-                     ("acc1", U, torch.float32), ("racc", E, torch.float32),
-                     ("gb0", U, torch.bfloat16), ("gb1", U, torch.bfloat16)],
-                    gname, dev, rank, self.N, ctas=symm_ctas)
+                self.symm = K.SymmWorkspace(self.symm_regions(arch), gname, dev, rank, self.N,
+                                            ctas=symm_ctas)
             except Exception as e:            # e.g. no peer mapping on this fabric
                 err = f"{type(e).__name__}: {e}"
             # every rank drops the fused route if any rank could not build the workspace
-            if _any_rank(err is not None, dev):
+            if self._group.sum_ranks(int(err is not None)) > 0:
                 self.symm = None
                 self.symm_error = err or "another rank failed to build the symmetric workspace"
         if self.symm is not None:
@@ -262,15 +269,26 @@ class UnevenFSDPTrainer:
             self._pf_free: list[torch.cuda.Event | None] = [None, None]
             self._last_d2h: torch.cuda.Event | None = None   # most recent offload
 
+    @staticmethod
+    def symm_regions(arch: ArchSpec) -> list[tuple[str, int, torch.dtype]]:
+        """Regions of the symmetric workspace: double-buffered gathered bf16 units,
+        the gathered root, fp32 unit / root accumulators, bf16-wire gradients."""
+        U, E = arch.unit_params, arch.root_params
+        return [("ub0", U, torch.bfloat16), ("ub1", U, torch.bfloat16),
+                ("rbuf", E, torch.bfloat16), ("acc0", U, torch.float32),
+                ("acc1", U, torch.float32), ("racc", E, torch.float32),
+                ("gb0", U, torch.bfloat16), ("gb1", U, torch.bfloat16)]
+
     # ------------------------------------------------------------------ routes
     def _set_routes(self, sym: bool) -> None:
         """Per-unit collective routes (fused symmetric kernels vs NCCL ring), fixed by shape."""
         units = range(self.L.blocks + 1)
         self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
         self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
-        # fused AG units on skewed shards at N >= 3: relay policy (hetstep.ag_symm_policy)
+        # fused-route kernel policy per unit (hetstep.symm_policy): plain / multicast,
+        # pair relay (AG) or helpers (skewed and single-owner units at N >= 3)
         mc = self.symm is not None and self.symm.multicast
-        self.ag_policy = [K.ag_symm_policy(self.L.counts[u], self.N, multicast=mc)
+        self.ag_policy = [K.symm_policy("ag", self.L.counts[u], self.N, multicast=mc)
                           if self.ag_route[u] == "symm" else None for u in units]
         # a fused RS whose successor (RS order: L-1..0, root) is not fused must end with a
         # cross-rank barrier: nothing later proves that peers finished reading its acc
@@ -284,6 +302,13 @@ class UnevenFSDPTrainer:
         # cast (het_symm_reduce_scatter_bf16), half the link bytes of the fp32 form
         self.wire16 = [sym and self.bf16_wire and self.pair_units and u < self.L.blocks and
                        self.rs_route[u] == "symm" for u in units]
+        self.rs_policy = [K.symm_policy("rs16" if self.wire16[u] else "rs", self.L.counts[u],
+                                        self.N, multicast=mc)
+                          if self.rs_route[u] == "symm" else None for u in units]
+        # the helper reduce-scatter ends with the cross-rank barrier in-kernel
+        for u in units:
+            if self.rs_policy[u] == K.SYMM_HELPERS:
+                self.rs_end[u] = True
         if self.pair_units:
             for u in range(self.L.blocks):
                 second = (self.L.blocks - 1 - u) % 2 == 1 or u == 0
@@ -329,8 +354,11 @@ class UnevenFSDPTrainer:
                 out = torch.full((cnt,), float("nan"), device=dev)
                 torch.cuda.synchronize(dev)
                 self.symm.handle.barrier()
+                hel = self.rs_policy[u] == K.SYMM_HELPERS
                 self.symm.reduce_scatter_bf16("gb0", 0, out, counts, offsets, self.rank_weights,
-                                              end_barrier=True, stream=self._current())
+                                              end_barrier=True, stream=self._current(),
+                                              policy=self.rs_policy[u],
+                                              stage="acc0" if hel else None)
                 idx = torch.arange(lo, lo + cnt, device=dev)
                 want = torch.zeros(cnt, device=dev)
                 for r, w in enumerate(self.rank_weights):
@@ -345,15 +373,16 @@ class UnevenFSDPTrainer:
                 out = torch.full((cnt,), float("nan"), device=dev)
                 torch.cuda.synchronize(dev)
                 self.symm.handle.barrier()
+                pol = K.symm_policy("rs", counts, self.N, self.symm.multicast)
                 self.symm.reduce_scatter(acc, 0, out, counts, offsets, end_barrier=True,
-                                         stream=self._current())
+                                         stream=self._current(), policy=pol)
                 idx = torch.arange(lo, lo + cnt, device=dev)
                 want = sum(pattern(idx, r) for r in range(self.N))
                 bad += int(not torch.equal(out, want))
                 checked += 1
         torch.cuda.synchronize(dev)
         status = K.SymmWorkspace.status(reset=True)
-        failures = _sum_ranks(bad + (1 if status else 0), dev)
+        failures = self._group.sum_ranks(bad + (1 if status else 0))
         self.symm.handle.barrier()
         for name in ("ub0", "acc0", "rbuf", "racc", "gb0"):
             self.symm[name].zero_()
@@ -521,14 +550,19 @@ class UnevenFSDPTrainer:
 
     def _rs_issue(self, u: int, src: torch.Tensor) -> None:
         if self.wire16[u]:               # bf16 wire: weighting + cast inside the RS
+            # helpers stage their fp32 sums in the unit's (unused) fp32 accumulator
+            hel = self.rs_policy[u] == K.SYMM_HELPERS
             self.symm.reduce_scatter_bf16(f"gb{u % 2}", 0, self._local(self.g32, u),
                                           self.L.counts[u], self.L.offsets[u], self.rank_weights,
-                                          end_barrier=self.rs_end[u], stream=self.rs_stream)
+                                          end_barrier=self.rs_end[u], stream=self.rs_stream,
+                                          policy=self.rs_policy[u],
+                                          stage=f"acc{u % 2}" if hel else None)
             self.launches += 1
         elif self.rs_route[u] == "symm":   # switch/peer reduction straight into the fp32 shard
             self.symm.reduce_scatter(self._region(src), 0, self._local(self.g32, u),
                                      self.L.counts[u], self.L.offsets[u],
-                                     end_barrier=self.rs_end[u], stream=self.rs_stream)
+                                     end_barrier=self.rs_end[u], stream=self.rs_stream,
+                                     policy=self.rs_policy[u])
             self.launches += 1
         else:
             K.reduce_scatter_uneven(src, self._local(self.g32, u), self.L.counts[u],

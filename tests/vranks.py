@@ -125,3 +125,81 @@ class VirtualGroup:
                                                       self.ctas, st),
                      "het_symm_reduce_scatter_bf16")
         self._launch(go, range(self.n))
+
+
+# ---------------------------------------------------------------------------
+# virtual ranks of the whole train step: N trainers in N threads on one GPU
+
+class VirtualRankGroup:
+    """Host-side agreement of N trainers running in N threads of one process
+    (the step's DistGroup stand-in): sum_ranks is a barrier + shared sum."""
+
+    def __init__(self, n: int):
+        import threading
+        self.n = n
+        self._bar = threading.Barrier(n)
+        self._lock = threading.Lock()
+        self._vals: list[int] = []
+        self._out = 0
+
+    def sum_ranks(self, value: int) -> int:
+        with self._lock:
+            self._vals.append(int(value))
+        if self._bar.wait() == 0:
+            with self._lock:
+                self._out = sum(self._vals)
+                self._vals = []
+        self._bar.wait()
+        return self._out
+
+    def barrier(self) -> None:
+        self._bar.wait()
+
+
+class _Handle:
+    def __init__(self, group: VirtualRankGroup, device):
+        self.group, self.device = group, device
+
+    def barrier(self) -> None:
+        torch.cuda.current_stream(self.device).synchronize()
+        self.group.barrier()
+
+
+class VirtualSymmWorkspace(K.SymmWorkspace):
+    """Rank r's view of a VirtualGroup allocation, with SymmWorkspace's methods:
+    the trainer issues the same fused kernels as on N GPUs (peer route; no NVLS
+    multicast object on one GPU)."""
+
+    def __init__(self, vg: VirtualGroup, rank: int, group: VirtualRankGroup,
+                 policy: int = K.SYMM_AUTO):
+        self.offsets = dict(vg.offsets)
+        self.signal_off = vg.signal_off
+        self.multicast = False
+        self.desc = vg.desc[rank]
+        self.views = {name: vg.view(rank, name) for name, _, _ in vg.regions}
+        self.epoch = [0, 0]
+        self.ctas = vg.ctas
+        self.policy = policy
+        self.handle = _Handle(group, vg.device)
+
+
+def run_ranks(n: int, fn) -> list:
+    """fn(r) for r in 0..n-1 in n threads; re-raises the first exception."""
+    import threading
+    out, err = [None] * n, [None] * n
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:          # noqa: BLE001 (reported below)
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
