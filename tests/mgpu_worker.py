@@ -43,10 +43,18 @@ def offsets(c):
     return [int(sum(c[:j])) for j in range(len(c))]
 
 
+def stage(rank: int, what: str) -> None:
+    print(f"[rank {rank}] {what}", file=sys.stderr, flush=True)
+
+
 def main(out_dir: str) -> None:
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ["LOCAL_RANK"])
+    import faulthandler
+    # a hung rank dumps every thread's Python stack (then keeps running)
+    faulthandler.dump_traceback_later(int(os.environ.get("HET_WORKER_DUMP_S", "240")),
+                                      repeat=True, file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -55,6 +63,7 @@ def main(out_dir: str) -> None:
     cag, crs = K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
     report = {}
     try:
+        stage(rank, "nccl collectives")
         for ci, counts in enumerate(shard_cases(world)):
             offs = offsets(counts)
             total = sum(counts)
@@ -80,6 +89,7 @@ def main(out_dir: str) -> None:
                 err = max_rel(out.cpu().numpy(), want) if counts[rank] else 0.0
                 report[f"rs{ci}_{algo}"] = float(err)
 
+        stage(rank, "fused collectives")
         # fused symmetric-memory collectives (NVLS multicast when available, then peer)
         maxu = max(sum(c) for c in shard_cases(world)) + 64
         for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO),
@@ -90,6 +100,7 @@ def main(out_dir: str) -> None:
                                  use_multicast=use_mc, policy=policy)
             use_mc = f"{int(use_mc)}{policy}"
             report[f"symm_mc_available_{use_mc}"] = float(ws.multicast)
+            stage(rank, f"workspace {use_mc} multicast={ws.multicast}")
             for ci, counts in enumerate(shard_cases(world)):
                 offs = offsets(counts)
                 total = sum(counts)
@@ -135,6 +146,7 @@ def main(out_dir: str) -> None:
             dist.barrier()
             del ws
 
+        stage(rank, "nccl-route step")
         # one train step under a mixed uneven plan with l_i > 1 on some ranks
         arch = ARCHS["tiny_gpt"]
         micro = [(2, 2), (1, 3), (3, 1), (0, 0), (2, 1), (1, 1), (4, 1), (1, 2)][:world]
@@ -160,6 +172,7 @@ def main(out_dir: str) -> None:
         dist.all_reduce(loss)
         g = [t.cpu().numpy() for t in tr.full_units("g32")]
         p = [t.cpu().numpy() for t in tr.full_units("p32")]
+        stage(rank, "fused-route step")
         # the same step through the fused symmetric-memory (NVLS) collectives
         trs = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev,
                                 algo=K.ALGO_SYMM)
@@ -176,6 +189,7 @@ def main(out_dir: str) -> None:
         gs = [t.cpu().numpy() for t in trs.full_units("g32")]
         ps = [t.cpu().numpy() for t in trs.full_units("p32")]
         report["symm_status_step"] = float(K.SymmWorkspace.status(reset=True))
+        stage(rank, "bf16-wire pair steps")
         # l_i <= 1 on every rank: the bf16-wire reduce-scatter against the fp32 one
         pmicro = [(3, 1), (2, 1), (1, 1), (0, 0)][:world] if world > 2 else [(3, 1), (2, 1)]
         pB = sum(m * l for m, l in pmicro)
@@ -197,6 +211,7 @@ def main(out_dir: str) -> None:
             del t2
         report["symm_status_pair"] = float(K.SymmWorkspace.status(reset=True))
 
+        stage(rank, "fault injection")
         # fault injection: rank 0 enters a fused all-gather that no other rank joins
         # (shortened spin limit). Its barrier times out; the trainer's asynchronous
         # status check must then raise CollectiveFault on rank 0 after its next step
@@ -223,6 +238,7 @@ def main(out_dir: str) -> None:
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
+        stage(rank, "saving")
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), loss=float(loss),
                  micro=np.array(micro), ratios=np.array(ratios),
                  report_keys=np.array(list(report.keys())),
@@ -235,9 +251,11 @@ def main(out_dir: str) -> None:
                  **{f"gf{u}": x for u, x in enumerate(pair[False])},
                  pmicro=np.array(pmicro))
     finally:
+        stage(rank, "teardown")
         cag.close()
         crs.close()
         dist.destroy_process_group()
+        stage(rank, "done")
 
 
 if __name__ == "__main__":
