@@ -173,6 +173,43 @@ def _stream(stream: torch.cuda.Stream | None) -> int:
     return s.cuda_stream
 
 
+# Weight-gradient destinations. The step registers, for one unit's backward,
+# where each parameter's bf16 gradient should land (its slot in the symmetric
+# bf16-wire staging buffer); the fused autograd ops below write their weight /
+# bias / norm gradients there directly, so no staging copy follows. Keyed by
+# (data_ptr, shape) of the parameter tensor the op sees.
+_GRAD_DST: dict[tuple[int, tuple[int, ...]], torch.Tensor] = {}
+
+
+def _key(p: torch.Tensor) -> tuple:
+    return (p.data_ptr(), tuple(p.shape), p.dtype, p.device)
+
+
+def grad_out(p) -> torch.Tensor:
+    """The registered destination of the gradient of p (a tensor or its _key),
+    else a fresh tensor."""
+    ptr, shape, dtype, device = p if isinstance(p, tuple) else _key(p)
+    d = _GRAD_DST.get((ptr, shape))
+    if d is not None and d.dtype == dtype:
+        return d
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
+class grad_destinations:
+    """Context manager registering {(data_ptr, shape): destination} for a backward."""
+
+    def __init__(self, mapping: dict):
+        self.mapping = mapping
+
+    def __enter__(self):
+        _GRAD_DST.update(self.mapping)
+        return self
+
+    def __exit__(self, *exc):
+        for k in self.mapping:
+            _GRAD_DST.pop(k, None)
+
+
 def pack_bf16(src: torch.Tensor, dst: torch.Tensor, stream=None) -> None:
     n = src.numel()
     if dst.numel() != n:
@@ -407,17 +444,19 @@ class LayerNormFn(torch.autograd.Function):
                                         mean.data_ptr(), rstd.data_ptr(), rows, d, float(eps),
                                         _stream(None)), "het_layernorm_fwd")
         ctx.save_for_backward(xc, w, mean, rstd)
+        ctx.b = _key(b)       # gradient destination lookup only
         return y
 
     @staticmethod
     def backward(ctx, dy):
         xc, w, mean, rstd = ctx.saved_tensors
+        b = ctx.b
         d = xc.shape[-1]
         rows = xc.numel() // d
         dyc = dy.contiguous()
         dx = torch.empty_like(xc)
-        dw = torch.empty_like(w)
-        db = torch.empty_like(w)
+        dw = grad_out(w)
+        db = grad_out(b)
         part = torch.empty(int(load().het_layernorm_partial_floats(d)), dtype=torch.float32,
                            device=xc.device)
         _check(load().het_layernorm_bwd(_cuda(dyc, torch.bfloat16, "dy"), xc.data_ptr(),
@@ -482,7 +521,7 @@ class RMSNormFn(torch.autograd.Function):
         rows = xc.numel() // d
         dyc = dy.contiguous()
         dx = torch.empty_like(xc)
-        dw = torch.empty_like(w)
+        dw = grad_out(w)
         part = torch.empty(int(load().het_rmsnorm_partial_floats(d)), dtype=torch.float32,
                            device=xc.device)
         _check(load().het_rmsnorm_bwd(_cuda(dyc, torch.bfloat16, "dy"), xc.data_ptr(),
@@ -519,6 +558,7 @@ class AddLayerNormFn(torch.autograd.Function):
                                             y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), rows,
                                             d, float(eps), _stream(None)), "het_layernorm_add_fwd")
         ctx.save_for_backward(sm, w, mean, rstd)
+        ctx.b = _key(b)
         return sm, y
 
     @staticmethod
@@ -530,7 +570,7 @@ class AddLayerNormFn(torch.autograd.Function):
             return ds, ds, None, None, None
         dyc = dy.contiguous()
         dx = torch.empty_like(sm)
-        dw, db = torch.empty_like(w), torch.empty_like(w)
+        dw, db = grad_out(w), grad_out(ctx.b)
         part = torch.empty(int(load().het_layernorm_partial_floats(d)), dtype=torch.float32,
                            device=sm.device)
         _check(load().het_layernorm_bwd_add(_cuda(dyc, torch.bfloat16, "dy"), _ptr_or_none(ds),
@@ -569,7 +609,7 @@ class AddRMSNormFn(torch.autograd.Function):
             return ds, ds, None, None
         dyc = dy.contiguous()
         dx = torch.empty_like(sm)
-        dw = torch.empty_like(w)
+        dw = grad_out(w)
         part = torch.empty(int(load().het_rmsnorm_partial_floats(d)), dtype=torch.float32,
                            device=sm.device)
         _check(load().het_rmsnorm_bwd_add(_cuda(dyc, torch.bfloat16, "dy"), _ptr_or_none(ds),
@@ -647,10 +687,10 @@ def _colsum_scratch(rows: int, n: int, device) -> torch.Tensor:
                        device=device)
 
 
-def bias_grad(g2: torch.Tensor) -> torch.Tensor:
+def bias_grad(g2: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """Column sums of a contiguous bf16 [rows, n] gradient (fp32 sums, bf16 out)."""
     rows, n = g2.shape
-    db = torch.empty(n, dtype=torch.bfloat16, device=g2.device)
+    db = out if out is not None else torch.empty(n, dtype=torch.bfloat16, device=g2.device)
     part = _colsum_scratch(rows, n, g2.device)
     _check(load().het_bias_grad(_cuda(g2, torch.bfloat16, "g"), rows, n, db.data_ptr(),
                                 part.data_ptr(), _stream(None)), "het_bias_grad")
@@ -664,6 +704,7 @@ class LinearFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, b):
         ctx.save_for_backward(x, w)
+        ctx.b = None if b is None else _key(b)
         return torch.nn.functional.linear(x, w, b)
 
     @staticmethod
@@ -671,8 +712,33 @@ class LinearFn(torch.autograd.Function):
         x, w = ctx.saved_tensors
         g2 = g.reshape(-1, g.shape[-1]).contiguous()
         dx = (g2 @ w).view(x.shape) if ctx.needs_input_grad[0] else None
-        dw = g2.t() @ x.reshape(-1, x.shape[-1])
-        return dx, dw, bias_grad(g2)
+        dw = torch.mm(g2.t(), x.reshape(-1, x.shape[-1]), out=grad_out(w))
+        db = None if ctx.b is None else bias_grad(g2, grad_out(ctx.b))
+        return dx, dw, db
+
+
+class LinearNBFn(torch.autograd.Function):
+    """y = x W^T (no bias) with the weight gradient written to its registered
+    destination (grad_out): the Llama projections."""
+
+    @staticmethod
+    def forward(ctx, x, w):
+        ctx.save_for_backward(x, w)
+        return x @ w.t()
+
+    @staticmethod
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        g2 = g.reshape(-1, g.shape[-1])
+        dx = (g2 @ w).view(x.shape) if ctx.needs_input_grad[0] else None
+        dw = torch.mm(g2.t(), x.reshape(-1, x.shape[-1]), out=grad_out(w))
+        return dx, dw
+
+
+def linear_nb(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    if not torch.is_grad_enabled():
+        return x @ w.t()
+    return LinearNBFn.apply(x, w)
 
 
 class LinearGeluFn(torch.autograd.Function):
@@ -686,6 +752,7 @@ class LinearGeluFn(torch.autograd.Function):
         _check(load().het_gelu_fwd(pre.data_ptr(), y.data_ptr(), pre.numel(), _stream(None)),
                "het_gelu_fwd")
         ctx.save_for_backward(x, w, pre)
+        ctx.b = _key(b)
         return y
 
     @staticmethod
@@ -695,13 +762,13 @@ class LinearGeluFn(torch.autograd.Function):
         rows = pre.numel() // n
         g2 = g.reshape(rows, n).contiguous()
         dpre = torch.empty((rows, n), dtype=torch.bfloat16, device=g.device)
-        db = torch.empty(n, dtype=torch.bfloat16, device=g.device)
+        db = grad_out(ctx.b)
         part = _colsum_scratch(rows, n, g.device)
         _check(load().het_gelu_bwd_bias(g2.data_ptr(), pre.data_ptr(), dpre.data_ptr(), rows, n,
                                         db.data_ptr(), part.data_ptr(), _stream(None)),
                "het_gelu_bwd_bias")
         dx = (dpre @ w).view(x.shape) if ctx.needs_input_grad[0] else None
-        dw = dpre.t() @ x.reshape(-1, x.shape[-1])
+        dw = torch.mm(dpre.t(), x.reshape(-1, x.shape[-1]), out=grad_out(w))
         return dx, dw, db
 
 

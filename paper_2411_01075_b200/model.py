@@ -172,17 +172,17 @@ def block_forward(arch: ArchSpec, p: dict[str, torch.Tensor], x: torch.Tensor) -
             # each (no weight copies), RoPE and the head split in one pass, SwiGLU over
             # the packed projection
             h = _K.rms_norm(x, p["rms1"])
-            qkv = h @ _K.adjacent_rows(p["wq"], p["wk"], p["wv"]).t()
+            qkv = _K.linear_nb(h, _K.adjacent_rows(p["wq"], p["wk"], p["wv"]))
             q, k, v = (t.transpose(1, 2) for t in _K.rope_qkv(qkv, H))
             a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-            o = a.transpose(1, 2).reshape(b, s, d) @ p["wo"].t()
+            o = _K.linear_nb(a.transpose(1, 2).reshape(b, s, d), p["wo"])
             if FUSE_RESIDUAL_NORM:
                 x, h = _K.add_rms_norm(x, o, p["rms2"])
             else:
                 x = x + o
                 h = _K.rms_norm(x, p["rms2"])
             w13 = _K.adjacent_rows(p["w1"], p["w3"])
-            return x + _K.swiglu_packed(h @ w13.t()) @ p["w2"].t()
+            return x + _K.linear_nb(_K.swiglu_packed(_K.linear_nb(h, w13)), p["w2"])
         h = _rms(x, p["rms1"])
         q = (h @ p["wq"].t()).view(b, s, H, dh).transpose(1, 2)
         k = (h @ p["wk"].t()).view(b, s, H, dh).transpose(1, 2)

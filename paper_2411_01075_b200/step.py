@@ -205,6 +205,10 @@ class UnevenFSDPTrainer:
         # group instead of per microbatch, bit-identical to one pass each
         self.acc_microbatches = 2
         self.bf16_wire = bf16_wire
+        # bf16-wire units: the backward's fused ops write each parameter gradient
+        # straight into its slot of the symmetric staging buffer gb{u % 2}
+        # (hetstep.grad_destinations), so no het_gather_bf16 copy follows
+        self.grad_in_place = True
         # Eq. 1 weights of every rank (the bf16-wire reduce-scatter applies them itself)
         self.rank_weights = [a.microbatch / plan.total_batch for a in plan.assignments]
         self._set_routes(self.symm is not None)
@@ -591,16 +595,39 @@ class UnevenFSDPTrainer:
         span = (self.acc[1].data_ptr() - a0.data_ptr()) // 4 + self.acc[1].numel()
         return a0.as_strided((span,), (1,), a0.storage_offset()), off
 
+    def _grad_dst(self, u: int, params: dict) -> dict:
+        """Destinations of unit u's parameter gradients in gb{u % 2} (keyed as
+        hetstep.grad_out looks them up), including the adjacent-row groups the
+        Llama unit multiplies as one matrix (wq|wk|wv, w1|w3)."""
+        gb = self.symm[f"gb{u % 2}"]
+        out = {}
+        for nm, shape in self.arch.unit_layout():
+            t, off = params[nm], self.unit_seg[nm]
+            out[(t.data_ptr(), tuple(t.shape))] = gb[off:off + t.numel()].view(shape)
+        for group in (("wq", "wk", "wv"), ("w1", "w3")):
+            if all(g in params for g in group):
+                ts = [params[g] for g in group]
+                rows = sum(t.shape[0] for t in ts)
+                shape = (rows,) + tuple(ts[0].shape[1:])
+                off = self.unit_seg[group[0]]
+                n = rows * ts[0].shape[1]
+                out[(ts[0].data_ptr(), shape)] = gb[off:off + n].view(shape)
+        return out
+
     def _accumulate_units(self, items, names, seg):
         """One het_accumulate (FIRST) over [(u, grads), ...] of several units; units
-        on the bf16 wire are staged unscaled into their bf16 buffer instead."""
+        on the bf16 wire are staged unscaled into their bf16 buffer instead (only
+        the gradients the backward did not already write there)."""
         w16 = [(u, g) for u, g in items if self.wire16[u]]
         items = [(u, g) for u, g in items if not self.wire16[u]]
         if w16:
             stage = []
+            base = self.symm["gb0"].data_ptr()
             for u, grads in w16:
-                off = (self.symm[f"gb{u % 2}"].data_ptr() - self.symm["gb0"].data_ptr()) // 2
-                stage += [(g, off + seg[nm]) for g, nm in zip(grads, names)]
+                off = (self.symm[f"gb{u % 2}"].data_ptr() - base) // 2
+                stage += [(g, off + seg[nm]) for g, nm in zip(grads, names)
+                          if g.data_ptr() != base + 2 * (off + seg[nm])]
+        if w16 and stage:
             n16 = sum(g.numel() for g, _ in stage)
             gb = self.symm["gb0"]
             span = (self.symm["gb1"].data_ptr() - gb.data_ptr()) // 2 + self.symm["gb1"].numel()
@@ -881,6 +908,18 @@ class UnevenFSDPTrainer:
             flat = self._unit_flat(u)
             pl = {nm: t.requires_grad_(True) for nm, t in views(flat, arch.unit_layout()).items()}
             plist = [pl[nm] for nm in unit_names]
+            in_place = (self.grad_in_place and self.pair_units and self.wire16[u] and nmb > 0
+                        and self.cuda)
+            if in_place:
+                # the backward writes gb{u % 2} itself: its last readers are RS(u+2) here
+                # and on every peer; RS(u+1) / RS(u+2), whichever is issued and carries
+                # the end barrier, proves they finished
+                for w_ in (u + 1, u + 2):
+                    if w_ in rs_ev:
+                        comp.wait_event(rs_ev[w_])
+                dst = K.grad_destinations(self._grad_dst(u, pl))
+            else:
+                dst = contextlib.nullcontext()
             for k in range(nmb):
                 nk, nu = (k + 1, u) if k + 1 < nmb else (0, u - 1)
                 if deep:
@@ -904,7 +943,7 @@ class UnevenFSDPTrainer:
                         fetched[("grad", nk, nu)] = self._fetch("grad", nk, nu, "bwd")
                 else:
                     g_in = dy[k]
-                with self._span("bwd_compute", u, k + 1, "bwd", comp):
+                with self._span("bwd_compute", u, k + 1, "bwd", comp), dst:
                     grads = torch.autograd.grad(y, plist_u + [x], g_in)
                     h[k][u] = dy[k] = None
                     if self.pair_units:
