@@ -326,7 +326,9 @@ class UnevenFSDPTrainer:
         for THIS world size before a step trusts it). Exactly representable
         integer patterns make the expected bf16 gather and fp32 sum
         order-independent. Any mismatch or barrier timeout on any rank turns
-        every route to NCCL on every rank."""
+        every route to NCCL on every rank. Only this rank's stream is
+        synchronised (never the device): ranks driven from threads of one
+        process (tests/vranks.py) must not wait on each other's spinning kernels."""
         import torch.distributed as dist
         dev = self.device
         shapes = {}
@@ -356,7 +358,7 @@ class UnevenFSDPTrainer:
                 gb = self.symm["gb0"]
                 gb[:size].copy_(pattern(torch.arange(size, device=dev), self.rank))
                 out = torch.full((cnt,), float("nan"), device=dev)
-                torch.cuda.synchronize(dev)
+                self._current().synchronize()
                 self.symm.handle.barrier()
                 hel = self.rs_policy[u] == K.SYMM_HELPERS
                 self.symm.reduce_scatter_bf16("gb0", 0, out, counts, offsets, self.rank_weights,
@@ -375,7 +377,7 @@ class UnevenFSDPTrainer:
             if rs:
                 self.symm[acc][:size].copy_(pattern(torch.arange(size, device=dev), self.rank))
                 out = torch.full((cnt,), float("nan"), device=dev)
-                torch.cuda.synchronize(dev)
+                self._current().synchronize()
                 self.symm.handle.barrier()
                 pol = K.symm_policy("rs", counts, self.N, self.symm.multicast)
                 self.symm.reduce_scatter(acc, 0, out, counts, offsets, end_barrier=True,
@@ -384,13 +386,13 @@ class UnevenFSDPTrainer:
                 want = sum(pattern(idx, r) for r in range(self.N))
                 bad += int(not torch.equal(out, want))
                 checked += 1
-        torch.cuda.synchronize(dev)
+        self._current().synchronize()
         status = K.SymmWorkspace.status(reset=True)
         failures = self._group.sum_ranks(bad + (1 if status else 0))
         self.symm.handle.barrier()
         for name in ("ub0", "acc0", "rbuf", "racc", "gb0"):
             self.symm[name].zero_()
-        torch.cuda.synchronize(dev)
+        self._current().synchronize()
         self.symm.handle.barrier()
         return {"ok": failures == 0, "checked": checked, "failures": failures, "status": status}
 

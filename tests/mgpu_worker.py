@@ -221,7 +221,7 @@ def main(out_dir: str) -> None:
         K.set_symm_timeout_ms(300)
         if rank == 0:
             trs.symm.allgather_pack(torch.zeros(4, device=dev), "ub0", 0, [4] + [0] * (world - 1),
-                                    [0] * world)
+                                    [0] + [4] * (world - 1))
             torch.cuda.synchronize()
         K.set_symm_timeout_ms(10_000)
         if rank != 0:

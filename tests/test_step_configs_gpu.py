@@ -24,8 +24,9 @@ Bars, as this repo reads north_star's "2e-2 for bf16-input gradients" and
   * the post-AdamW master against the fully independent oracle (oracle
     gradients -> oracle AdamW): AdamW's first step moves every parameter by
     about lr * sign(g), so bf16-level gradient differences flip signs only
-    where |g_ref| is tiny; on elements with |g_ref| > 1e-2 * max|g_ref| the
-    update must agree to 1e-3 relative, and sign flips may touch at most
+    where |g_ref| is within the gradient error; on elements with |g_ref| >
+    ELEM_ABS * max|g_ref| the update must agree to 1e-3 relative, and sign
+    flips may touch at most
     FLIP_FRAC of all elements.
 """
 import numpy as np
@@ -122,7 +123,8 @@ def test_baseline_arch_step_matches_cpu_oracle(cuda, name, m, l, offload):
     # fully independent: oracle gradient -> oracle AdamW
     ip, _, _ = SO.adamw(p0, g_ref_flat, z, z, step=1, **OPT_D)
     d_gpu, d_ref = p_gpu.astype(np.float64) - p0, ip.astype(np.float64) - p0
-    big = np.abs(g_ref_flat) > 1e-2 * np.max(np.abs(g_ref_flat))
+    # elements whose gradient exceeds the element-wise error bar cannot flip sign
+    big = np.abs(g_ref_flat) > ELEM_ABS * np.max(np.abs(g_ref_flat))
     assert np.max(np.abs(d_gpu[big] - d_ref[big]) / np.abs(d_ref[big])) <= 1e-3
     flips = float(np.mean(np.sign(d_gpu + OPT.lr * OPT.weight_decay * p0) !=
                           np.sign(d_ref + OPT.lr * OPT.weight_decay * p0)))
