@@ -1162,6 +1162,21 @@ def ag_symm_policy(counts: Sequence[int], nranks: int, multicast: bool = True) -
 SYMM_ALIGN = 256
 
 
+def region_tensor(raw: torch.Tensor, byte_off: int, numel: int, dtype: torch.dtype
+                  ) -> torch.Tensor:
+    """A typed region of a workspace allocation that aliases its memory but is
+    NOT an autograd view of it: every region keeps its own version counter, so
+    the backward writing gradients into the bf16-wire staging region does not
+    look like an in-place update of the parameters (views of the gathered-unit
+    regions) that autograd saved."""
+    esz = torch.tensor([], dtype=dtype).element_size()
+    start = raw.storage_offset() * raw.element_size() + byte_off
+    if start % esz:
+        raise InputError("workspace region is not aligned to its element size")
+    return torch.empty(0, dtype=dtype, device=raw.device).set_(
+        raw.untyped_storage(), start // esz, (numel,), (1,))
+
+
 class SymmWorkspace:
     """One allocation with the same layout on every rank (torch symmetric
     memory = plumbing: allocation, peer mapping, NVLS multicast binding),
@@ -1199,11 +1214,8 @@ class SymmWorkspace:
         d.mc_base = mc
         d.signal_off = self.signal_off
         self.desc = d
-        self.views: dict[str, torch.Tensor] = {}
-        for name, numel, dtype in regions:
-            o = self.offsets[name]
-            nbytes = numel * torch.tensor([], dtype=dtype).element_size()
-            self.views[name] = self.raw[o:o + nbytes].view(dtype)
+        self.views = {name: region_tensor(self.raw, self.offsets[name], numel, dtype)
+                      for name, numel, dtype in regions}
         self.epoch = [0, 0]
         self.ctas = ctas
         self.policy = policy

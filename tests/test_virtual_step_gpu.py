@@ -94,7 +94,7 @@ def test_virtual_multirank_step_matches_oracle(cuda, name, n):
             torch.cuda.current_stream().synchronize()
             return tr
 
-    trs = run_ranks(n, build)
+    trs = run_ranks(n, build, group)
     assert all(t.route_check["ok"] for t in trs), [t.route_check for t in trs]
     assert all(r == "symm" for t in trs for r in t.ag_route + t.rs_route)
     p0 = [t.p32.clone() for t in trs]
@@ -105,7 +105,7 @@ def test_virtual_multirank_step_matches_oracle(cuda, name, n):
             trs[r].check_faults()
             return float(loss)
 
-    losses = run_ranks(n, step)
+    losses = run_ranks(n, step, group)
     torch.cuda.synchronize()
     assert K.SymmWorkspace.status(reset=True) == 0
     live = [(toks[r], (a.microbatch, a.num_microbatches))

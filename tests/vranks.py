@@ -65,11 +65,12 @@ class VirtualGroup:
         torch.cuda.synchronize(device)
 
     def view(self, r: int, name: str) -> torch.Tensor:
+        """Rank r's copy of a region (its own version counter, like the real
+        workspace's regions: hetstep.region_tensor)."""
         for nm, numel, dtype in self.regions:
             if nm == name:
-                o = r * self.stride + self.offsets[name]
-                esz = torch.tensor([], dtype=dtype).element_size()
-                return self.raw[o:o + numel * esz].view(dtype)
+                return K.region_tensor(self.raw, r * self.stride + self.offsets[name], numel,
+                                       dtype)
         raise KeyError(name)
 
     def _launch(self, fn, ranks) -> None:
@@ -134,10 +135,11 @@ class VirtualRankGroup:
     """Host-side agreement of N trainers running in N threads of one process
     (the step's DistGroup stand-in): sum_ranks is a barrier + shared sum."""
 
-    def __init__(self, n: int):
+    def __init__(self, n: int, timeout: float = 300.0):
         import threading
         self.n = n
-        self._bar = threading.Barrier(n)
+        # a rank that dies breaks the barrier for the others instead of hanging them
+        self._bar = threading.Barrier(n, timeout=timeout)
         self._lock = threading.Lock()
         self._vals: list[int] = []
         self._out = 0
@@ -183,8 +185,9 @@ class VirtualSymmWorkspace(K.SymmWorkspace):
         self.handle = _Handle(group, vg.device)
 
 
-def run_ranks(n: int, fn) -> list:
-    """fn(r) for r in 0..n-1 in n threads; re-raises the first exception."""
+def run_ranks(n: int, fn, group: VirtualRankGroup | None = None) -> list:
+    """fn(r) for r in 0..n-1 in n threads; re-raises the first exception (a
+    failing rank aborts the group's barrier so the others fail too)."""
     import threading
     out, err = [None] * n, [None] * n
 
@@ -193,6 +196,8 @@ def run_ranks(n: int, fn) -> list:
             out[r] = fn(r)
         except BaseException as e:          # noqa: BLE001 (reported below)
             err[r] = e
+            if group is not None:
+                group._bar.abort()
 
     ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
     for t in ts:
