@@ -338,6 +338,11 @@ class UnevenFSDPTrainer:
         K.SymmWorkspace.status(reset=True)
         bad = 0
         checked = 0
+        # every rank has finished its construction (allocations, pinned buffers,
+        # streams: implicit device synchronisation points) before any rank enters a
+        # fused kernel whose barrier waits for it
+        self._current().synchronize()
+        self.symm.handle.barrier()
 
         def pattern(idx: torch.Tensor, r: int) -> torch.Tensor:
             return (((idx * 7 + r * 13) % 251) - 125).to(torch.float32)
