@@ -302,6 +302,18 @@ typedef struct {
 } het_symm_t;
 
 int64_t het_symm_signal_bytes(void);
+/* Test support: all N ranks of one fused collective (op = HET_OP_AG / RS /
+ * RS_BF16 with the given policy) as ONE cooperative launch on one GPU, CTA b of
+ * rank r at blockIdx r * ctas + b, descs[r] being rank r's descriptor over one
+ * allocation (mc_base = 0). The same kernel bodies and barriers as N real
+ * launches with every CTA co-resident by construction (refused with HET_EARG
+ * if N * ctas CTAs cannot be). srcs[r] / outs[r]: rank r's fp32 range (AG) or
+ * output shard (RS). Synchronous. */
+int het_symm_virtual(int op, int nranks, const het_symm_t* descs, const float* const* srcs,
+                     float* const* outs, const int64_t* counts, const int64_t* offsets,
+                     uint64_t off, const float* weights, uint32_t epoch, int channel,
+                     int end_barrier, int policy, uint64_t stage_off, int ctas, void* stream);
+
 /* Sticky device status of the symmetric kernels (0 or HET_SYMM_TIMEOUT).
  * Synchronous (device-wide copy); reset=1 clears it. */
 int het_symm_status(int reset);

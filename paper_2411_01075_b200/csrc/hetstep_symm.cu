@@ -42,6 +42,19 @@ constexpr int kUnroll = 8;                   // independent 16-byte remote ops p
 constexpr int kMaxCtas = HET_SYMM_MAX_CTAS;
 // signal slot kinds: 0 start barrier, 1 end barrier, 2 pair-relay flag, 3 helper progress
 constexpr int kKinds = 4;
+
+// The CTA's index and count WITHIN ITS RANK's grid. A real launch runs one rank
+// per grid (blockIdx.x, gridDim.x). The virtual-rank launch (het_symm_virtual)
+// runs N ranks as ONE cooperative grid of N * ctas CTAs -- CTA b of rank r at
+// blockIdx.x = r * ctas + b -- so all CTAs are co-resident by construction.
+// Every barrier slot, grid-stride loop and "CTA 0" edge below uses these.
+__shared__ int s_cta, s_ncta;
+
+__device__ __forceinline__ void set_ctx(int cta, int ncta) {
+  s_cta = cta;              // every thread writes the same value
+  s_ncta = ncta;
+  __syncthreads();
+}
 // Barrier spin limit (wall clock); het_tune(HET_TUNE_SYMM_TIMEOUT_MS) overrides it
 // so a fault-injection test need not wait the full 10 s.
 uint64_t g_spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
@@ -127,8 +140,8 @@ __device__ void cross_barrier(const Sym& s, const uint64_t* peer, int channel, i
   const int t = threadIdx.x;
   if (t < s.nranks) {
     __threadfence_system();
-    st_release_sys(slot(peer[t], s.signal_off, channel, kind, blockIdx.x, s.rank), epoch);
-    wait_epoch(slot(peer[s.rank], s.signal_off, channel, kind, blockIdx.x, t), epoch,
+    st_release_sys(slot(peer[t], s.signal_off, channel, kind, s_cta, s.rank), epoch);
+    wait_epoch(slot(peer[s.rank], s.signal_off, channel, kind, s_cta, t), epoch,
                s.timeout_ns);
   }
   __syncthreads();
@@ -190,8 +203,8 @@ template <int NR>
 __device__ __forceinline__ void ag_push(const float* __restrict__ src, int64_t h2, int64_t lo,
                                         int64_t hi, uint64_t dst0, const uint64_t* peer, int nr,
                                         uint32_t mask, bool src_vec) {
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(s_ncta) * blockDim.x;
   for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kUnroll) {
     uint4 w[kUnroll];
 #pragma unroll
@@ -232,8 +245,8 @@ __device__ __forceinline__ void ag_push(const float* __restrict__ src, int64_t h
 template <int NR>
 __device__ __forceinline__ void ag_forward(int64_t h2, int64_t lo, int64_t hi, uint64_t dst0,
                                            const uint64_t* peer, int me, int nr, uint32_t mask) {
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(s_ncta) * blockDim.x;
   for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kUnroll) {
     uint4 w[kUnroll];
 #pragma unroll
@@ -257,8 +270,8 @@ __device__ __forceinline__ void ag_forward(int64_t h2, int64_t lo, int64_t hi, u
 }
 
 template <bool MC, int NR>
-__global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restrict__ src,
-                                                           const __grid_constant__ Args a) {
+__device__ __forceinline__ void symm_ag_kernel_body(const float* __restrict__ src,
+                                                           const Args& a) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
@@ -273,8 +286,8 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
   if (h2 > n) h2 = n;
   const int64_t nvec = (n - h2) / 8;
   const int64_t body_end = h2 + nvec * 8;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(s_ncta) * blockDim.x;
   // body: 8 bf16 per 16-byte multicast store; kUnroll vectors per thread in
   // flight (all local loads issued before the remote stores)
   const bool src_vec = ((reinterpret_cast<uintptr_t>(src + h2)) & 15) == 0;
@@ -291,14 +304,14 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence_system();
-        st_release_sys(slot(peer[a.relay_to], s.signal_off, a.channel, 2, blockIdx.x, s.rank),
+        st_release_sys(slot(peer[a.relay_to], s.signal_off, a.channel, 2, s_cta, s.rank),
                        a.epoch);
       }
     }
     ag_push<NR>(src, h2, 0, direct, dst0, peer, nr, all, src_vec);
     if (a.relay_from >= 0) {
       if (threadIdx.x == 0) {
-        wait_epoch(slot(peer[s.rank], s.signal_off, a.channel, 2, blockIdx.x, a.relay_from),
+        wait_epoch(slot(peer[s.rank], s.signal_off, a.channel, 2, s_cta, a.relay_from),
                    a.epoch, s.timeout_ns);
       }
       __syncthreads();
@@ -345,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
     }
   }
   // edges (CTA 0): 4-byte pairs via multicast, a lone 2-byte element via peer stores
-  if (blockIdx.x == 0) {
+  if (s_cta == 0) {
     auto pair = [&](int64_t e) {
       const uint64_t off = dst0 + static_cast<uint64_t>(e) * 2;
       const uint32_t w = pack_bf16x2(src[e], src[e + 1]);
@@ -370,6 +383,13 @@ __global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restri
   cross_barrier(s, peer, a.channel, 1, a.epoch);   // every rank's stores have landed
 }
 
+template <bool MC, int NR>
+__global__ void __launch_bounds__(kThreads) symm_ag_kernel(const float* __restrict__ src,
+                                                           const __grid_constant__ Args a) {
+  set_ctx(blockIdx.x, gridDim.x);
+  symm_ag_kernel_body<MC, NR>(src, a);
+}
+
 // ---------------------------------------------------------------- reduce-scatter
 
 __device__ __forceinline__ void store4(float* out, int64_t e, const float4& r, bool vec) {
@@ -384,7 +404,7 @@ __device__ __forceinline__ void store4(float* out, int64_t e, const float4& r, b
 }
 
 template <bool MC, int NR>
-__global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const __grid_constant__ Args a) {
+__device__ __forceinline__ void symm_rs_kernel_body(float* __restrict__ out, const Args& a) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
@@ -397,8 +417,8 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
   const int64_t nvec = (n - head) / 4;
   const int64_t body_end = head + nvec * 4;
   const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(s_ncta) * blockDim.x;
   if (MC) {
     for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kUnroll) {
       float4 r[kUnroll];
@@ -447,7 +467,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
       }
     }
   }
-  if (blockIdx.x == 0) {
+  if (s_cta == 0) {
     auto one = [&](int64_t e) {
       const uint64_t off = src0 + static_cast<uint64_t>(e) * 4;
       float r = 0.f;
@@ -462,6 +482,12 @@ __global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ o
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
   if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading my acc
+}
+
+template <bool MC, int NR>
+__global__ void __launch_bounds__(kThreads) symm_rs_kernel(float* __restrict__ out, const __grid_constant__ Args a) {
+  set_ctx(blockIdx.x, gridDim.x);
+  symm_rs_kernel_body<MC, NR>(out, a);
 }
 
 // ---------------------------------------------------------------- reduce-scatter, bf16 wire
@@ -480,9 +506,9 @@ __device__ __forceinline__ void bf8_to_f(const uint4& raw, float (&f)[8]) {
 }
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restrict__ out,
-                                                                const __grid_constant__ Args a,
-                                                                const __grid_constant__ Weights wt) {
+__device__ __forceinline__ void symm_rs_bf16_kernel_body(float* __restrict__ out,
+                                                                const Args& a,
+                                                                const Weights& wt) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
@@ -496,8 +522,8 @@ __global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restric
   const int64_t nvec = (n - head) / 8;
   const int64_t body_end = head + nvec * 8;
   const bool out_vec = ((reinterpret_cast<uintptr_t>(out + head)) & 15) == 0;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(s_ncta) * blockDim.x;
   constexpr int kB = NR > 0 ? (16 / NR > 1 ? 16 / NR : 2) : 2;   // vectors per batch
   for (int64_t v0 = gtid; v0 < nvec; v0 += gsz * kB) {
     uint4 x[kB][kMaxR];
@@ -540,7 +566,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restric
       }
     }
   }
-  if (blockIdx.x == 0) {
+  if (s_cta == 0) {
     auto one = [&](int64_t e) {
       const uint64_t off = src0 + static_cast<uint64_t>(e) * 2;
       float r = 0.f;
@@ -555,6 +581,14 @@ __global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restric
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
   if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading mine
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads) symm_rs_bf16_kernel(float* __restrict__ out,
+                                                                const __grid_constant__ Args a,
+                                                                const __grid_constant__ Weights wt) {
+  set_ctx(blockIdx.x, gridDim.x);
+  symm_rs_bf16_kernel_body<NR>(out, a, wt);
 }
 
 
@@ -602,21 +636,21 @@ __device__ __forceinline__ void signal_progress(uint64_t owner_base, const Sym& 
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    st_release_sys(slot(owner_base, s.signal_off, channel, 3, blockIdx.x, s.rank), v);
+    st_release_sys(slot(owner_base, s.signal_off, channel, 3, s_cta, s.rank), v);
   }
 }
 
 __device__ __forceinline__ void await_progress(const uint64_t* peer, const Sym& s, int channel,
                                                int src, uint32_t v) {
   if (threadIdx.x == 0)
-    wait_epoch(slot(peer[s.rank], s.signal_off, channel, 3, blockIdx.x, src), v, s.timeout_ns);
+    wait_epoch(slot(peer[s.rank], s.signal_off, channel, 3, s_cta, src), v, s.timeout_ns);
   __syncthreads();
 }
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads) symm_ag_help_kernel(const float* __restrict__ src,
-                                                                const __grid_constant__ Args a,
-                                                                const __grid_constant__ HArgs h) {
+__device__ __forceinline__ void symm_ag_help_kernel_body(const float* __restrict__ src,
+                                                                const Args& a,
+                                                                const HArgs& h) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
@@ -629,7 +663,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_help_kernel(const float* __r
   int64_t h1, h2, nvec;
   ag_geometry(dst0, n, &h1, &h2, &nvec);
   const bool src_vec = ((reinterpret_cast<uintptr_t>(src + h2)) & 15) == 0;
-  const int64_t per_iter = static_cast<int64_t>(gridDim.x) * blockDim.x * kUnroll;
+  const int64_t per_iter = static_cast<int64_t>(s_ncta) * blockDim.x * kUnroll;
   // 1) my pieces to their helpers only (interleaved, so every helper starts early)
   int64_t kmax = 0;
   for (int p = 0; p < h.n_own; ++p) {
@@ -670,7 +704,7 @@ __global__ void __launch_bounds__(kThreads) symm_ag_help_kernel(const float* __r
     }
   }
   // 4) edges of my range (CTA 0), straight to every rank
-  if (blockIdx.x == 0) {
+  if (s_cta == 0) {
     const int64_t body_end = h2 + nvec * 8;
     auto pair = [&](int64_t e) {
       const uint32_t w = pack_bf16x2(src[e], src[e + 1]);
@@ -690,6 +724,14 @@ __global__ void __launch_bounds__(kThreads) symm_ag_help_kernel(const float* __r
     if (t == 0 && (n - body_end) % 2 == 1) single(n - 1);
   }
   cross_barrier(s, peer, a.channel, 1, a.epoch);   // every rank's stores have landed
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads) symm_ag_help_kernel(const float* __restrict__ src,
+                                                                const __grid_constant__ Args a,
+                                                                const __grid_constant__ HArgs h) {
+  set_ctx(blockIdx.x, gridDim.x);
+  symm_ag_help_kernel_body<NR>(src, a, h);
 }
 
 // Reduce-scatter element geometry of a rank's range: 16-byte vectors of VE
@@ -743,18 +785,18 @@ struct RsVec {
 };
 
 template <int NR, bool BF16>
-__global__ void __launch_bounds__(kThreads) symm_rs_help_kernel(float* __restrict__ out,
-                                                                const __grid_constant__ Args a,
-                                                                const __grid_constant__ HArgs h,
-                                                                const __grid_constant__ Weights wt) {
+__device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out,
+                                                                const Args& a,
+                                                                const HArgs& h,
+                                                                const Weights& wt) {
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
   cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's input is final
   const int nr = NR > 0 ? NR : s.nranks;
   constexpr int ES = BF16 ? 2 : 4, VE = 16 / ES;
-  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t gsz = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
+  const int64_t gsz = static_cast<int64_t>(s_ncta) * blockDim.x;
   const int64_t per_iter = gsz * kUnroll;
   // 1) helper: reduce the owners' pieces into my staging copy, signal each iteration
   int64_t kmax = 0;
@@ -847,7 +889,7 @@ __global__ void __launch_bounds__(kThreads) symm_rs_help_kernel(float* __restric
     }
   }
   // 4) head / tail elements of my range (CTA 0), reduced directly
-  if (blockIdx.x == 0) {
+  if (s_cta == 0) {
     const int64_t body_end = head + nvec * VE;
     auto one = [&](int64_t le) {
       const uint64_t off = a.data_off + static_cast<uint64_t>(a.offset + le) * ES;
@@ -871,6 +913,52 @@ __global__ void __launch_bounds__(kThreads) symm_rs_help_kernel(float* __restric
   }
   // every owner finished pulling its helpers' staging (and every helper its inputs)
   cross_barrier(s, peer, a.channel, 1, a.epoch);
+}
+
+template <int NR, bool BF16>
+__global__ void __launch_bounds__(kThreads) symm_rs_help_kernel(float* __restrict__ out,
+                                                                const __grid_constant__ Args a,
+                                                                const __grid_constant__ HArgs h,
+                                                                const __grid_constant__ Weights wt) {
+  set_ctx(blockIdx.x, gridDim.x);
+  symm_rs_help_kernel_body<NR, BF16>(out, a, h, wt);
+}
+
+// ---------------------------------------------------------------- virtual ranks
+//
+// All N ranks of one collective as ONE cooperative grid on one GPU (CTA b of
+// rank r at blockIdx.x = r * ctas + b, each rank's arguments from device
+// memory, the peer table of every rank pointing into one allocation): the
+// same kernel bodies and in-kernel barriers as N real launches, with every
+// CTA guaranteed co-resident. Test support for the 1-GPU parity runs
+// (het_symm_virtual; tests/test_virtual_ranks.py).
+
+struct VRank {
+  Args a;
+  HArgs h;
+  const float* src;
+  float* out;
+};
+
+enum VKind { kVAg = 0, kVAgHelp = 1, kVRs = 2, kVRs16 = 3, kVRsHelp = 4 };
+
+template <int KIND, int NR, bool BF16>
+__global__ void __launch_bounds__(kThreads) symm_virtual_kernel(const VRank* __restrict__ v,
+                                                                int ctas,
+                                                                const __grid_constant__ Weights wt) {
+  const VRank& x = v[blockIdx.x / ctas];
+  set_ctx(blockIdx.x % ctas, ctas);
+  if constexpr (KIND == kVAg) {
+    symm_ag_kernel_body<false, NR>(x.src, x.a);
+  } else if constexpr (KIND == kVAgHelp) {
+    symm_ag_help_kernel_body<NR>(x.src, x.a, x.h);
+  } else if constexpr (KIND == kVRs) {
+    symm_rs_kernel_body<false, NR>(x.out, x.a);
+  } else if constexpr (KIND == kVRs16) {
+    symm_rs_bf16_kernel_body<NR>(x.out, x.a, wt);
+  } else {
+    symm_rs_help_kernel_body<NR, BF16>(x.out, x.a, x.h, wt);
+  }
 }
 
 // multicast kernels do not loop over ranks; peer kernels get the rank count
@@ -1198,6 +1286,85 @@ int het_symm_helper_plan(int op, int nranks, const int64_t* counts, const int64_
     }
   }
   return hp.npieces;
+}
+
+int het_symm_virtual(int op, int nranks, const het_symm_t* descs, const float* const* srcs,
+                     float* const* outs, const int64_t* counts, const int64_t* offsets,
+                     uint64_t off, const float* weights, uint32_t epoch, int channel,
+                     int end_barrier, int policy, uint64_t stage_off, int ctas, void* stream) {
+  if (!descs || nranks < 1 || nranks > HET_MAX_RANKS || !srcs || !outs ||
+      (op != HET_OP_AG && op != HET_OP_RS && op != HET_OP_RS_BF16))
+    return fail(HET_EARG, "het_symm_virtual: bad args");
+  if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
+  if (off & 15) return fail(HET_EARG, "het_symm_virtual: offset not 16B aligned");
+  if (op != HET_OP_AG && policy == HET_SYMM_RELAY) policy = HET_SYMM_AUTO;
+  const bool helpers = policy == HET_SYMM_HELPERS;
+  if (op == HET_OP_RS_BF16 && (!weights || (helpers && (stage_off & 15))))
+    return fail(HET_EARG, "het_symm_virtual: bf16 wire needs weights (and a 16B stage)");
+  VRank host[HET_MAX_RANKS];
+  HelperPlan hp;
+  if (helpers) hp = plan_for(op, nranks, counts, offsets, off);
+  for (int r = 0; r < nranks; ++r) {
+    const het_symm_t* d = &descs[r];
+    int rc = check_symm(d, counts, offsets, ctas);
+    if (rc != HET_OK) return rc;
+    if (d->nranks != nranks || d->rank != r || d->mc_base)
+      return fail(HET_EARG, "het_symm_virtual: descriptor %d is not rank %d of %d (no multicast)",
+                  r, r, nranks);
+    std::memset(&host[r], 0, sizeof(VRank));
+    Args a{*d, off, counts[r], offsets[r], epoch, channel, op == HET_OP_AG ? 1 : end_barrier,
+           -1, -1, 0, 0, 0, 0, g_spin_timeout_ns};
+    if (op == HET_OP_AG && policy == HET_SYMM_RELAY) relay_plan(d, counts, offsets, off, &a);
+    host[r].a = a;
+    if (helpers) {
+      fill_hargs(hp, r, counts, offsets, ctas, &host[r].h);
+      host[r].h.stage_off = op == HET_OP_RS_BF16 ? stage_off : off;
+    }
+    host[r].src = srcs[r];
+    host[r].out = outs[r];
+  }
+  Weights wt{};
+  if (weights)
+    for (int j = 0; j < nranks; ++j) wt.w[j] = weights[j];
+  const int kind = op == HET_OP_AG ? (helpers ? kVAgHelp : kVAg)
+                                   : (helpers ? kVRsHelp : (op == HET_OP_RS ? kVRs : kVRs16));
+  const bool bf16 = op == HET_OP_RS_BF16;
+  void* kern = nullptr;
+#define HET_VK(K, NRV, B) reinterpret_cast<void*>(symm_virtual_kernel<K, NRV, B>)
+#define HET_VK_NR(K, B)                                                              \
+  (nranks == 2 ? HET_VK(K, 2, B) : nranks == 4 ? HET_VK(K, 4, B)                     \
+   : nranks == 8 ? HET_VK(K, 8, B) : HET_VK(K, 0, B))
+  switch (kind) {
+    case kVAg: kern = HET_VK_NR(kVAg, false); break;
+    case kVAgHelp: kern = HET_VK_NR(kVAgHelp, false); break;
+    case kVRs: kern = HET_VK_NR(kVRs, false); break;
+    case kVRs16: kern = HET_VK_NR(kVRs16, false); break;
+    default: kern = bf16 ? HET_VK_NR(kVRsHelp, true) : HET_VK_NR(kVRsHelp, false);
+  }
+#undef HET_VK_NR
+#undef HET_VK
+  // every CTA of the grid must be co-resident: refuse instead of risking a wait
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  const int grid = nranks * ctas;
+  if (grid > per_sm * sms)
+    return fail(HET_EARG, "het_symm_virtual: %d CTAs exceed the %d co-resident (%d per SM)",
+                grid, per_sm * sms, per_sm);
+  VRank* dv = nullptr;
+  if (cudaMalloc(&dv, sizeof(VRank) * nranks) != cudaSuccess)
+    return fail(HET_ECUDA, "het_symm_virtual: %s", cudaGetErrorString(cudaGetLastError()));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(dv, host, sizeof(VRank) * nranks, cudaMemcpyHostToDevice, st);
+  int c = ctas;
+  void* args[] = {&dv, &c, &wt};
+  if (e == cudaSuccess)
+    e = cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args, 0, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // test support: synchronous
+  cudaFree(dv);
+  if (e != cudaSuccess) return fail(HET_ECUDA, "het_symm_virtual: %s", cudaGetErrorString(e));
+  return HET_OK;
 }
 
 int het_symm_status_async(int32_t* dst, void* stream) {

@@ -39,7 +39,8 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
            "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi",
            "het_embedding_grad_dev", "het_adamw_coef", "het_adamw_devcoef",
-           "het_symm_status_async", "het_probe_smid", "het_symm_helper_plan")
+           "het_symm_status_async", "het_probe_smid", "het_symm_helper_plan",
+           "het_symm_virtual")
 
 
 class HetSeg(ctypes.Structure):
@@ -121,6 +122,10 @@ def load(build: bool = False) -> ctypes.CDLL:
                                           ctypes.POINTER(i64), ctypes.POINTER(i64),
                                           ctypes.POINTER(f32), ctypes.c_uint32, i32, i32, i32,
                                           ctypes.c_uint64, i32, vp], i32),
+        "het_symm_virtual": ([i32, i32, ctypes.POINTER(HetSymm), ctypes.POINTER(vp),
+                              ctypes.POINTER(vp), ctypes.POINTER(i64), ctypes.POINTER(i64),
+                              ctypes.c_uint64, ctypes.POINTER(f32), ctypes.c_uint32, i32, i32,
+                              i32, ctypes.c_uint64, i32, vp], i32),
         "het_symm_helper_plan": ([i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                   ctypes.c_uint64, ctypes.POINTER(i64),
                                   ctypes.POINTER(ctypes.c_int32), i32,

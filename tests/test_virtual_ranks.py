@@ -1,6 +1,6 @@
 """Parity of the fused uneven collectives at N = 2, 4 and 8 ranks on ONE GPU.
 
-The virtual-rank harness (tests/vranks.py) runs N concurrent instances of
+The virtual-rank harness (tests/vranks.py) runs N ranks, as one cooperative launch, of
 het_symm_allgather_pack / het_symm_reduce_scatter / het_symm_reduce_scatter_bf16
 over N copies of the symmetric buffer in one allocation, so the 1-GPU test
 run proves the rank-count specialisations (NR = 2, 4, 8), the peer and relay
@@ -24,7 +24,9 @@ order) and within 1e-5 of oracle.reduce_scatter (fp64 sum); bf16-wire
 reduce-scatter bit-exact vs oracle.reduce_scatter_bf16. het_symm_status
 must stay 0 (no barrier timed out).
 
-The multicast (NVLS) route needs N real GPUs; tests/test_multigpu.py covers it.
+All N ranks of a collective run as ONE cooperative launch (het_symm_virtual),
+so every CTA that waits on another is co-resident by construction. The
+multicast (NVLS) route needs N real GPUs; tests/test_multigpu.py covers it.
 """
 from __future__ import annotations
 
@@ -176,26 +178,34 @@ def test_virtual_ranks_planner_shapes_n8(cuda, name):
 
 
 def test_missing_rank_times_out_and_is_reported(cuda):
-    """Fault injection: rank 1 never joins the all-gather. Rank 0's kernel must
-    give up after the (shortened) spin limit, the sticky status must say so,
-    and the asynchronous StatusWatch the step driver uses must raise
-    CollectiveFault instead of letting the step train on its output."""
+    """Fault injection: rank 0 of a 2-rank all-gather is launched alone (the
+    real per-rank entry point, one launch) and rank 1 never joins. Rank 0's
+    kernel must give up after the (shortened) spin limit, the sticky status
+    must say so, and the asynchronous StatusWatch the step driver uses must
+    raise CollectiveFault instead of letting the step train on its output."""
+    import ctypes
     vg = VirtualGroup(2, [("unit", 4096, torch.bfloat16)], cuda)
     counts = [2048, 2048]
     src = [torch.randn(2048, device=cuda) for _ in range(2)]
     watch = K.StatusWatch()
+    lib = K.load()
     K.set_symm_timeout_ms(200)
     try:
         t0 = time.time()
-        vg.allgather_pack(src, "unit", 0, counts, [0, 2048], ranks=[0])
-        assert time.time() - t0 < 5.0
+        K._check(lib.het_symm_allgather_pack(ctypes.byref(vg.desc[0]), src[0].data_ptr(),
+                                             vg.offsets["unit"], K._i64(counts),
+                                             K._i64([0, 2048]), 1, 0, K.SYMM_PEER, 4,
+                                             torch.cuda.current_stream().cuda_stream),
+                 "het_symm_allgather_pack")
         watch.record(torch.cuda.current_stream(), "step 7")
         with pytest.raises(K.CollectiveFault, match="step 7"):
             watch.check()
+        assert time.time() - t0 < 5.0
         assert K.SymmWorkspace.status(reset=True) == K.HET_SYMM_TIMEOUT
     finally:
         K.set_symm_timeout_ms(10_000)
-    # a clean call afterwards reports 0
+    # a clean collective afterwards (both ranks, one cooperative launch) reports 0
+    vg.epoch[0] = 1
     vg.allgather_pack(src, "unit", 0, counts, [0, 2048])
     watch.record(torch.cuda.current_stream(), "step 8")
     watch.check()

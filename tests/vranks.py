@@ -3,16 +3,13 @@
 The fused kernels (csrc/hetstep_symm.cu) address every rank's copy of the
 symmetric buffer through ``het_symm_t.peer_base[j]``; they never ask where
 that memory lives. Here one allocation holds N equal copies (rank j's copy at
-``base + j * stride``), N descriptors differ only in ``rank``, and rank r's
-kernel is launched on its own stream. The N launches run concurrently, meet
-at the same in-kernel CTA-pairwise barriers as on N GPUs (peer stores and
-loads are plain HBM accesses here), and produce the same bytes, so the
-driver's 1-GPU test run exercises the NR = 2 / 4 / 8 specialisations, the
-peer and relay all-gathers and both reduce-scatters against the oracle.
-
-Co-residency: every barrier needs CTA b of all N launches resident at once.
-``ctas * N`` is kept below one CTA per SM (148), so they always are, and the
-barriers cannot time out unless a rank is deliberately left out.
+``base + j * stride``) and N descriptors differ only in ``rank``. All N ranks
+run as ONE cooperative launch (``het_symm_virtual``: CTA b of rank r at
+blockIdx r * ctas + b, the same kernel bodies and in-kernel barriers as N real
+launches), so every CTA is co-resident by construction -- kernels that wait on
+one another are never separate launches on one GPU (B200_PROFILING.md). The
+driver's 1-GPU test run thereby exercises the NR = 2 / 4 / 8 specialisations,
+the peer, relay and helper routes and both reduce-scatters against the oracle.
 
 This is test infrastructure (it measures nothing: a "link" is local HBM).
 """
@@ -55,12 +52,9 @@ class VirtualGroup:
             d.mc_base = 0                       # one GPU: no NVLS multicast object
             d.signal_off = self.signal_off
             self.desc.append(d)
-        # one CTA per SM at most across all virtual ranks (co-residency of every barrier)
+        # one cooperative grid of n * ctas CTAs (het_symm_virtual refuses more than fit)
         sms = torch.cuda.get_device_properties(device).multi_processor_count
-        self.ctas = ctas if ctas is not None else max(1, min(32, (sms - 4) // n))
-        if self.ctas * n > sms:
-            raise ValueError("ctas * n exceeds one CTA per SM: barriers could deadlock")
-        self.streams = [torch.cuda.Stream(device=device) for _ in range(n)]
+        self.ctas = ctas if ctas is not None else max(1, min(32, sms // n))
         self.epoch = [0, 0]
         torch.cuda.synchronize(device)
 
@@ -73,138 +67,41 @@ class VirtualGroup:
                                        dtype)
         raise KeyError(name)
 
-    def _launch(self, fn, ranks) -> None:
-        torch.cuda.synchronize(self.device)     # inputs written on the default stream
-        for r in ranks:
-            fn(r, self.streams[r].cuda_stream)
+    def _run(self, op: int, region: str, byte_off: int, srcs, outs, counts, offsets,
+             weights=None, channel: int = 0, end_barrier: bool = True,
+             policy: int = K.SYMM_AUTO, stage_off: int = 0) -> None:
+        lib, n = K.load(), self.n
+        self.epoch[channel] += 1
+        descs = (K.HetSymm * n)(*self.desc)
+        src_p = (ctypes.c_void_p * n)(*[(t.data_ptr() if t is not None and t.numel() else None)
+                                        for t in srcs])
+        out_p = (ctypes.c_void_p * n)(*[(t.data_ptr() if t is not None and t.numel() else None)
+                                        for t in outs])
+        w = (ctypes.c_float * n)(*[float(x) for x in weights]) if weights is not None else None
         torch.cuda.synchronize(self.device)
+        K._check(lib.het_symm_virtual(op, n, descs, src_p, out_p, K._i64(counts), K._i64(offsets),
+                                      byte_off, w, self.epoch[channel], channel,
+                                      int(end_barrier), int(policy), int(stage_off), self.ctas,
+                                      torch.cuda.current_stream(self.device).cuda_stream),
+                 "het_symm_virtual")
 
     def allgather_pack(self, srcs: Sequence[torch.Tensor], region: str, elem_off: int,
-                       counts: Sequence[int], offsets: Sequence[int], policy: int = K.SYMM_AUTO,
-                       ranks: Sequence[int] | None = None) -> None:
-        self.epoch[0] += 1
-        lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
-        byte_off = self.offsets[region] + 2 * elem_off
-
-        def go(r, st):
-            src = srcs[r].data_ptr() if srcs[r].numel() else None
-            K._check(lib.het_symm_allgather_pack(ctypes.byref(self.desc[r]), src, byte_off, c, o,
-                                                 self.epoch[0], 0, policy, self.ctas, st),
-                     "het_symm_allgather_pack")
-        self._launch(go, range(self.n) if ranks is None else ranks)
+                       counts: Sequence[int], offsets: Sequence[int], policy: int = K.SYMM_AUTO
+                       ) -> None:
+        self._run(K.OP_AG, region, self.offsets[region] + 2 * elem_off, srcs, [None] * self.n,
+                  counts, offsets, channel=0, policy=policy)
 
     def reduce_scatter(self, region: str, elem_off: int, outs: Sequence[torch.Tensor],
                        counts: Sequence[int], offsets: Sequence[int], end_barrier: bool = True,
                        policy: int = K.SYMM_AUTO) -> None:
-        self.epoch[1] += 1
-        lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
-        byte_off = self.offsets[region] + 4 * elem_off
-
-        def go(r, st):
-            out = outs[r].data_ptr() if outs[r].numel() else None
-            K._check(lib.het_symm_reduce_scatter(ctypes.byref(self.desc[r]), byte_off, out, c, o,
-                                                 self.epoch[1], 1, int(end_barrier), policy,
-                                                 self.ctas, st),
-                     "het_symm_reduce_scatter")
-        self._launch(go, range(self.n))
+        self._run(K.OP_RS, region, self.offsets[region] + 4 * elem_off, [None] * self.n, outs,
+                  counts, offsets, channel=1, end_barrier=end_barrier, policy=policy)
 
     def reduce_scatter_bf16(self, region: str, elem_off: int, outs: Sequence[torch.Tensor],
                             counts: Sequence[int], offsets: Sequence[int],
                             weights: Sequence[float], end_barrier: bool = True,
                             policy: int = K.SYMM_AUTO, stage: str | None = None) -> None:
-        self.epoch[1] += 1
-        lib, c, o = K.load(), K._i64(counts), K._i64(offsets)
-        byte_off = self.offsets[region] + 2 * elem_off
         stage_off = self.offsets[stage] + 4 * elem_off if stage is not None else 0
-        w = (ctypes.c_float * len(weights))(*[float(x) for x in weights])
-
-        def go(r, st):
-            out = outs[r].data_ptr() if outs[r].numel() else None
-            K._check(lib.het_symm_reduce_scatter_bf16(ctypes.byref(self.desc[r]), byte_off, out,
-                                                      c, o, w, self.epoch[1], 1,
-                                                      int(end_barrier), policy, stage_off,
-                                                      self.ctas, st),
-                     "het_symm_reduce_scatter_bf16")
-        self._launch(go, range(self.n))
-
-
-# ---------------------------------------------------------------------------
-# virtual ranks of the whole train step: N trainers in N threads on one GPU
-
-class VirtualRankGroup:
-    """Host-side agreement of N trainers running in N threads of one process
-    (the step's DistGroup stand-in): sum_ranks is a barrier + shared sum."""
-
-    def __init__(self, n: int, timeout: float = 300.0):
-        import threading
-        self.n = n
-        # a rank that dies breaks the barrier for the others instead of hanging them
-        self._bar = threading.Barrier(n, timeout=timeout)
-        self._lock = threading.Lock()
-        self._vals: list[int] = []
-        self._out = 0
-
-    def sum_ranks(self, value: int) -> int:
-        with self._lock:
-            self._vals.append(int(value))
-        if self._bar.wait() == 0:
-            with self._lock:
-                self._out = sum(self._vals)
-                self._vals = []
-        self._bar.wait()
-        return self._out
-
-    def barrier(self) -> None:
-        self._bar.wait()
-
-
-class _Handle:
-    def __init__(self, group: VirtualRankGroup, device):
-        self.group, self.device = group, device
-
-    def barrier(self) -> None:
-        torch.cuda.current_stream(self.device).synchronize()
-        self.group.barrier()
-
-
-class VirtualSymmWorkspace(K.SymmWorkspace):
-    """Rank r's view of a VirtualGroup allocation, with SymmWorkspace's methods:
-    the trainer issues the same fused kernels as on N GPUs (peer route; no NVLS
-    multicast object on one GPU)."""
-
-    def __init__(self, vg: VirtualGroup, rank: int, group: VirtualRankGroup,
-                 policy: int = K.SYMM_AUTO):
-        self.offsets = dict(vg.offsets)
-        self.signal_off = vg.signal_off
-        self.multicast = False
-        self.desc = vg.desc[rank]
-        self.views = {name: vg.view(rank, name) for name, _, _ in vg.regions}
-        self.epoch = [0, 0]
-        self.ctas = vg.ctas
-        self.policy = policy
-        self.handle = _Handle(group, vg.device)
-
-
-def run_ranks(n: int, fn, group: VirtualRankGroup | None = None) -> list:
-    """fn(r) for r in 0..n-1 in n threads; re-raises the first exception (a
-    failing rank aborts the group's barrier so the others fail too)."""
-    import threading
-    out, err = [None] * n, [None] * n
-
-    def body(r):
-        try:
-            out[r] = fn(r)
-        except BaseException as e:          # noqa: BLE001 (reported below)
-            err[r] = e
-            if group is not None:
-                group._bar.abort()
-
-    ts = [threading.Thread(target=body, args=(r,)) for r in range(n)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    for e in err:
-        if e is not None:
-            raise e
-    return out
+        self._run(K.OP_RS_BF16, region, self.offsets[region] + 2 * elem_off, [None] * self.n,
+                  outs, counts, offsets, weights=weights, channel=1, end_barrier=end_barrier,
+                  policy=policy, stage_off=stage_off)

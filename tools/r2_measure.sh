@@ -6,6 +6,8 @@ set -u
 OUT=gpurun_out/r2
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python -m pytest tests/test_virtual_ranks.py -q -m gpu > $OUT/pytest_virtual_ranks.log 2>&1
+echo "virtual ranks rc=$?"
 N=$(python -c "import torch; print(torch.cuda.device_count())")
 echo "gpus $N"
 run() {   # run <nproc> <port> <script> args...
@@ -26,6 +28,8 @@ for c in gpt2_small bert_large llama_1b3; do
 done
 timeout 900 python -m pytest tests/test_multigpu.py -q -m gpu > $OUT/pytest_mgpu_n$N.log 2>&1
 echo "mgpu n$N rc=$?"
+timeout 1500 python -m pytest tests/test_multigpu_configs.py -q -m gpu -s > $OUT/pytest_mgpu_configs_n$N.log 2>&1
+echo "mgpu configs n$N rc=$?"
 if [ "$N" -ge 4 ]; then
   export CUDA_VISIBLE_DEVICES=0,1
   timeout 300 bash -c "$(declare -f run); run 2 29604 tools/nvlink_peak.py" > $OUT/nvlink_peak_n2.json 2> $OUT/nvlink_peak_n2.err
