@@ -211,6 +211,33 @@ def main(out_dir: str) -> None:
             del t2
         report["symm_status_pair"] = float(K.SymmWorkspace.status(reset=True))
 
+        # odd block count in pair mode: a 3-block model's last group is
+        # unit 0 alone, whose accumulate must wait for RS(1)'s end barrier too
+        from paper_2411_01075_b200.model import ArchSpec
+        arch3 = ArchSpec("tiny_gpt3", "gpt", d=256, layers=3, heads=4, ffn=1024, vocab=4096,
+                         seq=128)
+        m3 = ModelSpec(arch3.layers, arch3.unit_params, pB)
+        plan3 = TrainPlan(tuple(GpuAssignment(f"g{i}", m, l, m * l, r, 0.0, r * m3.state_bytes)
+                                for i, ((m, l), r) in enumerate(zip(pmicro, ratios))),
+                          1.0, 1.0, 2.0 * arch3.layers, True, assign_unit_shards(ratios, m3))
+        units3 = []
+        for u in range(arch3.layers + 1):
+            g3 = torch.Generator().manual_seed(71 + u)
+            units3.append(init_flat(arch3.root_layout() if u == arch3.layers else
+                                    arch3.unit_layout(), g3, "cpu"))
+        tok3 = rank_tokens(plan3, rank, arch3.seq, arch3.vocab, seed=17, step=0)
+        t3 = UnevenFSDPTrainer(arch3, plan3, rank, comm_ag=cag, comm_rs=crs, device=dev,
+                               algo=K.ALGO_SYMM)
+        report["odd_pair_mode"] = float(t3.pair_units and t3.L.blocks % 2 == 1)
+        t3.load_full_units(units3)
+        t3.step(torch.from_numpy(tok3).to(dev))
+        g3full = [t.cpu().numpy() for t in t3.full_units("g32")]
+        for _ in range(2):                   # more steps: no barrier fault either
+            t3.step(torch.from_numpy(tok3).to(dev))
+        t3.check_faults()
+        report["symm_status_odd"] = float(K.SymmWorkspace.status(reset=True))
+        del t3
+
         stage(rank, "fault injection")
         # fault injection: rank 0 enters a fused all-gather that no other rank joins
         # (shortened spin limit). Its barrier times out; the trainer's asynchronous
@@ -249,7 +276,8 @@ def main(out_dir: str) -> None:
                  **{f"ps{u}": x for u, x in enumerate(ps)},
                  **{f"gw{u}": x for u, x in enumerate(pair[True])},
                  **{f"gf{u}": x for u, x in enumerate(pair[False])},
-                 pmicro=np.array(pmicro))
+                 pmicro=np.array(pmicro),
+                 **{f"g3_{u}": x for u, x in enumerate(g3full)})
     finally:
         stage(rank, "teardown")
         cag.close()

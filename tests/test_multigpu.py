@@ -53,6 +53,8 @@ def test_multigpu_collectives_and_step(tmp_path):
                 assert v > 0, "the l<=1 plan did not use the bf16-wire reduce-scatter"
             elif k == "symm_route_check_ok":
                 assert v == 1.0, "fused collectives failed their startup known-answer check"
+            elif k == "odd_pair_mode":
+                assert v == 1.0, "the 3-block case did not run in pair mode"
             elif k == "fault_raised":
                 assert v == 1.0, "a fused-collective timeout was not raised as CollectiveFault"
             elif k == "trace_lint_problems":
@@ -106,3 +108,22 @@ def test_multigpu_collectives_and_step(tmp_path):
         gw, gf = r[0][f"gw{u}"], r[0][f"gf{u}"]
         assert norm_rel(gw, gf) <= 1e-6, f"bf16 wire vs fp32 wire, unit {u}"
         assert norm_rel(gw, ref.numpy()) <= BF16_GRAD_RTOL, f"bf16 wire vs oracle, unit {u}"
+    # 3 blocks in pair mode (odd block count: the last group is unit 0 alone)
+    from paper_2411_01075_b200.model import ArchSpec
+    arch3 = ArchSpec("tiny_gpt3", "gpt", d=256, layers=3, heads=4, ffn=1024, vocab=4096, seq=128)
+    m3 = ModelSpec(arch3.layers, arch3.unit_params, pB)
+    plan3 = TrainPlan(tuple(GpuAssignment(f"g{i}", m, l, m * l, rr, 0.0, rr * m3.state_bytes)
+                            for i, ((m, l), rr) in enumerate(zip(pmicro, ratios))),
+                      1.0, 1.0, 2.0 * arch3.layers, True, assign_unit_shards(ratios, m3))
+    units3 = []
+    for u in range(arch3.layers + 1):
+        g = torch.Generator().manual_seed(71 + u)
+        units3.append(init_flat(arch3.root_layout() if u == arch3.layers else
+                                arch3.unit_layout(), g, "cpu"))
+    toks3 = [rank_tokens(plan3, i, arch3.seq, arch3.vocab, seed=17, step=0) for i in range(world)]
+    live3 = [(t, mi) for t, mi in zip(toks3, pmicro) if mi[0] > 0]
+    g3u, g3r, _ = MO.weighted_gradient(arch3, units3[:-1], units3[-1], [t for t, _ in live3],
+                                       [mi for _, mi in live3])
+    for u, ref in enumerate(g3u + [g3r]):
+        assert norm_rel(r[0][f"g3_{u}"], ref.numpy()) <= BF16_GRAD_RTOL, f"3-block unit {u}"
+
