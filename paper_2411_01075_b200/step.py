@@ -209,6 +209,10 @@ class UnevenFSDPTrainer:
         # straight into its slot of the symmetric staging buffer gb{u % 2}
         # (hetstep.grad_destinations), so no het_gather_bf16 copy follows
         self.grad_in_place = True
+        # N > 1: AdamW of each unit's shard runs on the RS stream right after that
+        # unit's reduce-scatter (overlapping the rest of the backward) instead of
+        # one pass over the whole shard at the end of the step
+        self.overlap_adamw = self.N > 1
         # Eq. 1 weights of every rank (the bf16-wire reduce-scatter applies them itself)
         self.rank_weights = [a.microbatch / plan.total_batch for a in plan.assignments]
         self._set_routes(self.symm is not None)
@@ -557,7 +561,30 @@ class UnevenFSDPTrainer:
         self.rs_stream.wait_event(after)
         with self._span("reducescatter", u, 0, "bwd", self.rs_stream):
             self._rs_issue(u, src)
+        if self.overlap_adamw:
+            self._adamw_unit(u)
         return self._event(self.rs_stream)
+
+    def _adamw_unit(self, u: int) -> None:
+        """AdamW over unit u's (padded) local range on the RS stream, right behind
+        the unit's reduce-scatter: the optimizer of the early-reduced units runs
+        under the backward of the later ones instead of as one pass at the end of
+        the step. The pads are zero in p, g, m and v and stay zero."""
+        lo = self.L.local_off[u]
+        hi = self.L.local_off[u + 1] if u + 1 <= self.L.root else self.L.local_len
+        if hi <= lo:
+            return
+        shadow = self.p16[lo:hi] if self.need_shadow else None
+        a, b = self.timers.pair("adamw", (30.0 if self.need_shadow else 28.0) * (hi - lo))
+        if a is not None:
+            a.record(self.rs_stream)
+        K.adamw(self.p32[lo:hi], self.g32[lo:hi], self.m32[lo:hi], self.v32[lo:hi], shadow,
+                lr=self.opt.lr, beta1=self.opt.betas[0], beta2=self.opt.betas[1],
+                eps=self.opt.eps, weight_decay=self.opt.weight_decay, step=self.steps + 1,
+                stream=self.rs_stream)
+        if b is not None:
+            b.record(self.rs_stream)
+        self.launches += 1
 
     def _rs_issue(self, u: int, src: torch.Tensor) -> None:
         if self.wire16[u]:               # bf16 wire: weighting + cast inside the RS
@@ -1014,6 +1041,8 @@ class UnevenFSDPTrainer:
 
         # ---- optimizer -------------------------------------------------------
         self.steps += 1
+        if multi and self.overlap_adamw:       # already applied unit by unit (_adamw_unit)
+            return loss
         a, b = self.timers.pair("adamw", (30.0 if self.need_shadow else 28.0) *
                                 self.L.local_len)
         if a is not None:
