@@ -560,10 +560,13 @@ def main() -> None:
                          "step_share": kern[dom]["ms_total"] / steps_timed / ms},
             # model FLOPs (6 P T + attention, no recompute) per second against the
             # measured sustained dense bf16 peak: the step-level context of the line
+            # (whole job: the peak of all N GPUs; the emulated tiers use fewer SMs, so
+            # the per-full-B200-equivalent figure is frac * n_gpus / tier_capacity)
             "mfu": {"model_tflop_per_step": B * arch.model_flops_per_sample() / 1e12,
                     "achieved_tflops": B * arch.model_flops_per_sample() / (ms * 1e-3) / 1e12,
-                    "peak_tflops": bf16_peak,
-                    "frac": B * arch.model_flops_per_sample() / (ms * 1e-3) / 1e12 / bf16_peak},
+                    "peak_tflops": bf16_peak * world,
+                    "frac": B * arch.model_flops_per_sample() / (ms * 1e-3) / 1e12
+                    / (bf16_peak * world)},
             "kernels": {k: dict(v, ms_per_step=v["ms_total"] / steps_timed)
                         for k, v in kern.items()},
             "gpu_launches": launches,

@@ -1171,7 +1171,14 @@ void fill_hargs(const HelperPlan& hp, int rank, const int64_t* counts, const int
       h->help_offset[j] = offsets[hp.owner[k]];
     }
   }
-  h->gran = static_cast<int>((kmax + 3999) / 4000);
+  // iterations per progress signal: at most 4000 signals (the epoch * 4096 + k
+  // encoding); HET_HELPER_GRAN forces a coarser hand-off for measurement sweeps
+  static const int forced = [] {
+    const char* e = getenv("HET_HELPER_GRAN");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t fine = (kmax + 3999) / 4000;
+  h->gran = static_cast<int>(forced > fine ? forced : fine);
 }
 
 // Body-vector counts of every rank's range (AG: bf16 at unit_off; RS: fp32 or

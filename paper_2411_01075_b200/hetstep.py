@@ -995,10 +995,12 @@ def reduce_scatter_uneven(src: torch.Tensor, shard: torch.Tensor, counts: Sequen
 # ---------------------------------------------------------------------------
 # route table
 
-# HET_SYMM_HELPERS routes for skewed units at N >= 3 (off: HET_HELPERS=0, which
-# restores the round-1 table: NCCL for near-single-owner units at N >= 4)
+# HET_SYMM_HELPERS routes for skewed units at N >= 3: opt-in (HET_HELPERS=1). At
+# N=4, 1 GB they measured below NCCL's rings on single-owner units (AG 418 vs 669,
+# RS 445 vs 665 GB/s) and below the pair relay / multicast on the other skews
+# (profiles/r2/summary.md), so the default table keeps round 1's choices.
 import os as _os
-HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "1") != "0"
+HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "0") == "1"
 # NVLS multicast stores / ld_reduce reach a smaller share of the link than peer
 # stores / loads: single-owner AG at N=4, 1 GB, round 1: multicast 554 GB/s against
 # 660-700 for the peer-class routes (profiles/r1_collectives_n4*.jsonl)
@@ -1082,6 +1084,11 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
         # the helper routes move S (not (N-1) S) over the owner's link: fused for
         # every shape (the reduce-scatter of very large skewed units included)
         return "symm"
+    if op == "rs16":
+        # bf16 wire (weights + cast in the RS, half the link bytes): fused except
+        # near-single-owner units at N >= 4, where NCCL's fp32 ring reduce measured
+        # 665 against the wire's 507 fp32-equivalent GB/s (profiles/r2/summary.md)
+        return "nccl" if owner_like else "symm"
     if op == "ag":
         return "nccl" if owner_like else "symm"
     if op == "rs":

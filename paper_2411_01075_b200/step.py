@@ -614,6 +614,10 @@ class UnevenFSDPTrainer:
             return self.p16[off:off + self.L.unit_size(u)]
         return self.rbuf if u == self.L.root else self.ubuf[u % 2]
 
+    def _zero_acc(self, u: int) -> None:
+        K.fill(self._acc(u), 0.0)
+        self.launches += 1
+
     def _acc(self, u: int) -> torch.Tensor:
         if self.N == 1:
             return self._local(self.g32, u)
@@ -1004,11 +1008,18 @@ class UnevenFSDPTrainer:
                 else:
                     dy[k] = grads[-1]
                 del grads, y, x, g_in
+            if multi and nmb == 0 and not self.wire16[u]:
+                # an idle rank contributes zeros; its acc may hold a helper
+                # reduce-scatter's staged sums from the last use of this buffer
+                for ev_ in acc_free:
+                    comp.wait_event(ev_)
+                acc_free = []
+                self._zero_acc(u)
             done_ev[u] = self._event(comp)
             if off and not deep:
                 self._pf_free[u % 2] = done_ev[u]    # staging slot of unit u reusable
             if not self.pair_units:
-                if multi:                            # an idle rank's acc holds zeros
+                if multi:
                     rs_ev[u] = self._rs(u, acc, done_ev[u])
                 continue
             pending.append((u, unit_grads if mb else []))   # idle ranks still reduce-scatter
@@ -1026,6 +1037,10 @@ class UnevenFSDPTrainer:
                             comp.wait_event(rs_ev[w_])
             if mb:
                 self._accumulate_units([p for p in pending if p[1]], unit_names, self.unit_seg)
+            elif multi:              # idle rank: zeros (helpers may have staged sums there)
+                for v, _ in pending:
+                    if not self.wire16[v]:
+                        self._zero_acc(v)
             ev = self._event(comp)
             if multi:
                 for v, _ in pending:
