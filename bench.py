@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import argparse
 import contextlib
+import gc
 import json
 import os
 import statistics
@@ -414,6 +415,10 @@ def main() -> None:
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # rank 0 samples its GPU (the line reports rank 0's clocks); one NVML poller
     # per node instead of one per rank keeps driver calls off the other ranks
+    # no collector pauses inside the timed loops (the host enqueues the eager
+    # multi-rank steps; a GC pause there shows up as an idle GPU)
+    gc.collect()
+    gc.disable()
     with (sampler if rank == 0 else contextlib.nullcontext(None)) as clocks:
         barrier()
         t0.record(comp)
@@ -452,6 +457,7 @@ def main() -> None:
     barrier()
     tr.check_faults()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    gc.enable()
     trace_report = None
     if args.trace_dir:
         from paper_2411_01075_b200 import trace as T
@@ -543,7 +549,11 @@ def main() -> None:
                        # the reference's crosscheck_optimizer (sim.py:445-452) against the
                        # measured step instead of the simulator
                        "crosscheck": {"predicted_ms": xc.predicted_ms, "measured_ms": xc.measured_ms,
-                                      "rel_error": xc.rel_error},
+                                      "rel_error": xc.rel_error,
+                                      "measured_median_ms": statistics.median(step_ms),
+                                      "rel_error_median": abs(statistics.median(step_ms)
+                                                              - xc.predicted_ms)
+                                      / statistics.median(step_ms)},
                        "parallelism": f"uneven-fsdp{world}",
                        "emulation_rank0": emu.describe(),
                        # sum over ranks of the emulated tiers' SM fractions (N=1: 1.0);
