@@ -329,6 +329,8 @@ def main() -> None:
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as one CUDA graph (auto: on where eligible: "
                          "one rank, no activation offload)")
+    ap.add_argument("--symm-ctas", type=int, default=64,
+                    help="CTAs per fused collective launch (each holds one SM while it runs)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
                     help="collective route for N>1: 4 = fused symmetric-memory kernels "
                          "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")
@@ -356,7 +358,7 @@ def main() -> None:
     tr = UnevenFSDPTrainer(job.arch, job.plan, rank, comm_ag=comm_ag, comm_rs=comm_rs, opt=OPT,
                            device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO,
                            offload_activations=offload,
-                           offload_schedule=args.offload_schedule)
+                           offload_schedule=args.offload_schedule, symm_ctas=args.symm_ctas)
     tr.init_params(seed=0)
     # a memory-capped rank runs its head in row chunks so the [rows, vocab]
     # logits transient stays within 10% of its emulated HBM
@@ -560,6 +562,7 @@ def main() -> None:
                        # value / tier_capacity is the throughput per full-B200 equivalent
                        "tier_capacity": tier_capacity(job, args.no_emulate),
                        "collectives": route_summary(tr),
+                       "symm_ctas": args.symm_ctas,
                        "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": tok_bytes, "d2h_bytes_per_step": 4 * world},

@@ -752,15 +752,24 @@ __device__ __forceinline__ void rs_geometry(uint64_t data_off, int64_t offset, i
 template <int NR, bool BF16>
 struct RsVec {
   static constexpr int VE = BF16 ? 8 : 4;
+  static constexpr int kMaxR = NR > 0 ? NR : HET_MAX_RANKS;
   float r[VE];
-  __device__ __forceinline__ void reduce(const uint64_t* peer, int nr, uint64_t byte_off,
-                                         const Weights& wt) {
-    constexpr int kMaxR = NR > 0 ? NR : HET_MAX_RANKS;
-    uint4 x[kMaxR];
+  uint4 x[kMaxR];
+  // issue the N peer loads of one vector (the caller batches several vectors'
+  // loads before any combine, for memory-level parallelism)
+  __device__ __forceinline__ void load(const uint64_t* peer, int nr, uint64_t byte_off,
+                                       const Weights& wt) {
 #pragma unroll
     for (int p = 0; p < kMaxR; ++p)
       if (p < nr && (!BF16 || wt.w[p] != 0.f))
         x[p] = __ldcg(reinterpret_cast<const uint4*>(peer[p] + byte_off));
+  }
+  __device__ __forceinline__ void reduce(const uint64_t* peer, int nr, uint64_t byte_off,
+                                         const Weights& wt) {
+    load(peer, nr, byte_off, wt);
+    combine(nr, wt);
+  }
+  __device__ __forceinline__ void combine(int nr, const Weights& wt) {
 #pragma unroll
     for (int i = 0; i < VE; ++i) r[i] = 0.f;
     bool first = true;
@@ -812,14 +821,30 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
       rs_geometry<BF16>(a.data_off, h.help_offset[q], h.help_count[q], &head, &nv);
       const int64_t lo = h.help_lo[q] + k * per_iter;
       const int64_t hi = lo + per_iter < h.help_hi[q] ? lo + per_iter : h.help_hi[q];
-      for (int64_t v = lo + gtid; v < hi; v += gsz) {
-        const int64_t e = h.help_offset[q] + head + v * VE;      // unit element
-        RsVec<NR, BF16> rv;
-        rv.reduce(peer, nr, a.data_off + static_cast<uint64_t>(e) * ES, wt);
-        float4* st = reinterpret_cast<float4*>(peer[s.rank] + h.stage_off +
-                                               static_cast<uint64_t>(e) * 4);
-        __stcg(st, make_float4(rv.r[0], rv.r[1], rv.r[2], rv.r[3]));
-        if (BF16) __stcg(st + 1, make_float4(rv.r[4 % VE], rv.r[5 % VE], rv.r[6 % VE], rv.r[7 % VE]));
+      // kB vectors' N loads in flight per thread before any combine
+      constexpr int kB = NR > 0 ? (16 / NR > 2 ? 16 / NR : 2) : 2;
+      for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kB) {
+        RsVec<NR, BF16> rv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int64_t v = v0 + u * gsz;
+          if (v < hi)
+            rv[u].load(peer, nr, a.data_off + static_cast<uint64_t>(
+                                     h.help_offset[q] + head + v * VE) * ES, wt);
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int64_t v = v0 + u * gsz;
+          if (v >= hi) continue;
+          rv[u].combine(nr, wt);
+          const int64_t e = h.help_offset[q] + head + v * VE;      // unit element
+          float4* st = reinterpret_cast<float4*>(peer[s.rank] + h.stage_off +
+                                                 static_cast<uint64_t>(e) * 4);
+          __stcg(st, make_float4(rv[u].r[0], rv[u].r[1], rv[u].r[2], rv[u].r[3]));
+          if (BF16)
+            __stcg(st + 1, make_float4(rv[u].r[4 % VE], rv[u].r[5 % VE], rv[u].r[6 % VE],
+                                       rv[u].r[7 % VE]));
+        }
       }
       if ((k + 1) % h.gran == 0 || k + 1 == kq)
         signal_progress(peer[h.help_peer[q]], s, a.channel, progress(a.epoch, k, h.gran));
@@ -1177,8 +1202,12 @@ void fill_hargs(const HelperPlan& hp, int rank, const int64_t* counts, const int
     const char* e = getenv("HET_HELPER_GRAN");
     return e ? atoi(e) : 0;
   }();
+  // Default 4 iterations per hand-off: every signal drains the CTA's remote
+  // stores (release fence), and per-iteration signals held the single-owner AG
+  // at N=4 to 421 GB/s against 627 with 4 (profiles/r2/helpers_c128_g*.jsonl).
   const int64_t fine = (kmax + 3999) / 4000;
-  h->gran = static_cast<int>(forced > fine ? forced : fine);
+  const int64_t want = forced > 0 ? forced : 4;
+  h->gran = static_cast<int>(want > fine ? want : fine);
 }
 
 // Body-vector counts of every rank's range (AG: bf16 at unit_off; RS: fp32 or
