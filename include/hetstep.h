@@ -323,6 +323,20 @@ int het_symm_status(int reset);
  * sync, and raises instead of training on unsynchronised gradients. */
 int het_symm_status_async(int32_t* dst, void* stream);
 
+/* Device-resident barrier epochs, for a CUDA graph that replays a multi-rank
+ * step (no host counter can change inside a replay). An epoch argument with
+ * HET_SYMM_EPOCH_DEVICE set means base[channel] + (epoch & ~FLAG), base being
+ * a counter in this rank's signal area (after the barrier slots, inside
+ * het_symm_signal_bytes()). het_symm_epoch_set seeds it (from the host
+ * counter, before capture); het_symm_epoch_add(delta = the channel's launches
+ * per step), queued after the step's last collective of that channel and
+ * captured with it, advances it every replay. Both are one-thread kernels on
+ * `stream`. Every rank issues the same epoch sequence whether it replays a
+ * graph or runs eagerly with host epochs. */
+#define HET_SYMM_EPOCH_DEVICE 0x80000000u
+int het_symm_epoch_set(const het_symm_t* s, int channel, uint32_t value, void* stream);
+int het_symm_epoch_add(const het_symm_t* s, int channel, uint32_t delta, void* stream);
+
 /* (1)+(2) fused: rank r rounds its fp32 master range src[0:counts[r]] to bf16
  * and stores it at unit_off + 2*offsets[r] on EVERY rank with one multicast
  * store (NVLS) or per-peer stores. In-kernel start/end barriers; `epoch`

@@ -133,6 +133,34 @@ __device__ __forceinline__ void wait_epoch(const uint32_t* p, uint32_t epoch, ui
   }
 }
 
+// Device-resident barrier epochs (CUDA-graph replay of a multi-rank step): the
+// rank's base epoch per channel lives in its own signal area, right after the
+// barrier slots. A launch whose epoch has HET_SYMM_EPOCH_DEVICE set runs at
+// base[channel] + (epoch & ~HET_SYMM_EPOCH_DEVICE); het_symm_epoch_add advances
+// the base, stream-ordered after the channel's last launch of the step, so the
+// same captured arguments yield fresh epochs on every replay.
+__host__ __device__ constexpr uint64_t slot_bytes() {
+  return static_cast<uint64_t>(HET_SYMM_CHANNELS) * kKinds * kMaxCtas * HET_MAX_RANKS * 4;
+}
+
+__device__ __forceinline__ uint32_t* epoch_base(uint64_t own_base, uint64_t signal_off,
+                                                int channel) {
+  return reinterpret_cast<uint32_t*>(own_base + signal_off + slot_bytes()) + channel;
+}
+
+// Every thread of the CTA returns the same value (the base is only written by
+// het_symm_epoch_add / _set, stream-ordered against the collectives).
+__device__ __forceinline__ uint32_t launch_epoch(const Args& a, const uint64_t* peer) {
+  __syncthreads();                                  // peer table staged
+  if (!(a.epoch & HET_SYMM_EPOCH_DEVICE)) return a.epoch;
+  const volatile uint32_t* b = epoch_base(peer[a.s.rank], a.s.signal_off, a.channel);
+  return *b + (a.epoch & ~HET_SYMM_EPOCH_DEVICE);
+}
+
+__global__ void epoch_update_kernel(uint32_t* base, uint32_t v, int add) {
+  *base = add ? *base + v : v;
+}
+
 // `peer` is the CTA's shared copy of the peer base table.
 __device__ void cross_barrier(const Sym& s, const uint64_t* peer, int channel, int kind,
                               uint32_t epoch) {
@@ -275,7 +303,8 @@ __device__ __forceinline__ void symm_ag_kernel_body(const float* __restrict__ sr
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
-  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank released its copy of the unit
+  const uint32_t ep = launch_epoch(a, peer);
+  cross_barrier(s, peer, a.channel, 0, ep);   // every rank released its copy of the unit
   const int64_t n = a.count;
   const uint64_t dst0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;  // byte offset
   const int nr = NR > 0 ? NR : s.nranks;   // compile-time for 2/4/8 ranks: loops unroll
@@ -305,14 +334,14 @@ __device__ __forceinline__ void symm_ag_kernel_body(const float* __restrict__ sr
       if (threadIdx.x == 0) {
         __threadfence_system();
         st_release_sys(slot(peer[a.relay_to], s.signal_off, a.channel, 2, s_cta, s.rank),
-                       a.epoch);
+                       ep);
       }
     }
     ag_push<NR>(src, h2, 0, direct, dst0, peer, nr, all, src_vec);
     if (a.relay_from >= 0) {
       if (threadIdx.x == 0) {
         wait_epoch(slot(peer[s.rank], s.signal_off, a.channel, 2, s_cta, a.relay_from),
-                   a.epoch, s.timeout_ns);
+                   ep, s.timeout_ns);
       }
       __syncthreads();
       const uint64_t fdst0 = a.data_off + static_cast<uint64_t>(a.from_offset) * 2;
@@ -380,7 +409,7 @@ __device__ __forceinline__ void symm_ag_kernel_body(const float* __restrict__ sr
     for (int64_t e = body_end + 2 * t; e + 1 < n; e += 2 * blockDim.x) pair(e);
     if (t == 0 && (n - body_end) % 2 == 1) single(n - 1);
   }
-  cross_barrier(s, peer, a.channel, 1, a.epoch);   // every rank's stores have landed
+  cross_barrier(s, peer, a.channel, 1, ep);   // every rank's stores have landed
 }
 
 template <bool MC, int NR>
@@ -408,7 +437,8 @@ __device__ __forceinline__ void symm_rs_kernel_body(float* __restrict__ out, con
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
-  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's accumulator is final
+  const uint32_t ep = launch_epoch(a, peer);
+  cross_barrier(s, peer, a.channel, 0, ep);   // every rank's accumulator is final
   const int64_t n = a.count;
   const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 4;
   const int nr = NR > 0 ? NR : s.nranks;   // compile-time for 2/4/8 ranks: loops unroll
@@ -481,7 +511,7 @@ __device__ __forceinline__ void symm_rs_kernel_body(float* __restrict__ out, con
     for (int64_t e = threadIdx.x; e < head; e += blockDim.x) one(e);
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
-  if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading my acc
+  if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, ep);  // peers done reading my acc
 }
 
 template <bool MC, int NR>
@@ -512,7 +542,8 @@ __device__ __forceinline__ void symm_rs_bf16_kernel_body(float* __restrict__ out
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
-  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's gradient is staged
+  const uint32_t ep = launch_epoch(a, peer);
+  cross_barrier(s, peer, a.channel, 0, ep);   // every rank's gradient is staged
   const int64_t n = a.count;
   const uint64_t src0 = a.data_off + static_cast<uint64_t>(a.offset) * 2;
   const int nr = NR > 0 ? NR : s.nranks;
@@ -580,7 +611,7 @@ __device__ __forceinline__ void symm_rs_bf16_kernel_body(float* __restrict__ out
     for (int64_t e = threadIdx.x; e < head; e += blockDim.x) one(e);
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
-  if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, a.epoch);  // peers done reading mine
+  if (a.end_barrier) cross_barrier(s, peer, a.channel, 1, ep);  // peers done reading mine
 }
 
 template <int NR>
@@ -654,7 +685,8 @@ __device__ __forceinline__ void symm_ag_help_kernel_body(const float* __restrict
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
-  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank released its copy of the unit
+  const uint32_t ep = launch_epoch(a, peer);
+  cross_barrier(s, peer, a.channel, 0, ep);   // every rank released its copy of the unit
   const int nr = NR > 0 ? NR : s.nranks;
   const uint32_t all = (nr >= 32) ? 0xffffffffu : ((1u << nr) - 1u);
   const int me = s.rank;
@@ -678,7 +710,7 @@ __device__ __forceinline__ void symm_ag_help_kernel_body(const float* __restrict
       const int64_t hi = lo + per_iter < h.own_hi[p] ? lo + per_iter : h.own_hi[p];
       ag_push<NR>(src, h2, lo, hi, dst0, peer, nr, (1u << me) | (1u << h.own_peer[p]), src_vec);
       if ((k + 1) % h.gran == 0 || k + 1 == kp)
-        signal_progress(peer[h.own_peer[p]], s, a.channel, progress(a.epoch, k, h.gran));
+        signal_progress(peer[h.own_peer[p]], s, a.channel, progress(ep, k, h.gran));
     }
   }
   // 2) my direct body vectors to every rank
@@ -694,7 +726,7 @@ __device__ __forceinline__ void symm_ag_help_kernel_body(const float* __restrict
       const int64_t kq = iters_of(h.help_lo[q], h.help_hi[q], per_iter);
       if (k >= kq) continue;
       const int owner = h.help_peer[q];
-      await_progress(peer, s, a.channel, owner, progress(a.epoch, k, h.gran));
+      await_progress(peer, s, a.channel, owner, progress(ep, k, h.gran));
       const uint64_t fdst0 = a.data_off + static_cast<uint64_t>(h.help_offset[q]) * 2;
       int64_t fh1, fh2, fnvec;
       ag_geometry(fdst0, h.help_count[q], &fh1, &fh2, &fnvec);
@@ -723,7 +755,7 @@ __device__ __forceinline__ void symm_ag_help_kernel_body(const float* __restrict
     for (int64_t e = body_end + 2 * t; e + 1 < n; e += 2 * blockDim.x) pair(e);
     if (t == 0 && (n - body_end) % 2 == 1) single(n - 1);
   }
-  cross_barrier(s, peer, a.channel, 1, a.epoch);   // every rank's stores have landed
+  cross_barrier(s, peer, a.channel, 1, ep);   // every rank's stores have landed
 }
 
 template <int NR>
@@ -801,7 +833,8 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
   __shared__ uint64_t peer[HET_MAX_RANKS];
   HET_STAGE_PEERS(a, peer);
   const Sym s{a.s.nranks, a.s.rank, a.s.mc_base, a.s.signal_off, a.timeout_ns};
-  cross_barrier(s, peer, a.channel, 0, a.epoch);   // every rank's input is final
+  const uint32_t ep = launch_epoch(a, peer);
+  cross_barrier(s, peer, a.channel, 0, ep);   // every rank's input is final
   const int nr = NR > 0 ? NR : s.nranks;
   constexpr int ES = BF16 ? 2 : 4, VE = 16 / ES;
   const int64_t gtid = static_cast<int64_t>(s_cta) * blockDim.x + threadIdx.x;
@@ -847,7 +880,7 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
         }
       }
       if ((k + 1) % h.gran == 0 || k + 1 == kq)
-        signal_progress(peer[h.help_peer[q]], s, a.channel, progress(a.epoch, k, h.gran));
+        signal_progress(peer[h.help_peer[q]], s, a.channel, progress(ep, k, h.gran));
     }
   }
   // 2) my direct vectors: reduce over all ranks straight into my shard
@@ -880,7 +913,7 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
     for (int p = 0; p < h.n_own; ++p) {
       const int64_t kp = iters_of(h.own_lo[p], h.own_hi[p], per_iter);
       if (k >= kp) continue;
-      await_progress(peer, s, a.channel, h.own_peer[p], progress(a.epoch, k, h.gran));
+      await_progress(peer, s, a.channel, h.own_peer[p], progress(ep, k, h.gran));
       const uint64_t base = peer[h.own_peer[p]] + h.stage_off;
       const int64_t lo = h.own_lo[p] + k * per_iter;
       const int64_t hi = lo + per_iter < h.own_hi[p] ? lo + per_iter : h.own_hi[p];
@@ -937,7 +970,7 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
     for (int64_t e = body_end + threadIdx.x; e < n; e += blockDim.x) one(e);
   }
   // every owner finished pulling its helpers' staging (and every helper its inputs)
-  cross_barrier(s, peer, a.channel, 1, a.epoch);
+  cross_barrier(s, peer, a.channel, 1, ep);
 }
 
 template <int NR, bool BF16>
@@ -1277,7 +1310,26 @@ int set_symm_timeout_ms(int ms) {
 extern "C" {
 
 int64_t het_symm_signal_bytes(void) {
-  return static_cast<int64_t>(HET_SYMM_CHANNELS) * kKinds * kMaxCtas * HET_MAX_RANKS * 4;
+  return static_cast<int64_t>(slot_bytes()) + 256;   // + the device epoch bases
+}
+
+static int epoch_update(const het_symm_t* s, int channel, uint32_t v, int add, void* stream,
+                        const char* who) {
+  if (!s || s->rank < 0 || s->rank >= s->nranks || s->nranks > HET_MAX_RANKS)
+    return fail(HET_EARG, "%s: bad descriptor", who);
+  if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "%s: bad channel", who);
+  uint32_t* b = reinterpret_cast<uint32_t*>(s->peer_base[s->rank] + s->signal_off +
+                                            slot_bytes()) + channel;
+  epoch_update_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(b, v, add);
+  return het::check_launch(who);
+}
+
+int het_symm_epoch_set(const het_symm_t* s, int channel, uint32_t value, void* stream) {
+  return epoch_update(s, channel, value, 0, stream, "het_symm_epoch_set");
+}
+
+int het_symm_epoch_add(const het_symm_t* s, int channel, uint32_t delta, void* stream) {
+  return epoch_update(s, channel, delta, 1, stream, "het_symm_epoch_add");
 }
 
 int het_symm_status(int reset) {

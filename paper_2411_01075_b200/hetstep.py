@@ -25,6 +25,8 @@ HET_MAX_RANKS = 8
 HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
 SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_RELAY, SYMM_HELPERS = 0, 1, 2, 3, 4
+SYMM_CHANNELS = 2                # HET_SYMM_CHANNELS: 0 = AG stream, 1 = RS stream
+EPOCH_DEVICE = 0x80000000        # HET_SYMM_EPOCH_DEVICE
 OP_AG, OP_RS, OP_RS_BF16 = 0, 1, 2
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
@@ -39,7 +41,7 @@ EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "
            "het_symm_status", "het_symm_allgather_pack", "het_symm_reduce_scatter",
            "het_symm_reduce_scatter_bf16", "het_gather_bf16", "het_accumulate_multi",
            "het_embedding_grad_dev", "het_adamw_coef", "het_adamw_devcoef",
-           "het_symm_status_async", "het_probe_smid", "het_symm_helper_plan",
+           "het_symm_status_async", "het_symm_epoch_set", "het_symm_epoch_add", "het_probe_smid", "het_symm_helper_plan",
            "het_symm_virtual")
 
 
@@ -111,6 +113,8 @@ def load(build: bool = False) -> ctypes.CDLL:
         "het_symm_signal_bytes": ([], i64),
         "het_symm_status": ([i32], i32),
         "het_symm_status_async": ([vp, vp], i32),
+        "het_symm_epoch_set": ([ctypes.POINTER(HetSymm), i32, ctypes.c_uint32, vp], i32),
+        "het_symm_epoch_add": ([ctypes.POINTER(HetSymm), i32, ctypes.c_uint32, vp], i32),
         "het_probe_smid": ([vp, i32, vp], i32),
         "het_symm_allgather_pack": ([ctypes.POINTER(HetSymm), vp, ctypes.c_uint64,
                                      ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.c_uint32,
@@ -1229,10 +1233,51 @@ class SymmWorkspace:
         self.views = {name: region_tensor(self.raw, self.offsets[name], numel, dtype)
                       for name, numel, dtype in regions}
         self.epoch = [0, 0]
+        # device-epoch mode (capture of a multi-rank step into a CUDA graph): the
+        # host counters at capture start; None = host epochs
+        self._dev_epoch0: list[int] | None = None
         self.ctas = ctas
         self.policy = policy
         torch.cuda.synchronize(device)
         self.handle.barrier()
+
+    def _next_epoch(self, ch: int) -> int:
+        """Epoch argument of the next launch on channel `ch`: the host counter, or
+        in device-epoch mode its offset from the capture start flagged
+        EPOCH_DEVICE (the kernel adds the device-resident base)."""
+        self.epoch[ch] += 1
+        if self._dev_epoch0 is None:
+            return self.epoch[ch]
+        return EPOCH_DEVICE | (self.epoch[ch] - self._dev_epoch0[ch])
+
+    def begin_device_epochs(self, stream) -> None:
+        """Seed the device bases from the host counters (queued on `stream`,
+        before the capture) and switch the following calls to device epochs."""
+        for ch in range(SYMM_CHANNELS):
+            _check(load().het_symm_epoch_set(ctypes.byref(self.desc), ch, self.epoch[ch],
+                                             _stream(stream)), "het_symm_epoch_set")
+        self._dev_epoch0 = list(self.epoch)
+
+    def end_device_epochs(self, stream) -> list[int]:
+        """Inside the capture, after the step's last collective of each channel
+        has been ordered before `stream`: queue the base advance by the step's
+        launches per channel, restore the host counters (the capture ran
+        nothing) and return those per-replay deltas (advance_host after each
+        replay keeps eager calls in sequence)."""
+        if self._dev_epoch0 is None:
+            raise InputError("end_device_epochs without begin_device_epochs")
+        deltas = [e - e0 for e, e0 in zip(self.epoch, self._dev_epoch0)]
+        for ch, d in enumerate(deltas):
+            if d:
+                _check(load().het_symm_epoch_add(ctypes.byref(self.desc), ch, d,
+                                                 _stream(stream)), "het_symm_epoch_add")
+        self.epoch = list(self._dev_epoch0)
+        self._dev_epoch0 = None
+        return deltas
+
+    def advance_host(self, deltas: Sequence[int]) -> None:
+        for ch, d in enumerate(deltas):
+            self.epoch[ch] += d
 
     def __getitem__(self, name: str) -> torch.Tensor:
         return self.views[name]
@@ -1242,11 +1287,11 @@ class SymmWorkspace:
                        policy: Optional[int] = None) -> None:
         """bf16 unit at `region`[elem_off:] <- every rank's fp32 range (fused pack+AG).
         `policy` overrides the workspace's route policy for this call."""
-        self.epoch[0] += 1
+        ep = self._next_epoch(0)
         src = _cuda(src_f32, torch.float32, "src") if src_f32.numel() else None
         byte_off = self.offsets[region] + 2 * elem_off
         _check(load().het_symm_allgather_pack(ctypes.byref(self.desc), src, byte_off,
-                                              _i64(counts), _i64(offsets), self.epoch[0], 0,
+                                              _i64(counts), _i64(offsets), ep, 0,
                                               self.policy if policy is None else int(policy),
                                               self.ctas, _stream(stream)),
                "het_symm_allgather_pack")
@@ -1257,14 +1302,14 @@ class SymmWorkspace:
         """out <- sum over ranks of the fp32 accumulator at `region`[elem_off:] (my range).
         `policy` overrides the workspace's route policy for this call (SYMM_HELPERS:
         helpers reduce pieces in place in their own accumulator)."""
-        self.epoch[1] += 1
+        ep = self._next_epoch(1)
         o = _cuda(out, torch.float32, "out") if out.numel() else None
         byte_off = self.offsets[region] + 4 * elem_off
         pol = self.policy if policy is None else int(policy)
         if pol == SYMM_RELAY:          # all-gather only
             pol = SYMM_AUTO
         _check(load().het_symm_reduce_scatter(ctypes.byref(self.desc), byte_off, o, _i64(counts),
-                                              _i64(offsets), self.epoch[1], 1, int(end_barrier),
+                                              _i64(offsets), ep, 1, int(end_barrier),
                                               pol, self.ctas, _stream(stream)),
                "het_symm_reduce_scatter")
 
@@ -1277,7 +1322,7 @@ class SymmWorkspace:
         (my range), in fp32: Eq. 1 weighting and the cast inside the RS.
         policy=SYMM_HELPERS stages the helpers' fp32 sums in the fp32 region
         `stage` (same element offsets)."""
-        self.epoch[1] += 1
+        ep = self._next_epoch(1)
         o = _cuda(out, torch.float32, "out") if out.numel() else None
         byte_off = self.offsets[region] + 2 * elem_off
         stage_off = self.offsets[stage] + 4 * elem_off if stage is not None else 0
@@ -1285,7 +1330,7 @@ class SymmWorkspace:
             raise InputError("reduce_scatter_bf16: the helper route needs an fp32 stage region")
         w = (ctypes.c_float * len(weights))(*[float(x) for x in weights])
         _check(load().het_symm_reduce_scatter_bf16(ctypes.byref(self.desc), byte_off, o,
-                                                   _i64(counts), _i64(offsets), w, self.epoch[1],
+                                                   _i64(counts), _i64(offsets), w, ep,
                                                    1, int(end_barrier), int(policy), stage_off,
                                                    self.ctas, _stream(stream)),
                "het_symm_reduce_scatter_bf16")

@@ -263,6 +263,9 @@ class UnevenFSDPTrainer:
         self.graph = False
         self.graph_warmup = 2
         self._graph = None
+        self._capturing = False
+        self._coef: torch.Tensor | None = None
+        self._epoch_deltas = [0, 0]
         self._graph_launches = 0
         self._eager_steps = 0
         if self.offload:
@@ -578,10 +581,14 @@ class UnevenFSDPTrainer:
         a, b = self.timers.pair("adamw", (30.0 if self.need_shadow else 28.0) * (hi - lo))
         if a is not None:
             a.record(self.rs_stream)
-        K.adamw(self.p32[lo:hi], self.g32[lo:hi], self.m32[lo:hi], self.v32[lo:hi], shadow,
-                lr=self.opt.lr, beta1=self.opt.betas[0], beta2=self.opt.betas[1],
-                eps=self.opt.eps, weight_decay=self.opt.weight_decay, step=self.steps + 1,
-                stream=self.rs_stream)
+        if self._coef is not None:      # graph capture: coefficients staged per replay
+            K.adamw_devcoef(self.p32[lo:hi], self.g32[lo:hi], self.m32[lo:hi],
+                            self.v32[lo:hi], shadow, self._coef, stream=self.rs_stream)
+        else:
+            K.adamw(self.p32[lo:hi], self.g32[lo:hi], self.m32[lo:hi], self.v32[lo:hi],
+                    shadow, lr=self.opt.lr, beta1=self.opt.betas[0], beta2=self.opt.betas[1],
+                    eps=self.opt.eps, weight_decay=self.opt.weight_decay, step=self.steps + 1,
+                    stream=self.rs_stream)
         if b is not None:
             b.record(self.rs_stream)
         self.launches += 1
@@ -741,7 +748,15 @@ class UnevenFSDPTrainer:
         return self._step(tok)
 
     def graph_eligible(self) -> bool:
-        return (self.cuda and self.N == 1 and not self.offload and self.tracer is None
+        """One rank, or several whose every unit routes through the fused
+        collectives (their barrier epochs then come from device memory, so a
+        replay needs no host counter); no offload, no tracer, a non-idle rank.
+        Ranks decide independently: a replaying rank issues the same epoch
+        sequence as an eager one."""
+        multi_ok = self.N == 1 or (self.symm is not None
+                                   and all(r == "symm" for r in self.ag_route)
+                                   and all(r == "symm" for r in self.rs_route))
+        return (self.cuda and multi_ok and not self.offload and self.tracer is None
                 and self.m > 0)
 
     @property
@@ -754,10 +769,16 @@ class UnevenFSDPTrainer:
             return self._step(tok)
         if self._graph is None:
             self._capture(tok)
+        if self._watch is not None:
+            self._watch.poll()           # earlier replays' collectives: raise on a timeout
         self._g_tok.copy_(tok, non_blocking=True)
         self._stage_coef()
         self._graph.replay()
         self.steps += 1
+        if self.N > 1:
+            self.symm.advance_host(self._epoch_deltas)
+            if self._watch is not None:
+                self._watch.record(self._current(), f"step {self.steps} on rank {self.rank}")
         K.LAUNCHES += self._graph_launches
         self.launches += self._graph_own
         return self._g_loss.clone()
@@ -784,6 +805,12 @@ class UnevenFSDPTrainer:
         self._coef_ev = [torch.cuda.Event() for _ in range(4)]
         for ev in self._coef_ev:
             ev.record()
+        cur = self._current()
+        # a green-context rank captures on its own compute stream, so the kernel
+        # nodes keep the SM partition (torch's default capture stream would not)
+        cap_stream = None if cur == torch.cuda.default_stream(self.device) else cur
+        if self.N > 1:                  # barrier epochs from device memory from now on
+            self.symm.begin_device_epochs(cur)
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         timers_on = self.timers.enabled
@@ -791,11 +818,19 @@ class UnevenFSDPTrainer:
             self.timers.reset()
             self.timers.external = True
         n0, s0, l0 = K.LAUNCHES, self.steps, self.launches
+        self._capturing = True
         try:
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=cap_stream):
                 self._g_loss = self._step(self._g_tok, coef=self._coef_dev)
+                if self.N > 1:
+                    # the capture stream has joined every AG / RS launch of the step
+                    self._epoch_deltas = self.symm.end_device_epochs(self._current())
         finally:
             self.timers.external = False
+            self._capturing = False
+            if self.N > 1 and self.symm._dev_epoch0 is not None:    # failed capture
+                self.symm.epoch = list(self.symm._dev_epoch0)
+                self.symm._dev_epoch0 = None
         # the capture issued no work: every replay counts the captured launches
         self._graph_launches = K.LAUNCHES - n0
         self._graph_own = self.launches - l0
@@ -808,7 +843,8 @@ class UnevenFSDPTrainer:
         if self.m > 0 and (tok.shape[0] != self.m * self.l or tok.shape[1] != arch.seq + 1):
             raise InputError(f"rank {self.rank} expects tokens [{self.m * self.l}, {arch.seq + 1}]")
         multi = self.N > 1
-        if self._watch is not None:
+        self._coef = coef                # graph capture: AdamW coefficients on the device
+        if self._watch is not None and not self._capturing:
             self._watch.poll()           # earlier steps' collectives: raise on a timeout
         unit_names = [nm for nm, _ in arch.unit_layout()]
         root_names = [nm for nm, _ in arch.root_layout()]
@@ -831,8 +867,10 @@ class UnevenFSDPTrainer:
             ag_ev[root] = self._ag(root, self.rbuf)
             ag_ev[0] = self._ag(0, self.ubuf[0])
         racc = self._acc(root)
-        if multi:
-            comp.wait_stream(self.rs_stream)     # racc no longer read by last step's RS
+        if multi and not self._capturing:
+            # racc no longer read by last step's RS (graph replays are serialised on
+            # the launch stream, so a captured step needs no such edge)
+            comp.wait_stream(self.rs_stream)
         K.fill(racc, 0.0)
         self.launches += 1
 
@@ -1051,7 +1089,7 @@ class UnevenFSDPTrainer:
         if multi:
             rs_ev[root] = self._rs(root, racc, self._event(comp))
             comp.wait_event(rs_ev[root])            # RS stream is in order: all shards ready
-            if self._watch is not None:
+            if self._watch is not None and not self._capturing:   # replays: _graph_step
                 self._watch.record(comp, f"step {self.steps + 1} on rank {self.rank}")
 
         # ---- optimizer -------------------------------------------------------

@@ -238,6 +238,27 @@ def main(out_dir: str) -> None:
         report["symm_status_odd"] = float(K.SymmWorkspace.status(reset=True))
         del t3
 
+        stage(rank, "graph replay")
+        # the multi-rank step as a CUDA graph (device-resident barrier epochs): five
+        # steps eager against two eager + capture + replays, same tokens every step
+        res = {}
+        for graph in (False, True):
+            tg = UnevenFSDPTrainer(arch, pplan, rank, comm_ag=cag, comm_rs=crs, device=dev,
+                                   algo=K.ALGO_SYMM)
+            tg.load_full_units(units)
+            tg.graph = graph and tg.graph_eligible()
+            for _ in range(5):
+                tg.step(ptok)
+            tg.check_faults()
+            if graph:
+                report["graph_active"] = float(tg.graph_active or tg.m == 0)
+            res[graph] = [t.cpu().numpy() for t in tg.full_units("p32")]
+            del tg
+        report["graph_vs_eager"] = max(
+            float(np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b), 1e-30))
+            for a, b in zip(res[True], res[False]))
+        report["symm_status_graph"] = float(K.SymmWorkspace.status(reset=True))
+
         stage(rank, "fault injection")
         # fault injection: rank 0 enters a fused all-gather that no other rank joins
         # (shortened spin limit). Its barrier times out; the trainer's asynchronous

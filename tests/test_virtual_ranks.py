@@ -177,6 +177,33 @@ def test_virtual_ranks_planner_shapes_n8(cuda, name):
             check_reduce_scatter_bf16(vg, counts, offs, 0, 400 + si, _weights(n), policy)
 
 
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_device_epochs(cuda, n):
+    """Device-resident barrier epochs (the CUDA-graph replay of a multi-rank
+    step): every rank's base seeded with het_symm_epoch_set, launches passing
+    EPOCH_DEVICE | offset, the base advanced with het_symm_epoch_add between
+    "replays". The collectives stay exact, no barrier times out, and the start
+    barrier's slots hold base + offset (the epoch the kernel resolved), not the
+    raw argument."""
+    counts = [3_571_623 // 64 + 5 * j for j in range(n)]
+    offs = _offsets(counts)
+    vg = VirtualGroup(n, [("unit", sum(counts) + 64, torch.bfloat16),
+                          ("acc", sum(counts) + 64, torch.float32),
+                          ("g16", sum(counts) + 64, torch.bfloat16)], cuda)
+    base = [0x00123450, 0x00ABC000]
+    vg.set_device_base(base)
+    for replay in range(3):
+        check_allgather(vg, counts, offs, K.SYMM_AUTO, 0, seed=replay)
+        check_reduce_scatter(vg, counts, offs, 0, 10 + replay)
+        check_reduce_scatter_bf16(vg, counts, offs, 0, 20 + replay, _weights(n))
+        want = vg.dev_base[0] + 1           # the replay's first AG channel launch
+        for r in range(n):
+            words = vg.signal_words(r, n).cpu().numpy().astype(np.int64)
+            assert (words == want).all(), f"rank {r} start-barrier slots {words} != {want}"
+        vg.add_device_base(0, 1)           # one AG launch per "replay"
+        vg.add_device_base(1, 2)           # two RS launches
+
+
 def test_missing_rank_times_out_and_is_reported(cuda):
     """Fault injection: rank 0 of a 2-rank all-gather is launched alone (the
     real per-rank entry point, one launch) and rank 1 never joins. Rank 0's

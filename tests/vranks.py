@@ -56,7 +56,34 @@ class VirtualGroup:
         sms = torch.cuda.get_device_properties(device).multi_processor_count
         self.ctas = ctas if ctas is not None else max(1, min(32, sms // n))
         self.epoch = [0, 0]
+        self.dev_base: list[int] | None = None
         torch.cuda.synchronize(device)
+
+    def set_device_base(self, base: Sequence[int]) -> None:
+        """Seed every rank's device epoch base (het_symm_epoch_set) and switch the
+        launches to device epochs; the host counters continue from `base`."""
+        lib = K.load()
+        for r in range(self.n):
+            for ch in range(K.SYMM_CHANNELS):
+                K._check(lib.het_symm_epoch_set(ctypes.byref(self.desc[r]), ch, int(base[ch]),
+                                                torch.cuda.current_stream(self.device).cuda_stream),
+                         "het_symm_epoch_set")
+        self.epoch = list(base)
+        self.dev_base = list(base)
+
+    def add_device_base(self, ch: int, delta: int) -> None:
+        """het_symm_epoch_add on every rank: launches numbered from the new base."""
+        lib = K.load()
+        for r in range(self.n):
+            K._check(lib.het_symm_epoch_add(ctypes.byref(self.desc[r]), ch, int(delta),
+                                            torch.cuda.current_stream(self.device).cuda_stream),
+                     "het_symm_epoch_add")
+        self.dev_base[ch] += delta
+
+    def signal_words(self, r: int, count: int) -> torch.Tensor:
+        """The first `count` uint32 barrier slots of rank r (channel 0, start
+        barrier, CTA 0: one per source rank)."""
+        return K.region_tensor(self.raw, r * self.stride + self.signal_off, count, torch.int32)
 
     def view(self, r: int, name: str) -> torch.Tensor:
         """Rank r's copy of a region (its own version counter, like the real
@@ -72,6 +99,10 @@ class VirtualGroup:
              policy: int = K.SYMM_AUTO, stage_off: int = 0) -> None:
         lib, n = K.load(), self.n
         self.epoch[channel] += 1
+        # device-epoch mode (set_device_base): the launch passes its offset from the
+        # per-rank device base, flagged EPOCH_DEVICE, as a captured step does
+        ep = self.epoch[channel] if self.dev_base is None else \
+            K.EPOCH_DEVICE | (self.epoch[channel] - self.dev_base[channel])
         descs = (K.HetSymm * n)(*self.desc)
         src_p = (ctypes.c_void_p * n)(*[(t.data_ptr() if t is not None and t.numel() else None)
                                         for t in srcs])
@@ -80,7 +111,7 @@ class VirtualGroup:
         w = (ctypes.c_float * n)(*[float(x) for x in weights]) if weights is not None else None
         torch.cuda.synchronize(self.device)
         K._check(lib.het_symm_virtual(op, n, descs, src_p, out_p, K._i64(counts), K._i64(offsets),
-                                      byte_off, w, self.epoch[channel], channel,
+                                      byte_off, w, ep, channel,
                                       int(end_barrier), int(policy), int(stage_off), self.ctas,
                                       torch.cuda.current_stream(self.device).cuda_stream),
                  "het_symm_virtual")
