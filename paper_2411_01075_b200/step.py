@@ -748,16 +748,12 @@ class UnevenFSDPTrainer:
         return self._step(tok)
 
     def graph_eligible(self) -> bool:
-        """One rank, or several whose every unit routes through the fused
-        collectives (their barrier epochs then come from device memory, so a
-        replay needs no host counter); no offload, no tracer, a non-idle rank.
-        Ranks decide independently: a replaying rank issues the same epoch
-        sequence as an eager one."""
-        multi_ok = self.N == 1 or (self.symm is not None
-                                   and all(r == "symm" for r in self.ag_route)
-                                   and all(r == "symm" for r in self.rs_route))
-        return (self.cuda and multi_ok and not self.offload and self.tracer is None
-                and self.m > 0)
+        """No offload, no tracer, a non-idle rank. With several ranks the fused
+        collectives take their barrier epochs from device memory inside a
+        replay (no host counter) and NCCL-routed units are captured as NCCL
+        graph nodes. Ranks decide independently: a replaying rank issues the
+        same collective and epoch sequence as an eager one."""
+        return self.cuda and not self.offload and self.tracer is None and self.m > 0
 
     @property
     def graph_active(self) -> bool:

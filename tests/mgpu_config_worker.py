@@ -70,7 +70,11 @@ def main(out_dir: str) -> None:
     dist.broadcast_object_list(ids, src=0)
     cag, crs = K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
     try:
-        for name in CASES.get(world, []):
+        # each config twice: the route table the bench uses ("default": NCCL for
+        # near-single-owner units at N >= 4) and every unit on the fused kernels
+        # ("fused": the helper routes forced)
+        for name, mode in [(c, m) for c in CASES.get(world, []) for m in ("default", "fused")]:
+            K.HELPERS_ROUTE = mode == "fused"
             arch, plan = scaled_plan(name, world)
             units = cpu_units(arch, seed=3)
             tr = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev,
@@ -90,7 +94,7 @@ def main(out_dir: str) -> None:
                                           if x == K.SYMM_HELPERS)),
                         wire16=float(sum(tr.wire16)), status=float(K.SymmWorkspace.status()))
             if rank == 0:
-                np.savez(os.path.join(out_dir, f"{name}.npz"), loss=float(loss),
+                np.savez(os.path.join(out_dir, f"{name}.{mode}.npz"), loss=float(loss),
                          micro=np.array([(a.microbatch, a.num_microbatches)
                                          for a in plan.assignments]),
                          ratios=np.array([a.state_ratio for a in plan.assignments]),
@@ -104,6 +108,7 @@ def main(out_dir: str) -> None:
             torch.cuda.empty_cache()
             dist.barrier()
     finally:
+        K.HELPERS_ROUTE = False
         cag.close()
         crs.close()
         dist.destroy_process_group()

@@ -3,7 +3,8 @@ budgets are set with a memory-fraction cap, and per-rank SM partitions are
 set with CUDA green contexts"; reference capacity semantics core.py:101-127):
 
   * a kernel launched on a tier's compute stream runs only on the tier's SMs
-    (every CTA records its %smid; the distinct ids are <= the partition);
+    (every CTA records its %smid; the distinct ids are <= the partition),
+    also when captured on that stream into a CUDA graph and replayed;
   * the persistent grids of the owned kernels are sized for the partition
     (het_tune HET_TUNE_SM_BUDGET is set by emulate_tier);
   * an allocation past the tier's HBM cap raises instead of succeeding.
@@ -40,6 +41,20 @@ def test_green_context_confines_kernels_to_the_partition(cuda):
         ids_all = K.probe_smid(total * 8)
         torch.cuda.synchronize()
         assert len(set(ids_all.cpu().tolist())) > emu.num_sms
+        # a CUDA graph captured on the partition's stream (how a green-context rank
+        # captures its step, step.UnevenFSDPTrainer._capture) keeps the partition
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=emu.stream):
+            ids_g = K.probe_smid(emu.num_sms * 8, stream=emu.stream)
+        for _ in range(3):
+            ids_g.fill_(-1)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(emu.stream):
+                g.replay()
+            torch.cuda.synchronize()
+            replayed = set(ids_g.cpu().tolist())
+            assert -1 not in replayed
+            assert len(replayed) <= emu.num_sms, (len(replayed), emu.num_sms)
     finally:
         K.set_sm_budget(0)
 

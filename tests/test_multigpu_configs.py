@@ -50,8 +50,11 @@ def test_multigpu_bench_layouts_match_oracle(tmp_path):
     dev = torch.device("cuda", 0)
     for name in names:
         d = np.load(tmp_path / f"{name}.npz")
-        assert d["route_ok"] == 1.0 and d["fused"] == 1.0 and d["status"] == 0.0, name
-        arch = ARCHS[name]
+        cfg, mode = name.split(".")
+        assert d["route_ok"] == 1.0 and d["status"] == 0.0, name
+        if mode == "fused":
+            assert d["fused"] == 1.0, f"{name}: a unit left the fused kernels"
+        arch = ARCHS[cfg]
         micro = [tuple(int(x) for x in mi) for mi in d["micro"]]
         toks = [d["toks"][r, :int(n)] for r, n in enumerate(d["tok_rows"])]
         live = [(t, mi) for t, mi in zip(toks, micro) if mi[0] > 0]
