@@ -592,11 +592,21 @@ def main() -> None:
             line["trace_rank0"] = {k: v for k, v in trace_report.items() if k != "events"}
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
+    # a captured step holds NCCL graph nodes of comm_ag / comm_rs: destroy it before
+    # the communicators (ncclCommDestroy would otherwise wait on the live graph)
+    tr.release_graph()
     if world > 1:
+        # teardown never costs the run: the line is printed, so a hung NCCL / symmetric
+        # memory destructor ends the process after a grace period instead of hanging
+        import threading
+        threading.Timer(120.0, lambda: os._exit(0)).start()
         dist.barrier()
         comm_ag.close()
         comm_rs.close()
         dist.destroy_process_group()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     if emu.green is not None:
         # The green context must outlive every tensor that touched its stream;
         # interpreter teardown frees them in arbitrary order (and then records

@@ -779,6 +779,14 @@ class UnevenFSDPTrainer:
         self.launches += self._graph_own
         return self._g_loss.clone()
 
+    def release_graph(self) -> None:
+        """Drop the captured step (before the communicators its NCCL nodes use are
+        destroyed); the next step runs eagerly and may capture again."""
+        if self._graph is not None:
+            torch.cuda.synchronize(self.device)
+            self._graph = None
+            self._eager_steps = 0
+
     def _stage_coef(self) -> None:
         """AdamW coefficients of the coming step into the device buffer the graph's
         het_adamw_devcoef reads: host math (het_adamw_coef, as het_adamw), a pinned
