@@ -329,6 +329,9 @@ def main() -> None:
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as one CUDA graph (auto: on where eligible: "
                          "one rank, no activation offload)")
+    ap.add_argument("--adamw-overlap", default="auto", choices=["auto", "on", "off"],
+                    help="N>1: AdamW of each unit's shard on the RS stream behind its "
+                         "reduce-scatter (on) or one pass over the shard at the end (off)")
     ap.add_argument("--symm-ctas", type=int, default=64,
                     help="CTAs per fused collective launch (each holds one SM while it runs)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
@@ -359,6 +362,8 @@ def main() -> None:
                            device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO,
                            offload_activations=offload,
                            offload_schedule=args.offload_schedule, symm_ctas=args.symm_ctas)
+    if args.adamw_overlap != "auto":
+        tr.overlap_adamw = world > 1 and args.adamw_overlap == "on"
     tr.init_params(seed=0)
     # a memory-capped rank runs its head in row chunks so the [rows, vocab]
     # logits transient stays within 10% of its emulated HBM
@@ -564,6 +569,7 @@ def main() -> None:
                        "tier_capacity": tier_capacity(job, args.no_emulate),
                        "collectives": route_summary(tr),
                        "symm_ctas": args.symm_ctas,
+                       "adamw_overlap": tr.overlap_adamw,
                        "l2": "working set (p,g,m,v,shadow = 30 B/param) >> 126 MB L2; no flush"},
             "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
                     "h2d_bytes_per_step": tok_bytes, "d2h_bytes_per_step": 4 * world},

@@ -771,8 +771,9 @@ class UnevenFSDPTrainer:
         self._stage_coef()
         self._graph.replay()
         self.steps += 1
-        if self.N > 1:
+        if self.symm is not None:
             self.symm.advance_host(self._epoch_deltas)
+        if self.N > 1:
             if self._watch is not None:
                 self._watch.record(self._current(), f"step {self.steps} on rank {self.rank}")
         K.LAUNCHES += self._graph_launches
@@ -813,7 +814,7 @@ class UnevenFSDPTrainer:
         # a green-context rank captures on its own compute stream, so the kernel
         # nodes keep the SM partition (torch's default capture stream would not)
         cap_stream = None if cur == torch.cuda.default_stream(self.device) else cur
-        if self.N > 1:                  # barrier epochs from device memory from now on
+        if self.symm is not None:       # barrier epochs from device memory from now on
             self.symm.begin_device_epochs(cur)
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
@@ -826,13 +827,13 @@ class UnevenFSDPTrainer:
         try:
             with torch.cuda.graph(g, stream=cap_stream):
                 self._g_loss = self._step(self._g_tok, coef=self._coef_dev)
-                if self.N > 1:
+                if self.symm is not None:
                     # the capture stream has joined every AG / RS launch of the step
                     self._epoch_deltas = self.symm.end_device_epochs(self._current())
         finally:
             self.timers.external = False
             self._capturing = False
-            if self.N > 1 and self.symm._dev_epoch0 is not None:    # failed capture
+            if self.symm is not None and self.symm._dev_epoch0 is not None:   # failed capture
                 self.symm.epoch = list(self.symm._dev_epoch0)
                 self.symm._dev_epoch0 = None
         # the capture issued no work: every replay counts the captured launches
