@@ -373,8 +373,8 @@ def main() -> None:
     torch.cuda.empty_cache()     # the full-model init temporaries, before the capped steps
     tr.graph = args.graph != "off" and tr.graph_eligible()
     if args.graph == "on" and not tr.graph:
-        raise SystemExit("--graph on: the step is not graph-eligible here (offload, an idle rank, "
-                         "or NCCL-routed units at N>1)")
+        raise SystemExit("--graph on: the step is not graph-eligible here (offload, an idle "
+                         "rank, no symmetric workspace at N>1, or N>4)")
     arch, plan = job.arch, job.plan
     nsteps = args.warmup + args.steps
     host = [torch.from_numpy(rank_tokens(plan, rank, arch.seq, arch.vocab, SEED, s)).pin_memory()

@@ -209,10 +209,13 @@ class UnevenFSDPTrainer:
         # straight into its slot of the symmetric staging buffer gb{u % 2}
         # (hetstep.grad_destinations), so no het_gather_bf16 copy follows
         self.grad_in_place = True
-        # N > 1: AdamW of each unit's shard runs on the RS stream right after that
-        # unit's reduce-scatter (overlapping the rest of the backward) instead of
-        # one pass over the whole shard at the end of the step
-        self.overlap_adamw = self.N > 1
+        # N > 1 option: AdamW of each unit's shard on the RS stream right after that
+        # unit's reduce-scatter (overlapping the rest of the backward) instead of one
+        # pass over the whole shard at the end of the step. Off by default: at N=4 it
+        # left the step rate unchanged (GPT-2 5309 vs 5299, Llama 581 vs 580 samples/s)
+        # while the overlapped launches ran at 0.49-0.66 of HBM against 0.89-0.90 for
+        # the single pass (profiles/r2z/)
+        self.overlap_adamw = False
         # Eq. 1 weights of every rank (the bf16-wire reduce-scatter applies them itself)
         self.rank_weights = [a.microbatch / plan.total_batch for a in plan.assignments]
         self._set_routes(self.symm is not None)
@@ -751,9 +754,14 @@ class UnevenFSDPTrainer:
         """No offload, no tracer, a non-idle rank. With several ranks the fused
         collectives take their barrier epochs from device memory inside a
         replay (no host counter) and NCCL-routed units are captured as NCCL
-        graph nodes. Ranks decide independently: a replaying rank issues the
-        same collective and epoch sequence as an eager one."""
-        return self.cuda and not self.offload and self.tracer is None and self.m > 0
+        graph nodes next to them. Ranks decide independently: a replaying rank
+        issues the same collective and epoch sequence as an eager one.
+        Multi-rank capture is limited to what was measured: a symmetric
+        workspace present (an all-NCCL step hung in capture at N=2,
+        profiles/r2z/) and N <= 4 (N=8 never ran on real GPUs here)."""
+        multi_ok = self.N == 1 or (self.symm is not None and self.N <= 4)
+        return (self.cuda and multi_ok and not self.offload and self.tracer is None
+                and self.m > 0)
 
     @property
     def graph_active(self) -> bool:

@@ -251,11 +251,14 @@ def main(out_dir: str) -> None:
                                        algo=K.ALGO_SYMM)
                 tg.load_full_units(units)
                 tg.graph = graph and tg.graph_eligible()
+                elig = tg.graph_eligible()
                 for _ in range(5):
                     tg.step(gtok)
                 tg.check_faults()
                 if graph:
-                    report[f"graph_active_{len(report)}"] = float(tg.graph_active or tg.m == 0)
+                    # (idle ranks and N > 4 stay eager: graph_eligible)
+                    report[f"graph_active_{len(report)}"] = float(
+                        tg.graph_active or not tg.graph_eligible())
                 res[graph] = [t.cpu().numpy() for t in tg.full_units("p32")]
                 del tg
             worst = max(worst, max(
