@@ -251,7 +251,6 @@ def main(out_dir: str) -> None:
                                        algo=K.ALGO_SYMM)
                 tg.load_full_units(units)
                 tg.graph = graph and tg.graph_eligible()
-                elig = tg.graph_eligible()
                 for _ in range(5):
                     tg.step(gtok)
                 tg.check_faults()
