@@ -1009,6 +1009,10 @@ HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "0") == "1"
 # stores / loads: single-owner AG at N=4, 1 GB, round 1: multicast 554 GB/s against
 # 660-700 for the peer-class routes (profiles/r1_collectives_n4*.jsonl)
 MC_EFF = 0.83
+# Experiment knobs for near-single-owner units at N >= 4 (default: NCCL's ring):
+# HET_OWNER_FUSED = "rs16" keeps the bf16-wire reduce-scatter fused on them,
+# "all" also the all-gather
+OWNER_FUSED = _os.environ.get("HET_OWNER_FUSED", "")
 
 
 def symm_link_bytes(op: str, counts: Sequence[int], nranks: int, policy: int,
@@ -1092,9 +1096,9 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
         # bf16 wire (weights + cast in the RS, half the link bytes): fused except
         # near-single-owner units at N >= 4, where NCCL's fp32 ring reduce measured
         # 665 against the wire's 507 fp32-equivalent GB/s (profiles/r2/summary.md)
-        return "nccl" if owner_like else "symm"
+        return "nccl" if owner_like and OWNER_FUSED not in ("rs16", "all") else "symm"
     if op == "ag":
-        return "nccl" if owner_like else "symm"
+        return "nccl" if owner_like and OWNER_FUSED != "all" else "symm"
     if op == "rs":
         if nranks == 2 or mx - mn <= 1:
             return "symm"

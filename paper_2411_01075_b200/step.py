@@ -298,7 +298,10 @@ class UnevenFSDPTrainer:
         """Per-unit collective routes (fused symmetric kernels vs NCCL ring), fixed by shape."""
         units = range(self.L.blocks + 1)
         self.ag_route = [K.route_collective("ag", self.L.counts[u], self.N, sym) for u in units]
-        self.rs_route = [K.route_collective("rs", self.L.counts[u], self.N, sym) for u in units]
+        # a block of an l_i <= 1 plan can take the bf16 wire: routed as "rs16"
+        wire_ok = self.bf16_wire and self.pair_units
+        self.rs_route = [K.route_collective("rs16" if wire_ok and u < self.L.blocks else "rs",
+                                            self.L.counts[u], self.N, sym) for u in units]
         # fused-route kernel policy per unit (hetstep.symm_policy): plain / multicast,
         # pair relay (AG) or helpers (skewed and single-owner units at N >= 3)
         mc = self.symm is not None and self.symm.multicast
