@@ -1010,8 +1010,8 @@ HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "0") == "1"
 # 660-700 for the peer-class routes (profiles/r1_collectives_n4*.jsonl)
 MC_EFF = 0.83
 # Experiment knobs for near-single-owner units at N >= 4 (default: NCCL's ring):
-# HET_OWNER_FUSED = "rs16" keeps the bf16-wire reduce-scatter fused on them,
-# "all" also the all-gather
+# HET_OWNER_FUSED = "rs16" keeps the bf16-wire reduce-scatter fused on them, "rs"
+# both reduce-scatter forms (bf16 wire and fp32), "all" also the all-gather
 OWNER_FUSED = _os.environ.get("HET_OWNER_FUSED", "")
 
 
@@ -1096,11 +1096,11 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
         # bf16 wire (weights + cast in the RS, half the link bytes): fused except
         # near-single-owner units at N >= 4, where NCCL's fp32 ring reduce measured
         # 665 against the wire's 507 fp32-equivalent GB/s (profiles/r2/summary.md)
-        return "nccl" if owner_like and OWNER_FUSED not in ("rs16", "all") else "symm"
+        return "nccl" if owner_like and OWNER_FUSED not in ("rs16", "rs", "all") else "symm"
     if op == "ag":
         return "nccl" if owner_like and OWNER_FUSED != "all" else "symm"
     if op == "rs":
-        if nranks == 2 or mx - mn <= 1:
+        if nranks == 2 or mx - mn <= 1 or OWNER_FUSED in ("rs", "all"):
             return "symm"
         return "nccl" if owner_like or total * 4 >= (512 << 20) else "symm"
     raise InputError(f"unknown collective {op!r}")
