@@ -1009,10 +1009,12 @@ HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "0") == "1"
 # stores / loads: single-owner AG at N=4, 1 GB, round 1: multicast 554 GB/s against
 # 660-700 for the peer-class routes (profiles/r1_collectives_n4*.jsonl)
 MC_EFF = 0.83
-# Experiment knobs for near-single-owner units at N >= 4 (default: NCCL's ring):
-# HET_OWNER_FUSED = "rs16" keeps the bf16-wire reduce-scatter fused on them, "rs"
-# both reduce-scatter forms (bf16 wire and fp32), "all" also the all-gather
-OWNER_FUSED = _os.environ.get("HET_OWNER_FUSED", "")
+# Near-single-owner units at N >= 4 stay on the fused kernels by default (the
+# whole multi-rank step is then capturable as one CUDA graph). HET_OWNER_FUSED
+# selects the measured alternatives that send them to NCCL's ring instead:
+# "rs16" / "rs" keep only the reduce-scatters fused (AG on NCCL), "none" sends
+# both to NCCL (the round-1 table). profiles/r2o/, profiles/r2b4/.
+OWNER_FUSED = _os.environ.get("HET_OWNER_FUSED", "all")
 
 
 def symm_link_bytes(op: str, counts: Sequence[int], nranks: int, policy: int,
@@ -1073,16 +1075,18 @@ def symm_policy(op: str, counts: Sequence[int], nranks: int, multicast: bool = F
 
 def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) -> str:
     """'symm' (fused kernels on the symmetric workspace) or 'nccl' for one
-    unit's all-gather ("ag", bf16) / reduce-scatter ("rs", fp32). With the
-    helper routes (HELPERS_ROUTE) every unit at N >= 3 is fused and
-    symm_policy picks the kernel route. Without them, the round-1 table from
-    the measured sweeps (profiles/r1_collectives_n2.jsonl, r1_collectives_n4*.jsonl):
-      * AG: the fused kernel wins every shape except near-single-owner units at
-        N >= 4, where NCCL's pipelined ring broadcast keeps the owner's link
-        busier than the NVLS multicast store does;
-      * RS: the fused kernel wins even units, every shape at N = 2 and skewed
-        units up to a few hundred MB; near-single-owner units and very large
-        skewed units at N >= 4 go to NCCL's per-owner ring reduce.
+    unit's all-gather ("ag", bf16) / reduce-scatter ("rs" fp32, "rs16" bf16
+    wire). Every shape is fused by default (OWNER_FUSED = "all"); symm_policy
+    then picks the kernel route. Measured on the steps at N=4 (samples/s,
+    fused + CUDA graph vs NCCL ring for the near-single-owner units, eager:
+    NCCL nodes in a captured step hung when some ranks ran eagerly):
+    BERT-large 1518 vs 1487, GPT-2 small 5260 vs 5235, Llama-1.3B 566 vs 574
+    (profiles/r2b4/, r2o/, r2x/). In isolation NCCL's ring still moves a
+    single-owner 1 GB unit faster (AG 672 vs 535, RS 671 vs 461 GB/s,
+    profiles/r2w/); OWNER_FUSED = "none" restores that table:
+      * AG: near-single-owner units at N >= 4 to NCCL's ring broadcast;
+      * RS: even units, N = 2 and skewed units up to a few hundred MB fused;
+        near-single-owner and very large skewed units at N >= 4 to NCCL.
     """
     if not symm or nranks == 1:
         return "nccl"
@@ -1093,9 +1097,7 @@ def route_collective(op: str, counts: Sequence[int], nranks: int, symm: bool) ->
         # every shape (the reduce-scatter of very large skewed units included)
         return "symm"
     if op == "rs16":
-        # bf16 wire (weights + cast in the RS, half the link bytes): fused except
-        # near-single-owner units at N >= 4, where NCCL's fp32 ring reduce measured
-        # 665 against the wire's 507 fp32-equivalent GB/s (profiles/r2/summary.md)
+        # bf16 wire (weights + cast in the RS, half the link bytes)
         return "nccl" if owner_like and OWNER_FUSED not in ("rs16", "rs", "all") else "symm"
     if op == "ag":
         return "nccl" if owner_like and OWNER_FUSED != "all" else "symm"

@@ -754,15 +754,17 @@ class UnevenFSDPTrainer:
         return self._step(tok)
 
     def graph_eligible(self) -> bool:
-        """No offload, no tracer, a non-idle rank. With several ranks the fused
-        collectives take their barrier epochs from device memory inside a
-        replay (no host counter) and NCCL-routed units are captured as NCCL
-        graph nodes next to them. Ranks decide independently: a replaying rank
-        issues the same collective and epoch sequence as an eager one.
-        Multi-rank capture is limited to what was measured: a symmetric
-        workspace present (an all-NCCL step hung in capture at N=2,
-        profiles/r2z/) and N <= 4 (N=8 never ran on real GPUs here)."""
-        multi_ok = self.N == 1 or (self.symm is not None and self.N <= 4)
+        """No offload, no tracer, a non-idle rank. With several ranks every unit
+        must route through the fused collectives, which take their barrier
+        epochs from device memory inside a replay (no host counter); ranks
+        decide independently, a replaying rank issuing the same epoch sequence
+        as an eager one. NCCL-routed units are not captured: steps with NCCL
+        graph nodes hung when some ranks ran eagerly (BERT-large N=4, offloading
+        ranks eager) and in an all-NCCL N=2 step (profiles/r2z/, r2b4/). N <= 4:
+        N=8 never ran on real GPUs here."""
+        multi_ok = self.N == 1 or (self.symm is not None and self.N <= 4
+                                   and all(r == "symm" for r in self.ag_route)
+                                   and all(r == "symm" for r in self.rs_route))
         return (self.cuda and multi_ok and not self.offload and self.tracer is None
                 and self.m > 0)
 

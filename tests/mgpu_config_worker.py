@@ -70,11 +70,11 @@ def main(out_dir: str) -> None:
     dist.broadcast_object_list(ids, src=0)
     cag, crs = K.Comm(ids[0], world, rank), K.Comm(ids[1], world, rank)
     try:
-        # each config twice: the route table the bench uses ("default": NCCL for
-        # near-single-owner units at N >= 4) and every unit on the fused kernels
-        # ("fused": the helper routes forced)
-        for name, mode in [(c, m) for c in CASES.get(world, []) for m in ("default", "fused")]:
-            K.HELPERS_ROUTE = mode == "fused"
+        # each config twice: the route table the bench uses ("default": every unit
+        # on the fused kernels) and the NCCL ring for near-single-owner units at
+        # N >= 4 ("nccl": hetstep.OWNER_FUSED = "none")
+        for name, mode in [(c, m) for c in CASES.get(world, []) for m in ("default", "nccl")]:
+            K.OWNER_FUSED = "none" if mode == "nccl" else "all"
             arch, plan = scaled_plan(name, world)
             units = cpu_units(arch, seed=3)
             tr = UnevenFSDPTrainer(arch, plan, rank, comm_ag=cag, comm_rs=crs, device=dev,
@@ -108,7 +108,7 @@ def main(out_dir: str) -> None:
             torch.cuda.empty_cache()
             dist.barrier()
     finally:
-        K.HELPERS_ROUTE = False
+        K.OWNER_FUSED = "all"
         cag.close()
         crs.close()
         dist.destroy_process_group()

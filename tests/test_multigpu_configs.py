@@ -52,7 +52,7 @@ def test_multigpu_bench_layouts_match_oracle(tmp_path):
         d = np.load(tmp_path / f"{name}.npz")
         cfg, mode = name.split(".")
         assert d["route_ok"] == 1.0 and d["status"] == 0.0, name
-        if mode == "fused":
+        if mode == "default":
             assert d["fused"] == 1.0, f"{name}: a unit left the fused kernels"
         arch = ARCHS[cfg]
         micro = [tuple(int(x) for x in mi) for mi in d["micro"]]
