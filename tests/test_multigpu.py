@@ -60,7 +60,9 @@ def test_multigpu_collectives_and_step(tmp_path):
             elif k.startswith("graph_active"):
                 assert v == 1.0, "the multi-rank step was not replayed as a CUDA graph"
             elif k == "graph_vs_eager":
-                assert v <= 1e-6, f"graph-replayed steps differ from eager steps: {v}"
+                # same kernels in the same order; the slack covers atomics-order
+                # differences of the attention backward, not a second path
+                assert v <= 1e-5, f"graph-replayed steps differ from eager steps: {v}"
             elif k == "trace_lint_problems":
                 assert v == 0.0, "measured multi-rank trace violates the schedule's causality"
     arch = ARCHS["tiny_gpt"]
