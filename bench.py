@@ -332,8 +332,9 @@ def main() -> None:
     ap.add_argument("--adamw-overlap", default="auto", choices=["auto", "on", "off"],
                     help="N>1: AdamW of each unit's shard on the RS stream behind its "
                          "reduce-scatter (on) or one pass over the shard at the end (off)")
-    ap.add_argument("--symm-ctas", type=int, default=64,
-                    help="CTAs per fused collective launch (each holds one SM while it runs)")
+    ap.add_argument("--symm-ctas", type=int, default=32,
+                    help="CTAs per fused collective launch (each holds one SM while it runs; "
+                         "32 measured best in the N=4 steps: profiles/r2c2/)")
     ap.add_argument("--algo", type=int, default=K.ALGO_SYMM,
                     help="collective route for N>1: 4 = fused symmetric-memory kernels "
                          "(default), 0 = NCCL auto, 1 = NCCL send/recv, 2 = NCCL per-owner")

@@ -133,7 +133,7 @@ class UnevenFSDPTrainer:
     def __init__(self, arch: ArchSpec, plan: TrainPlan, rank: int, *,
                  comm_ag: K.Comm | None = None, comm_rs: K.Comm | None = None,
                  opt: AdamWConfig = AdamWConfig(), device: torch.device | None = None,
-                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 64,
+                 algo: int = K.ALGO_AUTO, group_name: str | None = None, symm_ctas: int = 32,
                  offload_activations: bool = False, offload_schedule: str = "reference",
                  check_routes: bool = True,
                  bf16_wire: bool = True, group=None, symm_workspace=None):
