@@ -329,6 +329,9 @@ def main() -> None:
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as one CUDA graph (auto: on where eligible: "
                          "one rank, no activation offload)")
+    ap.add_argument("--acc-grid", type=int, default=None, choices=[0, 1],
+                    help="accumulate grids: 0 persistent (one resident wave), 1 one CTA per "
+                         "chunk (library default when unset)")
     ap.add_argument("--adamw-overlap", default="auto", choices=["auto", "on", "off"],
                     help="N>1: AdamW of each unit's shard on the RS stream behind its "
                          "reduce-scatter (on) or one pass over the shard at the end (off)")
@@ -363,6 +366,8 @@ def main() -> None:
                            device=dev, algo=args.algo if world > 1 else K.ALGO_AUTO,
                            offload_activations=offload,
                            offload_schedule=args.offload_schedule, symm_ctas=args.symm_ctas)
+    if args.acc_grid is not None:
+        K.set_acc_grid(args.acc_grid)
     if args.adamw_overlap != "auto":
         tr.overlap_adamw = world > 1 and args.adamw_overlap == "on"
     tr.init_params(seed=0)

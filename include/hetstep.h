@@ -214,6 +214,12 @@ int het_gelu_bwd_bias(const void* dy, const void* pre, void* dpre, int64_t rows,
 /* HET_TUNE_SYMM_TIMEOUT_MS: spin limit of the fused collectives' cross-rank
  * barriers (default 10000 ms); after it the kernel records HET_SYMM_TIMEOUT. */
 #define HET_TUNE_SYMM_TIMEOUT_MS 3
+/* HET_TUNE_ACC_GRID: grid of the accumulate kernels. 0 = persistent (one wave
+ * of the CTAs resident on the rank's SMs, each walking its share of chunks);
+ * 1 = one CTA per chunk, so the hardware scheduler spreads the work over
+ * whatever SMs are free (a persistent wave whose SMs are partly held by the
+ * fused collectives' CTAs runs as two waves). */
+#define HET_TUNE_ACC_GRID 4
 int het_tune(int key, int value);
 
 /* Emulation diagnostic: `ctas` CTAs each write the %smid they ran on to

@@ -40,6 +40,7 @@ int check_launch(const char* what) {
 }
 
 int g_sm_budget = 0;   // het_tune(HET_TUNE_SM_BUDGET); 0 = the whole device
+int g_acc_grid = 0;    // het_tune(HET_TUNE_ACC_GRID): 0 persistent, 1 one CTA per chunk
 
 int sm_count() {
   static int dev_sms = 0;
@@ -606,7 +607,8 @@ int het_accumulate(float* acc, const het_seg_t* segs, int nseg, int mode, float 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, T, 0);                   \
       if (per_sm <= 0) per_sm = 1;                                                        \
     }                                                                                     \
-    const int64_t r = static_cast<int64_t>(per_sm) * het::sm_count();                     \
+    const int64_t r = het::g_acc_grid ? blocks : static_cast<int64_t>(per_sm) *          \
+                                                 het::sm_count();                         \
     const dim3 grid(static_cast<unsigned>(blocks < r ? blocks : r));                      \
     kf<<<grid, T, 0, st>>>(acc, t, scale);                                                \
   } while (0)
@@ -659,7 +661,8 @@ int het_accumulate_multi(float* acc, const het_seg_t* segs, int nseg, int nsrc, 
                                                   accumulate_multi_kernel<HET_ACC_ADD, 4>, 512, 0);
     if (per_sm <= 0) per_sm = 1;
   }
-  const int64_t resident = static_cast<int64_t>(per_sm) * het::sm_count();
+  const int64_t resident = het::g_acc_grid ? blocks
+                                           : static_cast<int64_t>(per_sm) * het::sm_count();
   const dim3 grid(static_cast<unsigned>(blocks < resident ? blocks : resident));
 #define HET_ACCM(M, K) accumulate_multi_kernel<M, K><<<grid, 512, 0, st>>>(acc, t, ms, scale)
   if (mode == HET_ACC_FIRST) {
@@ -827,6 +830,11 @@ int het_tune(int key, int value) {
     return HET_OK;
   }
   if (key == HET_TUNE_SYMM_TIMEOUT_MS) return het::set_symm_timeout_ms(value);
+  if (key == HET_TUNE_ACC_GRID) {
+    if (value != 0 && value != 1) return fail(HET_EARG, "het_tune: accumulate grid mode 0 or 1");
+    het::g_acc_grid = value;
+    return HET_OK;
+  }
   if (key == HET_TUNE_ACC_VARIANT) {
     if (value < 0 || value >= static_cast<int>(sizeof(kAccShapes) / sizeof(kAccShapes[0])))
       return fail(HET_EARG, "het_tune: accumulate variant %d out of range", value);

@@ -433,6 +433,7 @@ def embedding_grad(acc: torch.Tensor, wte_off: int, wpe_off: int | None, dy: tor
 HET_TUNE_ACC_VARIANT = 1
 HET_TUNE_SM_BUDGET = 2
 HET_TUNE_SYMM_TIMEOUT_MS = 3
+HET_TUNE_ACC_GRID = 4
 LN_DIMS = (256, 768, 1024)
 
 
@@ -920,6 +921,11 @@ def set_sm_budget(nsm: int) -> None:
 def set_symm_timeout_ms(ms: int) -> None:
     """Spin limit of the fused collectives' cross-rank barriers (default 10 s)."""
     tune(HET_TUNE_SYMM_TIMEOUT_MS, int(ms))
+
+
+def set_acc_grid(mode: int) -> None:
+    """Accumulate grids: 0 persistent (one resident wave), 1 one CTA per chunk."""
+    tune(HET_TUNE_ACC_GRID, int(mode))
 
 
 def tune(key: int, value: int) -> None:

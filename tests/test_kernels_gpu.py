@@ -124,6 +124,29 @@ def test_accumulate_multi_bit_exact(cuda, nsrc, sizes):
         assert _rel(many.cpu().numpy(), ref) <= RTOL
 
 
+def test_accumulate_grid_modes_bit_identical(cuda):
+    """HET_TUNE_ACC_GRID: one CTA per chunk (1) and the persistent wave (0) give
+    bit-identical accumulators, single- and multi-source."""
+    w = 7.0 / 173.0
+    grads, offs, total = _segments([768 * 2304, 2304, 5, 768 * 768, 33000], 5)
+    src = [[(g * (j + 1)).to(torch.bfloat16).to(cuda) for g in grads] for j in range(2)]
+    out = {}
+    try:
+        for mode in (0, 1):
+            K.set_acc_grid(mode)
+            a = torch.zeros(total, device=cuda)
+            K.accumulate(a, list(zip(src[0], offs)), True, w)
+            K.accumulate(a, list(zip(src[1], offs)), False, w)
+            b = torch.zeros(total, device=cuda)
+            K.accumulate_multi(b, src, offs, True, w)
+            torch.cuda.synchronize()
+            out[mode] = (a, b)
+    finally:
+        K.set_acc_grid(0)
+    for x, y in zip(out[0], out[1]):
+        assert torch.equal(x.view(torch.int32), y.view(torch.int32))
+
+
 def test_accumulate_multi_unaligned_and_rejects(cuda):
     grads, offs, total = _segments([1000, 4099], 4)
     acc = torch.zeros(total + 1, device=cuda)[1:]            # 4-byte aligned only
