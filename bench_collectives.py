@@ -33,10 +33,11 @@ from paper_2411_01075_b200.configs import build_job  # noqa: E402
 ALGOS = {"auto": K.ALGO_AUTO, "p2p": K.ALGO_P2P, "owner": K.ALGO_OWNER,
          "symm": "symm", "symm_mc": "symm_mc", "symm_peer": "symm_peer", "route": "route",
          "symm_relay": "symm_relay", "symm_helpers": "symm_helpers",
+         "symm_helpers_mc": "symm_helpers_mc",
          "symm_bf16wire": "symm_bf16wire", "symm_bf16wire_helpers": "symm_bf16wire_helpers"}
 SYMM = {"symm": (True, K.SYMM_AUTO), "symm_mc": (True, K.SYMM_MULTICAST),
         "symm_peer": (False, K.SYMM_PEER), "symm_relay": (False, K.SYMM_RELAY),
-        "symm_helpers": (False, K.SYMM_HELPERS)}
+        "symm_helpers": (False, K.SYMM_HELPERS), "symm_helpers_mc": (True, K.SYMM_HELPERS_MC)}
 
 
 def skew_counts(skew: str, total: int, n: int) -> list[int]:
@@ -113,7 +114,8 @@ def main() -> None:
     ws = {}
     for an, (mc, policy) in SYMM.items():
         if an in args.algos or (an == "symm_helpers" and "symm_bf16wire_helpers" in args.algos) \
-                or (an in ("symm", "symm_relay", "symm_helpers") and world > 2 and
+                or (an in ("symm", "symm_relay", "symm_helpers", "symm_helpers_mc")
+                    and world > 2 and
                                 "route" in args.algos) or (an == "symm" and (
                                     "route" in args.algos or "symm_bf16wire" in args.algos)):
             ws[an] = K.SymmWorkspace([("unit", maxel, torch.bfloat16), ("acc", maxel + 64,
@@ -139,6 +141,8 @@ def main() -> None:
                         algo = ALGOS[an]
                         if op == "reduce_scatter" and algo in (K.ALGO_P2P, "symm_relay"):
                             continue
+                        if op == "allgather" and algo == "symm_helpers_mc":   # fp32 RS only
+                            continue
                         if algo == "route":   # the train step's per-unit choice
                             pick = K.route_collective("ag" if op == "allgather" else "rs", c,
                                                       world, "symm" in ws)
@@ -147,7 +151,8 @@ def main() -> None:
                                 pol = K.symm_policy("ag" if op == "allgather" else "rs", c,
                                                     world, multicast=ws["symm"].multicast)
                                 algo = {K.SYMM_RELAY: "symm_relay",
-                                        K.SYMM_HELPERS: "symm_helpers"}.get(pol, "symm")
+                                        K.SYMM_HELPERS: "symm_helpers",
+                                        K.SYMM_HELPERS_MC: "symm_helpers_mc"}.get(pol, "symm")
                         if algo in ("symm_bf16wire", "symm_bf16wire_helpers"):
                             if op != "reduce_scatter":
                                 continue

@@ -289,11 +289,18 @@ int het_reduce_scatter_uneven(const float* src, float* shard_out, const int64_t*
  * A single owner then moves S (not (N-1) S) over its link; the plan
  * (het_symm_helper_plan) balances every link's load. N >= 3. */
 #define HET_SYMM_HELPERS 4
+/* fp32 reduce-scatter only (others treat it as HELPERS; without a multicast
+ * object it is HELPERS): the helpers, and the owner for its direct part, reduce
+ * through the switch (multimem.ld_reduce: 4 B per element in) instead of
+ * pulling N-1 peer ranges, and the owner pulls the staged sums. Not rank-ordered
+ * (like HET_SYMM_MULTICAST). */
+#define HET_SYMM_HELPERS_MC 5
 
 /* Ops of het_symm_helper_plan */
 #define HET_OP_AG 0
 #define HET_OP_RS 1
 #define HET_OP_RS_BF16 2
+#define HET_OP_RS_MC 3     /* fp32 RS under HET_SYMM_HELPERS_MC (its link costs) */
 
 /* A buffer allocated at the same byte layout on every rank (torch symmetric
  * memory is the plumbing): peer_base[j] = its address on rank j mapped into

@@ -825,7 +825,12 @@ struct RsVec {
   }
 };
 
-template <int NR, bool BF16>
+// MC (fp32 only, HET_SYMM_HELPERS_MC): the helpers and the owner's direct part
+// reduce through the switch (multimem.ld_reduce: one stream of sums in, 4 B per
+// element) instead of pulling N-1 peers' ranges; the owner still pulls the
+// staged sums. Not rank-ordered: within 1e-5 of the fp64 oracle, like the
+// multicast route.
+template <int NR, bool BF16, bool MC = false>
 __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out,
                                                                 const Args& a,
                                                                 const HArgs& h,
@@ -854,6 +859,29 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
       rs_geometry<BF16>(a.data_off, h.help_offset[q], h.help_count[q], &head, &nv);
       const int64_t lo = h.help_lo[q] + k * per_iter;
       const int64_t hi = lo + per_iter < h.help_hi[q] ? lo + per_iter : h.help_hi[q];
+      if (MC && !BF16) {           // the switch sums the N ranks' vectors
+        constexpr int kM = 8;      // reduced vectors in flight per thread
+        for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kM) {
+          float4 r[kM];
+#pragma unroll
+          for (int u = 0; u < kM; ++u) {
+            const int64_t v = v0 + u * gsz;
+            if (v < hi)
+              r[u] = mc_ldr_v4(s.mc_base + a.data_off +
+                               static_cast<uint64_t>(h.help_offset[q] + head + v * VE) * ES);
+          }
+#pragma unroll
+          for (int u = 0; u < kM; ++u) {
+            const int64_t v = v0 + u * gsz;
+            if (v < hi)
+              __stcg(reinterpret_cast<float4*>(peer[s.rank] + h.stage_off + static_cast<uint64_t>(
+                                                   h.help_offset[q] + head + v * VE) * 4), r[u]);
+          }
+        }
+        if ((k + 1) % h.gran == 0 || k + 1 == kq)
+          signal_progress(peer[h.help_peer[q]], s, a.channel, progress(ep, k, h.gran));
+        continue;
+      }
       // kB vectors' N loads in flight per thread before any combine
       constexpr int kB = NR > 0 ? (16 / NR > 2 ? 16 / NR : 2) : 2;
       for (int64_t v0 = lo + gtid; v0 < hi; v0 += gsz * kB) {
@@ -899,8 +927,15 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
     }
   };
   for (int64_t v = gtid; v < h.direct; v += gsz) {
+    const uint64_t off = a.data_off + static_cast<uint64_t>(a.offset + head + v * VE) * ES;
+    if (MC && !BF16) {
+      const float4 r4 = mc_ldr_v4(s.mc_base + off);
+      const float r[4] = {r4.x, r4.y, r4.z, r4.w};
+      put(head + v * VE, r);
+      continue;
+    }
     RsVec<NR, BF16> rv;
-    rv.reduce(peer, nr, a.data_off + static_cast<uint64_t>(a.offset + head + v * VE) * ES, wt);
+    rv.reduce(peer, nr, off, wt);
     put(head + v * VE, rv.r);
   }
   // 3) owner: pull my pieces, reduced by their helpers, as they become ready
@@ -973,13 +1008,13 @@ __device__ __forceinline__ void symm_rs_help_kernel_body(float* __restrict__ out
   cross_barrier(s, peer, a.channel, 1, ep);
 }
 
-template <int NR, bool BF16>
+template <int NR, bool BF16, bool MC = false>
 __global__ void __launch_bounds__(kThreads) symm_rs_help_kernel(float* __restrict__ out,
                                                                 const __grid_constant__ Args a,
                                                                 const __grid_constant__ HArgs h,
                                                                 const __grid_constant__ Weights wt) {
   set_ctx(blockIdx.x, gridDim.x);
-  symm_rs_help_kernel_body<NR, BF16>(out, a, h, wt);
+  symm_rs_help_kernel_body<NR, BF16, MC>(out, a, h, wt);
 }
 
 // ---------------------------------------------------------------- virtual ranks
@@ -1252,7 +1287,7 @@ void body_vectors(int op, int n, const int64_t* counts, const int64_t* offsets, 
       int64_t h1, h2, nv;
       ag_geometry(off + static_cast<uint64_t>(offsets[j]) * 2, counts[j], &h1, &h2, &nv);
       nvecs[j] = nv;
-    } else {
+    } else {             // RS, RS_MC: fp32; RS_BF16: bf16
       const int es = op == HET_OP_RS_BF16 ? 2 : 4;
       const uint64_t src0 = off + static_cast<uint64_t>(offsets[j]) * es;
       int64_t hd = static_cast<int64_t>(((16 - (src0 & 15)) & 15) / es);
@@ -1268,6 +1303,11 @@ void helper_costs(int op, int n, double* alpha, double* beta, double* gamma) {
     *alpha = 2.0 * (n - 1); *beta = 2; *gamma = 2.0 * (n - 2);
   } else if (op == HET_OP_RS) {
     *alpha = 4.0 * (n - 1); *beta = 4; *gamma = 4.0 * (n - 1);
+  } else if (op == HET_OP_RS_MC) {
+    // the owner's direct part and the helpers' pieces arrive as one stream of
+    // switch-reduced sums (4 B per element) at MC_EFF = 0.83 of a peer stream's
+    // rate (hetstep.py), the staged sums as a plain pull: peer-equivalent bytes
+    *alpha = 4.0 / 0.83; *beta = 4; *gamma = 4.0 / 0.83;
   } else {
     *alpha = 2.0 * (n - 1); *beta = 4; *gamma = 2.0 * (n - 1);
   }
@@ -1347,7 +1387,7 @@ int het_symm_helper_plan(int op, int nranks, const int64_t* counts, const int64_
                          uint64_t off, int64_t* out_direct, int32_t* out_pieces, int max_pieces,
                          double* link_load) {
   if (nranks < 1 || nranks > HET_MAX_RANKS || !counts || !offsets ||
-      (op != HET_OP_AG && op != HET_OP_RS && op != HET_OP_RS_BF16))
+      (op != HET_OP_AG && op != HET_OP_RS && op != HET_OP_RS_BF16 && op != HET_OP_RS_MC))
     return -fail(HET_EARG, "het_symm_helper_plan: bad args");
   const HelperPlan hp = plan_for(op, nranks, counts, offsets, off);
   if (out_direct)
@@ -1386,6 +1426,7 @@ int het_symm_virtual(int op, int nranks, const het_symm_t* descs, const float* c
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
   if (off & 15) return fail(HET_EARG, "het_symm_virtual: offset not 16B aligned");
   if (op != HET_OP_AG && policy == HET_SYMM_RELAY) policy = HET_SYMM_AUTO;
+  if (policy == HET_SYMM_HELPERS_MC) policy = HET_SYMM_HELPERS;   // one GPU: no multicast
   const bool helpers = policy == HET_SYMM_HELPERS;
   if (op == HET_OP_RS_BF16 && (!weights || (helpers && (stage_off & 15))))
     return fail(HET_EARG, "het_symm_virtual: bf16 wire needs weights (and a 16B stage)");
@@ -1469,6 +1510,7 @@ int het_symm_allgather_pack(const het_symm_t* s, const float* src, uint64_t unit
   if (channel < 0 || channel >= HET_SYMM_CHANNELS) return fail(HET_EARG, "bad channel");
   if (counts[s->rank] > 0 && !src) return fail(HET_EARG, "het_symm_allgather_pack: null src");
   if (unit_off & 15) return fail(HET_EARG, "het_symm_allgather_pack: unit offset not 16B aligned");
+  if (policy == HET_SYMM_HELPERS_MC) policy = HET_SYMM_HELPERS;
   Args a{*s, unit_off, counts[s->rank], offsets[s->rank], epoch, channel, 1, -1, -1, 0, 0, 0, 0,
          g_spin_timeout_ns};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1503,6 +1545,21 @@ int het_symm_reduce_scatter(const het_symm_t* s, uint64_t acc_off, float* out,
   Args a{*s, acc_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
   a.timeout_ns = g_spin_timeout_ns;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (policy == HET_SYMM_HELPERS_MC && !s->mc_base) policy = HET_SYMM_HELPERS;
+  if (policy == HET_SYMM_HELPERS_MC) {    // helpers reduce their pieces in the switch
+    HArgs h;
+    fill_hargs(plan_for(HET_OP_RS_MC, s->nranks, counts, offsets, acc_off), s->rank, counts,
+               offsets, ctas, &h);
+    h.stage_off = acc_off;
+    Weights wt{};
+    switch (s->nranks) {
+      case 2: symm_rs_help_kernel<2, false, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      case 4: symm_rs_help_kernel<4, false, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      case 8: symm_rs_help_kernel<8, false, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt); break;
+      default: symm_rs_help_kernel<0, false, true><<<ctas, kThreads, 0, st>>>(out, a, h, wt);
+    }
+    return het::check_launch("het_symm_reduce_scatter");
+  }
   if (policy == HET_SYMM_HELPERS) {       // helpers reduce in place in their own acc
     HArgs h;
     fill_hargs(plan_for(HET_OP_RS, s->nranks, counts, offsets, acc_off), s->rank, counts,
@@ -1535,6 +1592,7 @@ int het_symm_reduce_scatter_bf16(const het_symm_t* s, uint64_t grad_off, float* 
   if (!weights) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: null weights");
   if (counts[s->rank] > 0 && !out) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: null out");
   if (grad_off & 15) return fail(HET_EARG, "het_symm_reduce_scatter_bf16: grad offset not 16B aligned");
+  if (policy == HET_SYMM_HELPERS_MC) policy = HET_SYMM_HELPERS;   // weights: no switch sum
   Args a{*s, grad_off, counts[s->rank], offsets[s->rank], epoch, channel, end_barrier};
   a.timeout_ns = g_spin_timeout_ns;
   Weights wt{};

@@ -25,9 +25,10 @@ HET_MAX_RANKS = 8
 HET_SYMM_MAX_CTAS = 256
 HET_SYMM_TIMEOUT = 17
 SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_RELAY, SYMM_HELPERS = 0, 1, 2, 3, 4
+SYMM_HELPERS_MC = 5              # fp32 RS: helpers reduce in the switch (multimem.ld_reduce)
 SYMM_CHANNELS = 2                # HET_SYMM_CHANNELS: 0 = AG stream, 1 = RS stream
 EPOCH_DEVICE = 0x80000000        # HET_SYMM_EPOCH_DEVICE
-OP_AG, OP_RS, OP_RS_BF16 = 0, 1, 2
+OP_AG, OP_RS, OP_RS_BF16, OP_RS_MC = 0, 1, 2, 3
 
 EXPORTS = ("het_version", "het_last_error", "het_pack_bf16", "het_accumulate", "het_adamw",
            "het_fill_f32", "het_tune", "het_embedding_grad", "het_layernorm_partial_floats",
@@ -1011,6 +1012,9 @@ def reduce_scatter_uneven(src: torch.Tensor, shard: torch.Tensor, counts: Sequen
 # (profiles/r2/summary.md), so the default table keeps round 1's choices.
 import os as _os
 HELPERS_ROUTE = _os.environ.get("HET_HELPERS", "0") == "1"
+# switch-reduced helpers for the fp32 reduce-scatter (SYMM_HELPERS_MC) where a
+# multicast object exists: HET_HELPERS_MC=1 lets symm_policy pick them
+HELPERS_MC_ROUTE = _os.environ.get("HET_HELPERS_MC", "0") == "1"
 # NVLS multicast stores / ld_reduce reach a smaller share of the link than peer
 # stores / loads: single-owner AG at N=4, 1 GB, round 1: multicast 554 GB/s against
 # 660-700 for the peer-class routes (profiles/r1_collectives_n4*.jsonl)
@@ -1044,6 +1048,9 @@ def symm_link_bytes(op: str, counts: Sequence[int], nranks: int, policy: int,
     egress = es * (total - mn)            # every rank's inputs read by the others
     if policy == SYMM_MULTICAST and op == "rs":
         return 4.0 * total / MC_EFF
+    if policy == SYMM_HELPERS_MC and op == "rs":
+        # plan link costs of OP_RS_MC are peer-equivalent bytes already
+        return max(helper_plan(OP_RS_MC, c, _prefix(c))["link_bytes"])
     if policy == SYMM_HELPERS:
         plan = helper_plan(OP_RS if op == "rs" else OP_RS_BF16, c, _prefix(c))
         return max(max(plan["link_bytes"]), egress)
@@ -1076,6 +1083,10 @@ def symm_policy(op: str, counts: Sequence[int], nranks: int, multicast: bool = F
         hb = symm_link_bytes(op, c, nranks, SYMM_HELPERS)
         if hb < 0.9 * best and hb < 0.9 * auto:
             best, pol = hb, SYMM_HELPERS
+    if HELPERS_MC_ROUTE and multicast and op == "rs" and nranks >= 3:
+        hb = symm_link_bytes(op, c, nranks, SYMM_HELPERS_MC)
+        if hb < 0.9 * best and hb < 0.9 * auto:
+            best, pol = hb, SYMM_HELPERS_MC
     return pol
 
 

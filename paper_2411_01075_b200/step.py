@@ -324,7 +324,7 @@ class UnevenFSDPTrainer:
                           if self.rs_route[u] == "symm" else None for u in units]
         # the helper reduce-scatter ends with the cross-rank barrier in-kernel
         for u in units:
-            if self.rs_policy[u] == K.SYMM_HELPERS:
+            if self.rs_policy[u] in (K.SYMM_HELPERS, K.SYMM_HELPERS_MC):
                 self.rs_end[u] = True
         if self.pair_units:
             for u in range(self.L.blocks):

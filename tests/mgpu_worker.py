@@ -93,7 +93,8 @@ def main(out_dir: str) -> None:
         # fused symmetric-memory collectives (NVLS multicast when available, then peer)
         maxu = max(sum(c) for c in shard_cases(world)) + 64
         for use_mc, policy in ((True, K.SYMM_MULTICAST), (True, K.SYMM_AUTO), (False, K.SYMM_AUTO),
-                               (False, K.SYMM_RELAY), (False, K.SYMM_HELPERS)):
+                               (False, K.SYMM_RELAY), (False, K.SYMM_HELPERS),
+                               (True, K.SYMM_HELPERS_MC)):
             ws = K.SymmWorkspace([("unit", maxu, torch.bfloat16), ("acc", maxu, torch.float32),
                                   ("g16", maxu, torch.bfloat16)],
                                  dist.group.WORLD.group_name, dev, rank, world,
