@@ -41,6 +41,7 @@ def ag_symm_policy(counts, nranks, multicast=True):
 
 
 SYMM_AUTO, SYMM_MULTICAST, SYMM_PEER, SYMM_RELAY, SYMM_HELPERS = 0, 1, 2, 3, 4
+SYMM_HELPERS_MC = 5
 
 
 def symm_policy(op, counts, nranks, multicast=False):
