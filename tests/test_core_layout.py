@@ -198,3 +198,68 @@ def test_helper_plan_balances_links():
                 assert max(p["link_bytes"]) == pytest.approx(es * sum(c), rel=1e-3), (c, op)
         if len(c) < 3:
             assert K.helper_plan(K.OP_AG, c, offs)["pieces"] == []
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_default_route_table_is_all_fused(n, monkeypatch):
+    """Round-2 default (hetstep.OWNER_FUSED = "all"): every unit shape of the
+    three bench plans routes through the fused kernels for AG and both RS forms,
+    so an all-fused step is graph-capturable; OWNER_FUSED = "none" restores the
+    NCCL ring for near-single-owner units at N >= 4 only."""
+    from paper_2411_01075_b200 import hetstep as K
+    from paper_2411_01075_b200.configs import build_job
+    from paper_2411_01075_b200.layout import RankLayout
+    for name in ("gpt2_small", "bert_large", "llama_1b3"):
+        job = build_job(name, n, measured=True)
+        lay = RankLayout.from_plan(job.plan, job.arch.unit_params, job.arch.root_params, 0)
+        for c in lay.counts:
+            for op in ("ag", "rs", "rs16"):
+                assert K.route_collective(op, c, n, True) == "symm", (name, n, op, c)
+                assert K.route_collective(op, c, n, False) == "nccl"
+        monkeypatch.setattr(K, "OWNER_FUSED", "none")
+        for c in lay.counts:
+            owner_like = n >= 4 and max(c) >= 0.75 * sum(c)
+            want = "nccl" if owner_like else "symm"
+            assert K.route_collective("ag", c, n, True) == want, (name, n, c)
+            assert K.route_collective("rs16", c, n, True) == want, (name, n, c)
+        monkeypatch.setattr(K, "OWNER_FUSED", "all")
+
+
+def test_device_epoch_bookkeeping(monkeypatch):
+    """SymmWorkspace device-epoch mode (the multi-rank CUDA graph), host side:
+    inside a capture each launch passes EPOCH_DEVICE | its offset from the
+    capture start, end_device_epochs queues one base advance per channel by the
+    step's launch count, restores the host counters (the capture ran nothing)
+    and returns those deltas; advance_host after each replay keeps the host
+    counters equal to the device bases."""
+    from paper_2411_01075_b200 import hetstep as K
+    calls = []
+
+    class Lib:
+        def het_symm_epoch_set(self, desc, ch, v, st):
+            calls.append(("set", ch, v))
+            return 0
+
+        def het_symm_epoch_add(self, desc, ch, d, st):
+            calls.append(("add", ch, d))
+            return 0
+
+    monkeypatch.setattr(K, "load", lambda: Lib())
+    monkeypatch.setattr(K, "_stream", lambda st: 0)      # no CUDA here
+    ws = K.SymmWorkspace.__new__(K.SymmWorkspace)
+    ws.desc, ws.epoch, ws._dev_epoch0 = K.HetSymm(), [7, 11], None
+    assert ws._next_epoch(0) == 8                      # host epochs
+    ws.begin_device_epochs(None)
+    assert calls == [("set", 0, 8), ("set", 1, 11)]
+    got = [ws._next_epoch(0), ws._next_epoch(1), ws._next_epoch(1), ws._next_epoch(0)]
+    assert got == [K.EPOCH_DEVICE | 1, K.EPOCH_DEVICE | 1, K.EPOCH_DEVICE | 2,
+                   K.EPOCH_DEVICE | 2]
+    deltas = ws.end_device_epochs(None)
+    assert deltas == [2, 2] and calls[-2:] == [("add", 0, 2), ("add", 1, 2)]
+    assert ws.epoch == [8, 11] and ws._dev_epoch0 is None
+    for _ in range(3):                                 # three replays
+        ws.advance_host(deltas)
+    assert ws.epoch == [14, 17]
+    assert ws._next_epoch(1) == 18                     # an eager call continues the sequence
+    with pytest.raises(K.InputError):
+        ws.end_device_epochs(None)
