@@ -1220,7 +1220,11 @@ class SymmWorkspace:
     """One allocation with the same layout on every rank (torch symmetric
     memory = plumbing: allocation, peer mapping, NVLS multicast binding),
     carved into named typed regions plus the barrier signal area. The fused
-    kernels address regions by byte offset from the peer / multicast bases."""
+    kernels address regions by byte offset from the peer / multicast bases.
+    Barrier epochs come from the host counters `epoch[channel]`, or, between
+    begin_device_epochs and end_device_epochs (a CUDA-graph capture of the
+    step), from a per-channel base in this rank's signal area plus the
+    launch's offset (HET_SYMM_EPOCH_DEVICE)."""
 
     def __init__(self, regions: Sequence[tuple[str, int, torch.dtype]], group_name: str,
                  device: torch.device, rank: int, nranks: int, ctas: int = 128,
