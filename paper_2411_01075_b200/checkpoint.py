@@ -130,7 +130,6 @@ def save_trainer(trainer, path: str | Path) -> None:
 def load_trainer(trainer, path: str | Path) -> int:
     """Resume an UnevenFSDPTrainer from a checkpoint written under any plan of
     the same model; refreshes the bf16 shadow. Returns the step count."""
-    from . import hetstep as K  # noqa: F401  (kernel path for the shadow refresh)
     parts, step = load_shards(path, trainer.L)
     for name in STATE:
         buf = getattr(trainer, name)

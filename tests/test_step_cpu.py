@@ -2,7 +2,6 @@
 plumbing and the Eq. 1 weighting, with the CUDA kernels replaced by the
 oracle-backed test double (tests/fake_kernels.py). N=1 here; world_size 2
 over gloo in tests/test_multirank_cpu.py."""
-import numpy as np
 import pytest
 import torch
 
